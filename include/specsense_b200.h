@@ -1,0 +1,179 @@
+/*
+ * specsense_b200.h -- the C-ABI drop-in boundary of the B200 spectrum-sensing
+ * hot path (plain pointers and sizes; no C++ or torch types cross it).
+ *
+ * The reference exposes the path as C++ free functions in the static library
+ * `specsense` (proj/src/CMakeLists.txt:1-13); there is no FFI.  Each entry
+ * point below replaces one of those functions (file:line cited); the C++
+ * drop-in library (include/specsense/*.hpp, implemented over this ABI in
+ * paper_2603_20481_b200/csrc/dropin.cpp) keeps the reference's signatures and
+ * exception types, so callers relink instead of rewriting.
+ *
+ * Memory: unless stated otherwise every array argument is DEVICE memory on the
+ * context's GPU, owned by the caller.  ss_sense_batch also accepts HOST
+ * buffers (pinned or pageable) and stages them itself.  Work is enqueued on
+ * the context's stream (ss_set_stream); functions that return counts or
+ * validate data-dependent results synchronise that stream.
+ *
+ * Errors: functions return an ss_status; ss_last_error(ctx) holds the
+ * message.  Status codes map one-to-one onto the reference's exception types
+ * (proj/include/specsense/types.hpp:43-70): SS_EVALIDATION -> ValidationError,
+ * SS_EFORMAT -> FormatError; SS_ECUDA / SS_ENOMEM / SS_EUNSUPPORTED /
+ * SS_ECAPACITY -> specsense::Error.  There is no CPU fallback: without a
+ * usable sm_100 device ss_open fails with SS_ECUDA.
+ */
+#ifndef SPECSENSE_B200_H
+#define SPECSENSE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SS_ABI_VERSION 1
+
+typedef enum {
+    SS_OK = 0,
+    SS_EVALIDATION = 1, /* bad sizes / config / ranges (ValidationError) */
+    SS_EFORMAT = 2,     /* malformed payloads (FormatError) */
+    SS_ECUDA = 3,       /* CUDA runtime failure or no device */
+    SS_ENOMEM = 4,      /* device allocation failed */
+    SS_EUNSUPPORTED = 5,/* valid for the reference, not supported on device (e.g. n_fft > 8192) */
+    SS_ECAPACITY = 6    /* caller-provided output capacity too small */
+} ss_status;
+
+typedef enum { SS_FMT_F32 = 0, SS_FMT_I16 = 1 } ss_fmt; /* frontend.hpp:134 SampleFormat */
+
+typedef enum { SS_ERODE = 0, SS_DILATE = 1, SS_OPEN = 2, SS_CLOSE = 3 } ss_morph_op; /* detector.hpp:54 */
+
+typedef struct ss_ctx ss_ctx;
+
+/* DetectorConfig (proj/include/specsense/detector.hpp:11-23), same defaults. */
+typedef struct {
+    int savgol_window;            /* 31 */
+    int savgol_order;             /* 3 */
+    double psd_margin_db;         /* 3.0 */
+    int min_component_area;       /* 4 */
+    int one_d_opening_along_time; /* 0 */
+} ss_detector_cfg;
+
+/* BoundingBox (types.hpp:17-26): half-open [t0,t1) x [f0,f1), seconds x Hz. */
+typedef struct {
+    double f0_hz, f1_hz, t0_s, t1_s;
+} ss_box;
+
+/* BinBox (types.hpp:30-39): half-open bin ranges. */
+typedef struct {
+    int32_t t0, t1, f0, f1;
+} ss_bin_box;
+
+/* ComponentExtent (detector.hpp:118-122): inclusive extents + pixel area. */
+typedef struct {
+    int64_t min_t, max_t, min_f, max_f, area;
+} ss_extent;
+
+/* Per-plot outputs of the fused pipeline (Detections, detector.hpp:159-164).
+   Arrays are caller-owned; any pointer may be NULL to skip that output.
+   Shapes for a batch of P plots with F columns and box capacity K:
+     psd_raw, psd_smoothed : P x F floats       floor_thr : P x 2 (floor, threshold)
+     active                : P x F ints (first n_active[p] valid)   n_active : P
+     boxes                 : P x K ss_box       bin_boxes : P x K ss_bin_box
+     n_boxes               : P (true count; > K means the record arrays overflowed)
+   Memory kind follows the batch call: device for ss_detect_batch; host or
+   device (auto-detected per pointer) for ss_sense_batch. */
+typedef struct {
+    float* psd_raw;
+    float* psd_smoothed;
+    float* floor_thr;
+    int32_t* active;
+    int32_t* n_active;
+    ss_box* boxes;
+    ss_bin_box* bin_boxes;
+    int32_t* n_boxes;
+    int32_t box_capacity; /* K */
+} ss_batch_out;
+
+/* ---- context ---------------------------------------------------------- */
+ss_status ss_open(int device, ss_ctx** out);
+void ss_close(ss_ctx* ctx);
+const char* ss_last_error(const ss_ctx* ctx);
+int ss_abi_version(void);
+void ss_default_detector_cfg(ss_detector_cfg* cfg);
+/* Enqueue subsequent work on `stream` (a cudaStream_t; NULL = the context's own). */
+ss_status ss_set_stream(ss_ctx* ctx, void* stream);
+ss_status ss_synchronize(ss_ctx* ctx);
+/* Device kernel launches issued by this context so far (instrumentation). */
+int64_t ss_launch_count(const ss_ctx* ctx);
+
+/* ---- frontend --------------------------------------------------------- */
+/* frontend::make_plot / make_plots (frontend.cpp:157-183) over n_plots
+   consecutive plots of `rows` rows: iq holds n_plots*rows*n_fft samples
+   (interleaved I,Q; 16-byte aligned), tf receives n_plots*rows*n_fft floats,
+   row r column k = |X_r[(k + n_fft/2) mod n_fft]| (frontend.cpp:127-149).
+   n_fft: power of two, 8 <= n_fft <= 8192 on device (reference: any power of
+   two >= 8, frontend.cpp:37-42; larger sizes -> SS_EUNSUPPORTED). */
+ss_status ss_tf_plots(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int rows, int n_plots,
+                      float* tf);
+
+/* ---- detector stages (one plot unless noted) --------------------------- */
+/* estimate_psd_into (detector.cpp:170-184): out[k - c0] for k in [c0, c1). */
+ss_status ss_psd_cols(ss_ctx* ctx, const float* tf, int rows, int cols, int c0, int c1, float* out);
+/* savgol_smooth (detector.cpp:192-208). */
+ss_status ss_savgol_smooth(ss_ctx* ctx, const float* values, int n, int window, int order,
+                           float* out);
+/* smooth_and_floor + prune_columns (detector.cpp:210-255) for one PSD row:
+   smoothed[n], floor_thr[2] = {noise_floor, threshold}, active[<= n],
+   *n_active (HOST int). */
+ss_status ss_floor(ss_ctx* ctx, const float* raw, int n, const ss_detector_cfg* cfg,
+                   float* smoothed, float* floor_thr, int32_t* active, int32_t* n_active);
+/* otsu_threshold (detector.cpp:257-271); *valid, *threshold are HOST. */
+ss_status ss_otsu(ss_ctx* ctx, const float* values, int n, int32_t* valid, float* threshold);
+/* binarize_columns (detector.cpp:273-335): writes columns [c0, c1) of the
+   rows x cols byte mask; active_host is a HOST array of plot-wide indices. */
+ss_status ss_binarize_cols(ss_ctx* ctx, const float* tf, int rows, int cols,
+                           const int32_t* active_host, int n_active, int c0, int c1,
+                           uint8_t* mask);
+/* morphology_cols (detector.cpp:441-472) on byte masks; dst must not alias src. */
+ss_status ss_morph_cols(ss_ctx* ctx, const uint8_t* src, int rows, int cols, ss_morph_op op,
+                        int se_rows, int se_cols, int c0, int c1, uint8_t* dst);
+/* consolidate (detector.cpp:482-492) on byte masks. */
+ss_status ss_consolidate(ss_ctx* ctx, const uint8_t* src, int rows, int cols, int along_time,
+                         uint8_t* dst);
+/* label_components / component_extents (detector.cpp:598-620): extents
+   (HOST, capacity cap) in first-pixel order; labels (DEVICE rows x cols int32,
+   0 = background) may be NULL; *n_out (HOST) = component count. */
+ss_status ss_components(ss_ctx* ctx, const uint8_t* mask, int rows, int cols, int min_area,
+                        int32_t* labels, ss_extent* extents_host, int64_t cap, int64_t* n_out);
+
+/* ---- fused batch pipelines -------------------------------------------- */
+/* detect (detector.cpp:637-670) on n_plots plot-major TF plots already in
+   device memory; plot p's start_seq = start_seq[p] (HOST array, may be NULL
+   = all 0).  Outputs in DEVICE memory. */
+ss_status ss_detect_batch(ss_ctx* ctx, const float* tf, int n_plots, int rows, int cols,
+                          const uint64_t* start_seq, double sample_rate_hz,
+                          const ss_detector_cfg* cfg, const ss_batch_out* out);
+
+/* IQ -> boxes for n_plots consecutive windows (make_plots + detect per
+   window, i.e. the runtime's per-plot work, runtime.cpp:324-445): plot p
+   covers samples [p*rows*n_fft, (p+1)*rows*n_fft) with start_seq =
+   first_seq + p*rows.  iq may be host or device memory; tf_out (DEVICE,
+   n_plots*rows*n_fft floats) may be NULL when the TF plots are not wanted
+   (they are still produced in the context's workspace). */
+ss_status ss_sense_batch(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int rows, int n_plots,
+                         uint64_t first_seq, double sample_rate_hz, const ss_detector_cfg* cfg,
+                         float* tf_out, const ss_batch_out* out);
+
+/* ---- test hooks -------------------------------------------------------- */
+/* Device ports of glibc log10f (which=0) / powf(10, x) (which=1) over n
+   DEVICE floats; variant: 1 FMA build, 0 SSE2 build, -1 host-matched. */
+ss_status ss_test_libm(ss_ctx* ctx, const float* x, int64_t n, int which, int variant, float* out);
+/* SSFFT-1 per-pass twiddle table for n_fft (HOST out, ss_fft_twiddle_count doubles2). */
+int64_t ss_fft_twiddle_count(int n_fft);
+ss_status ss_fft_twiddles(int n_fft, double* out_re_im);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECSENSE_B200_H */

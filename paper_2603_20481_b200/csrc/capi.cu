@@ -1,0 +1,709 @@
+// capi.cu -- the extern "C" boundary (include/specsense_b200.h): context,
+// device workspace, argument validation with the reference's error
+// semantics, and the fused batch pipelines that chain K1..K6 on one stream.
+#include "../../include/specsense_b200.h"
+#include "internal.h"
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+int ilog2(int n) {
+    int m = 0;
+    while ((1 << m) < n) ++m;
+    return m;
+}
+
+} // namespace
+
+struct ss_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    bool fma_variant = true;
+    std::string err;
+    std::map<int, double2*> tw;                       // per log2(n_fft)
+    std::map<std::pair<int, int>, double*> sg;        // per (window, order)
+    std::map<std::string, DevBuf> ws;                 // grow-only workspace
+    int64_t launches = 0;
+};
+
+namespace {
+
+ss_status fail(ss_ctx* c, ss_status s, const std::string& msg) {
+    if (c) c->err = msg;
+    return s;
+}
+
+ss_status cuda_fail(ss_ctx* c, cudaError_t e, const char* where) {
+    return fail(c, SS_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define SS_CK(ctx, expr)                                           \
+    do {                                                           \
+        cudaError_t e_ = (expr);                                   \
+        if (e_ != cudaSuccess) return cuda_fail((ctx), e_, #expr); \
+    } while (0)
+
+template <typename T>
+T* wsbuf(ss_ctx* c, const char* name, size_t count, ss_status* st) {
+    DevBuf& b = c->ws[name];
+    const size_t need = sizeof(T) * (count ? count : 1);
+    if (b.bytes < need) {
+        if (b.p) {
+            cudaStreamSynchronize(c->stream);
+            cudaFree(b.p);
+            b.p = nullptr;
+            b.bytes = 0;
+        }
+        const size_t alloc = need + need / 8;
+        if (cudaMalloc(&b.p, alloc) != cudaSuccess) {
+            cudaGetLastError();
+            *st = fail(c, SS_ENOMEM, std::string("device allocation failed: ") + name);
+            return nullptr;
+        }
+        b.bytes = alloc;
+    }
+    return static_cast<T*>(b.p);
+}
+
+#define SS_WS(var, T, name, count)                    \
+    T* var = nullptr;                                 \
+    do {                                              \
+        ss_status st_ = SS_OK;                        \
+        var = wsbuf<T>(ctx, name, (count), &st_);     \
+        if (!var) return st_;                         \
+    } while (0)
+
+ss_status twiddles(ss_ctx* ctx, int n_fft, const double2** out) {
+    const int lg = ilog2(n_fft);
+    auto it = ctx->tw.find(lg);
+    if (it == ctx->tw.end()) {
+        std::vector<double2> host;
+        ssb::fft_twiddles(lg, host);
+        double2* d = nullptr;
+        SS_CK(ctx, cudaMalloc(&d, sizeof(double2) * host.size()));
+        SS_CK(ctx, cudaMemcpy(d, host.data(), sizeof(double2) * host.size(), cudaMemcpyHostToDevice));
+        it = ctx->tw.emplace(lg, d).first;
+    }
+    *out = it->second;
+    return SS_OK;
+}
+
+ss_status check_savgol(ss_ctx* ctx, int window, int order) {
+    // detector.cpp:144-149
+    if (window < 5 || window % 2 == 0) return fail(ctx, SS_EVALIDATION, "savgol window must be odd and >= 5");
+    if (order < 1 || order >= window) return fail(ctx, SS_EVALIDATION, "savgol order must be in [1, window)");
+    return SS_OK;
+}
+
+ss_status weights(ss_ctx* ctx, int window, int order, const double** out) {
+    ss_status s = check_savgol(ctx, window, order);
+    if (s != SS_OK) return s;
+    auto key = std::make_pair(window, order);
+    auto it = ctx->sg.find(key);
+    if (it == ctx->sg.end()) {
+        std::vector<double> w;
+        if (!ssb::savgol_weights_host(window, order, w))
+            return fail(ctx, SS_EVALIDATION, "savgol normal equations are singular");
+        double* d = nullptr;
+        SS_CK(ctx, cudaMalloc(&d, sizeof(double) * w.size()));
+        SS_CK(ctx, cudaMemcpy(d, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice));
+        it = ctx->sg.emplace(key, d).first;
+    }
+    *out = it->second;
+    return SS_OK;
+}
+
+// DetectorConfig::validate (detector.cpp:153-159)
+ss_status check_cfg(ss_ctx* ctx, const ss_detector_cfg& c, int n_cols) {
+    ss_status s = check_savgol(ctx, c.savgol_window, c.savgol_order);
+    if (s != SS_OK) return s;
+    if (c.savgol_window > n_cols)
+        return fail(ctx, SS_EVALIDATION, "savgol window exceeds the number of frequency bins");
+    if (c.psd_margin_db < 0.0) return fail(ctx, SS_EVALIDATION, "psd_margin_db must be non-negative");
+    if (c.min_component_area < 1) return fail(ctx, SS_EVALIDATION, "min_component_area must be >= 1");
+    return SS_OK;
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// CCL over n_plots bit masks with a pool of pool_cap runs; fills the workspace
+// pointers and launches.
+ss_status run_ccl(ss_ctx* ctx, const uint32_t* bits, int n_plots, int rows, int cols, int min_area,
+                  long long pool_cap, int* n_comp, long long cap, long long* extents, int* bin_boxes,
+                  double* boxes, const unsigned long long* start_seq, double fs, int32_t* labels,
+                  int* overflow_host) {
+    ssb::CclLaunch L;
+    L.bits = bits;
+    L.n_plots = n_plots;
+    L.rows = rows;
+    L.cols = cols;
+    L.min_area = min_area;
+    L.n_comp = n_comp;
+    L.cap = cap;
+    L.extents = extents;
+    L.bin_boxes = bin_boxes;
+    L.boxes = boxes;
+    L.start_seq = start_seq;
+    L.fs = fs;
+    L.labels = labels;
+    ssb::CclWorkspace& w = L.ws;
+    SS_WS(rr, int, "ccl.row_runs", static_cast<size_t>(n_plots) * rows);
+    SS_WS(ro, int, "ccl.row_off", static_cast<size_t>(n_plots) * (rows + 1));
+    SS_WS(pb, long long, "ccl.plot_base", n_plots);
+    SS_WS(pok, int, "ccl.plot_ok", n_plots);
+    SS_WS(of, int, "ccl.overflow", 1);
+    SS_WS(rb, int, "ccl.run_begin", pool_cap);
+    SS_WS(re, int, "ccl.run_end", pool_cap);
+    SS_WS(rw, int, "ccl.run_row", pool_cap);
+    SS_WS(pa, int, "ccl.parent", pool_cap);
+    SS_WS(ar, unsigned long long, "ccl.area", pool_cap);
+    SS_WS(mnf, int, "ccl.min_f", pool_cap);
+    SS_WS(mxf, int, "ccl.max_f", pool_cap);
+    SS_WS(mxt, int, "ccl.max_t", pool_cap);
+    SS_WS(dn, int, "ccl.dense", pool_cap);
+    w.row_runs = rr;
+    w.row_off = ro;
+    w.plot_base = pb;
+    w.plot_ok = pok;
+    w.overflow = of;
+    w.run_begin = rb;
+    w.run_end = re;
+    w.run_row = rw;
+    w.parent = pa;
+    w.area = ar;
+    w.min_f = mnf;
+    w.max_f = mxf;
+    w.max_t = mxt;
+    w.dense = dn;
+    w.pool_cap = pool_cap;
+    SS_CK(ctx, ssb::ccl_launch(L, ctx->stream));
+    ctx->launches += 7 + (rows > 1 ? 1 : 0) + (labels ? 1 : 0);
+    if (overflow_host) SS_CK(ctx, cudaMemcpyAsync(overflow_host, of, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    return SS_OK;
+}
+
+long long default_pool(int n_plots, int rows, int cols) {
+    const long long per_row = std::min<long long>((cols + 1) / 2, 32);
+    return static_cast<long long>(n_plots) * rows * per_row + 1024;
+}
+
+long long worst_pool(int rows, int cols) { return static_cast<long long>(rows) * ((cols + 1) / 2) + 16; }
+
+// Stages 2..6 on TF plots resident in device memory.  psd_ready: raw PSD
+// already in psd (fused into K1); else computed here.
+ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int cols,
+                        const unsigned long long* seq_dev, double fs, const ss_detector_cfg& cfg,
+                        float* psd, bool psd_ready, const ss_batch_out& out_dev) {
+    const int W = (cols + 31) / 32;
+    const double* wts = nullptr;
+    ss_status s = weights(ctx, cfg.savgol_window, cfg.savgol_order, &wts);
+    if (s != SS_OK) return s;
+    if (!psd_ready) {
+        SS_CK(ctx, ssb::psd_cols_launch(tf, n_plots, rows, cols, 0, cols, psd, ctx->stream));
+        ctx->launches += 1;
+    }
+    SS_WS(sm, float, "det.smoothed", static_cast<size_t>(n_plots) * cols);
+    SS_WS(ft, float, "det.floor_thr", static_cast<size_t>(n_plots) * 2);
+    SS_WS(act, int, "det.active", static_cast<size_t>(n_plots) * cols);
+    SS_WS(nact, int, "det.n_active", n_plots);
+    SS_WS(abits, uint32_t, "det.active_bits", static_cast<size_t>(n_plots) * W);
+    SS_WS(m0, uint32_t, "det.mask0", static_cast<size_t>(n_plots) * rows * W);
+    SS_WS(m1, uint32_t, "det.mask1", static_cast<size_t>(n_plots) * rows * W);
+    ssb::FloorLaunch F;
+    F.raw = psd;
+    F.n_plots = n_plots;
+    F.n = cols;
+    F.window = cfg.savgol_window;
+    F.weights = wts;
+    F.pow10_margin = std::pow(10.0, cfg.psd_margin_db / 10.0);  // detector.cpp:247 (host libm)
+    F.fma_variant = ctx->fma_variant;
+    F.smoothed = out_dev.psd_smoothed ? out_dev.psd_smoothed : sm;
+    F.floor_thr = out_dev.floor_thr ? out_dev.floor_thr : ft;
+    F.active = out_dev.active ? out_dev.active : act;
+    F.n_active = out_dev.n_active ? out_dev.n_active : nact;
+    F.active_bits = abits;
+    SS_CK(ctx, ssb::floor_launch(F, ctx->stream));
+    ssb::BinarizeLaunch B;
+    B.tf = tf;
+    B.n_plots = n_plots;
+    B.rows = rows;
+    B.cols = cols;
+    B.active_bits = abits;
+    B.mask_bits = m0;
+    SS_CK(ctx, ssb::binarize_launch(B, ctx->stream));
+    SS_CK(ctx, ssb::consolidate_bits_launch(m0, n_plots, rows, cols, cfg.one_d_opening_along_time != 0, m1,
+                                            ctx->stream));
+    ctx->launches += 3;
+    const long long cap = out_dev.box_capacity > 0 ? out_dev.box_capacity : 0;
+    SS_WS(ncomp, int, "det.n_comp", n_plots);
+    int* overflow_h = nullptr;
+    SS_CK(ctx, cudaMallocHost(&overflow_h, sizeof(int)));
+    s = run_ccl(ctx, m1, n_plots, rows, cols, cfg.min_component_area, default_pool(n_plots, rows, cols),
+                out_dev.n_boxes ? out_dev.n_boxes : ncomp, cap, nullptr,
+                reinterpret_cast<int*>(out_dev.bin_boxes), reinterpret_cast<double*>(out_dev.boxes), seq_dev, fs,
+                nullptr, overflow_h);
+    if (s != SS_OK) {
+        cudaFreeHost(overflow_h);
+        return s;
+    }
+    SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    const int overflow = *overflow_h;
+    cudaFreeHost(overflow_h);
+    if (overflow) {
+        // rare: some plot had more runs than the shared pool; redo every plot
+        // alone with its exact worst-case pool
+        int* nb = out_dev.n_boxes ? out_dev.n_boxes : ncomp;
+        for (int p = 0; p < n_plots; ++p) {
+            const size_t mo = static_cast<size_t>(p) * rows * W;
+            s = run_ccl(ctx, m1 + mo, 1, rows, cols, cfg.min_component_area, worst_pool(rows, cols), nb + p, cap,
+                        nullptr, out_dev.bin_boxes ? reinterpret_cast<int*>(out_dev.bin_boxes) + 4 * cap * p : nullptr,
+                        out_dev.boxes ? reinterpret_cast<double*>(out_dev.boxes) + 4 * cap * p : nullptr,
+                        seq_dev ? seq_dev + p : nullptr, fs, nullptr, nullptr);
+            if (s != SS_OK) return s;
+        }
+        SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    return SS_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+int ss_abi_version(void) { return SS_ABI_VERSION; }
+
+void ss_default_detector_cfg(ss_detector_cfg* cfg) {
+    if (!cfg) return;
+    cfg->savgol_window = 31;
+    cfg->savgol_order = 3;
+    cfg->psd_margin_db = 3.0;
+    cfg->min_component_area = 4;
+    cfg->one_d_opening_along_time = 0;
+}
+
+ss_status ss_open(int device, ss_ctx** out) {
+    if (!out) return SS_EVALIDATION;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device || device < 0) {
+        cudaGetLastError();
+        return SS_ECUDA;
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major < 10) return SS_EUNSUPPORTED;
+    if (cudaSetDevice(device) != cudaSuccess) return SS_ECUDA;
+    ss_ctx* c = new ss_ctx();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    c->fma_variant = ssb::host_has_fma_avx2();
+    if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        return SS_ECUDA;
+    }
+    c->stream = c->own;
+    *out = c;
+    return SS_OK;
+}
+
+void ss_close(ss_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& kv : ctx->tw) cudaFree(kv.second);
+    for (auto& kv : ctx->sg) cudaFree(kv.second);
+    for (auto& kv : ctx->ws) cudaFree(kv.second.p);
+    cudaStreamDestroy(ctx->own);
+    delete ctx;
+}
+
+const char* ss_last_error(const ss_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+ss_status ss_set_stream(ss_ctx* ctx, void* stream) {
+    if (!ctx) return SS_EVALIDATION;
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+    return SS_OK;
+}
+
+ss_status ss_synchronize(ss_ctx* ctx) {
+    if (!ctx) return SS_EVALIDATION;
+    SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    return SS_OK;
+}
+
+int64_t ss_launch_count(const ss_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+ss_status ss_tf_plots(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int rows, int n_plots, float* tf) {
+    if (!ctx) return SS_EVALIDATION;
+    if (n_fft < 8 || !is_pow2(n_fft))
+        return fail(ctx, SS_EVALIDATION, "FFT size must be a power of two >= 8, got " + std::to_string(n_fft));
+    if (n_fft > 8192) return fail(ctx, SS_EUNSUPPORTED, "device FFT supports n_fft <= 8192");
+    if (rows < 0 || n_plots < 0) return fail(ctx, SS_EVALIDATION, "negative plot geometry");
+    if (fmt != SS_FMT_F32 && fmt != SS_FMT_I16) return fail(ctx, SS_EVALIDATION, "unknown sample format");
+    if (static_cast<long long>(rows) * n_plots == 0) return SS_OK;
+    if (reinterpret_cast<uintptr_t>(iq) % 16 != 0) return fail(ctx, SS_EVALIDATION, "IQ buffer must be 16-byte aligned");
+    const double2* tw = nullptr;
+    ss_status s = twiddles(ctx, n_fft, &tw);
+    if (s != SS_OK) return s;
+    ssb::FftLaunch L;
+    L.logn = ilog2(n_fft);
+    L.fmt = fmt;
+    L.psd = false;
+    L.iq = iq;
+    L.tf = tf;
+    L.tw = tw;
+    L.total_rows = static_cast<long long>(rows) * n_plots;
+    L.rows_per_plot = rows;
+    L.n_plots = n_plots;
+    L.num_sms = ctx->num_sms;
+    SS_CK(ctx, ssb::fft_mag_launch(L, ctx->stream));
+    ctx->launches += 1;
+    return SS_OK;
+}
+
+ss_status ss_psd_cols(ss_ctx* ctx, const float* tf, int rows, int cols, int c0, int c1, float* out) {
+    if (!ctx) return SS_EVALIDATION;
+    if (rows < 1 || cols < 1) return fail(ctx, SS_EVALIDATION, "empty TF plot");
+    if (c0 < 0 || c1 > cols || c0 >= c1) return fail(ctx, SS_EVALIDATION, "PSD column range out of bounds");
+    SS_CK(ctx, ssb::psd_cols_launch(tf, 1, rows, cols, c0, c1, out, ctx->stream));
+    ctx->launches += 1;
+    return SS_OK;
+}
+
+ss_status ss_savgol_smooth(ss_ctx* ctx, const float* values, int n, int window, int order, float* out) {
+    if (!ctx) return SS_EVALIDATION;
+    const double* w = nullptr;
+    ss_status s = check_savgol(ctx, window, order);
+    if (s != SS_OK) return s;
+    if (n < window) return fail(ctx, SS_EVALIDATION, "savgol window exceeds the input length");
+    s = weights(ctx, window, order, &w);
+    if (s != SS_OK) return s;
+    SS_CK(ctx, ssb::savgol_launch(values, n, window, w, out, ctx->stream));
+    ctx->launches += 1;
+    return SS_OK;
+}
+
+ss_status ss_floor(ss_ctx* ctx, const float* raw, int n, const ss_detector_cfg* cfg, float* smoothed,
+                   float* floor_thr, int32_t* active, int32_t* n_active) {
+    if (!ctx || !cfg) return SS_EVALIDATION;
+    ss_status s = check_savgol(ctx, cfg->savgol_window, cfg->savgol_order);
+    if (s != SS_OK) return s;
+    if (n < cfg->savgol_window) return fail(ctx, SS_EVALIDATION, "savgol window exceeds the input length");
+    const double* w = nullptr;
+    s = weights(ctx, cfg->savgol_window, cfg->savgol_order, &w);
+    if (s != SS_OK) return s;
+    SS_WS(nact, int, "floor.n_active", 1);
+    ssb::FloorLaunch F;
+    F.raw = raw;
+    F.n_plots = 1;
+    F.n = n;
+    F.window = cfg->savgol_window;
+    F.weights = w;
+    F.pow10_margin = std::pow(10.0, cfg->psd_margin_db / 10.0);
+    F.fma_variant = ctx->fma_variant;
+    F.smoothed = smoothed;
+    F.floor_thr = floor_thr;
+    F.active = active;
+    F.n_active = nact;
+    SS_CK(ctx, ssb::floor_launch(F, ctx->stream));
+    ctx->launches += 1;
+    int h = 0;
+    SS_CK(ctx, cudaMemcpyAsync(&h, nact, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (n_active) *n_active = h;
+    return SS_OK;
+}
+
+ss_status ss_otsu(ss_ctx* ctx, const float* values, int n, int32_t* valid, float* threshold) {
+    if (!ctx) return SS_EVALIDATION;
+    if (n < 1) return fail(ctx, SS_EVALIDATION, "otsu on an empty column");
+    SS_WS(bits, uint32_t, "otsu.bits", 1);
+    SS_WS(thr, float, "otsu.thr", 1);
+    SS_WS(val, int, "otsu.valid", 1);
+    const uint32_t one = 1u;
+    SS_CK(ctx, cudaMemcpyAsync(bits, &one, sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream));
+    ssb::BinarizeLaunch B;
+    B.tf = values;
+    B.n_plots = 1;
+    B.rows = n;
+    B.cols = 1;
+    B.active_bits = bits;
+    B.col_thr = thr;
+    B.col_valid = val;
+    SS_CK(ctx, ssb::binarize_launch(B, ctx->stream));
+    ctx->launches += 1;
+    float t = 0.0f;
+    int v = 0;
+    SS_CK(ctx, cudaMemcpyAsync(&t, thr, sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    SS_CK(ctx, cudaMemcpyAsync(&v, val, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (valid) *valid = v;
+    if (threshold) *threshold = v ? t : 0.0f;
+    return SS_OK;
+}
+
+ss_status ss_binarize_cols(ss_ctx* ctx, const float* tf, int rows, int cols, const int32_t* active_host,
+                           int n_active, int c0, int c1, uint8_t* mask) {
+    if (!ctx) return SS_EVALIDATION;
+    if (rows < 0 || cols < 0) return fail(ctx, SS_EVALIDATION, "binarize output mask shape mismatch");
+    if (c0 < 0 || c1 > cols || c0 > c1) return fail(ctx, SS_EVALIDATION, "binarize column range out of bounds");
+    if (c1 == c0) return SS_OK;
+    const int W = (cols + 31) / 32;
+    std::vector<uint32_t> bits(static_cast<size_t>(W), 0u);
+    for (int i = 0; i < n_active; ++i) {
+        const int k = active_host[i];
+        if (k < 0 || k >= cols) return fail(ctx, SS_EVALIDATION, "active column index out of range");
+        bits[static_cast<size_t>(k >> 5)] |= 1u << (k & 31);
+    }
+    if (rows == 0) return SS_OK;
+    SS_WS(dbits, uint32_t, "bin.bits", W);
+    SS_CK(ctx, cudaMemcpyAsync(dbits, bits.data(), sizeof(uint32_t) * W, cudaMemcpyHostToDevice, ctx->stream));
+    ssb::BinarizeLaunch B;
+    B.tf = tf;
+    B.n_plots = 1;
+    B.rows = rows;
+    B.cols = cols;
+    B.active_bits = dbits;
+    B.mask_u8 = mask;
+    B.c0 = c0;
+    B.c1 = c1;
+    SS_CK(ctx, ssb::binarize_launch(B, ctx->stream));
+    ctx->launches += 1;
+    // the bit vector lives on the host stack: finish before returning
+    SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    return SS_OK;
+}
+
+ss_status ss_morph_cols(ss_ctx* ctx, const uint8_t* src, int rows, int cols, ss_morph_op op, int se_rows,
+                        int se_cols, int c0, int c1, uint8_t* dst) {
+    if (!ctx) return SS_EVALIDATION;
+    // check_se (detector.cpp:345-349), morphology_cols range checks (:443-447)
+    if (se_rows < 1 || se_cols < 1 || se_rows % 2 == 0 || se_cols % 2 == 0)
+        return fail(ctx, SS_EVALIDATION, "structuring element dimensions must be odd and >= 1");
+    if (rows < 1 || cols < 1) return fail(ctx, SS_EVALIDATION, "empty mask");
+    if (c0 < 0 || c1 > cols || c0 > c1) return fail(ctx, SS_EVALIDATION, "morphology column range out of bounds");
+    if (op < SS_ERODE || op > SS_CLOSE) return fail(ctx, SS_EVALIDATION, "unknown morphology op");
+    if (src == dst) return fail(ctx, SS_EVALIDATION, "morphology dst must not alias src");
+    SS_WS(tmp, uint8_t, "morph.tmp", static_cast<size_t>(rows) * cols);
+    SS_CK(ctx, ssb::morph_u8_launch(src, rows, cols, op, se_rows, se_cols, c0, c1, tmp, dst, ctx->stream));
+    ctx->launches += (op >= SS_OPEN) ? 2 : 1;
+    return SS_OK;
+}
+
+ss_status ss_consolidate(ss_ctx* ctx, const uint8_t* src, int rows, int cols, int along_time, uint8_t* dst) {
+    if (!ctx) return SS_EVALIDATION;
+    if (rows < 1 || cols < 1) return fail(ctx, SS_EVALIDATION, "empty mask");
+    const int W = (cols + 31) / 32;
+    SS_WS(a, uint32_t, "cons.a", static_cast<size_t>(rows) * W);
+    SS_WS(b, uint32_t, "cons.b", static_cast<size_t>(rows) * W);
+    SS_CK(ctx, ssb::pack_u8_launch(src, 1, rows, cols, a, ctx->stream));
+    SS_CK(ctx, ssb::consolidate_bits_launch(a, 1, rows, cols, along_time != 0, b, ctx->stream));
+    SS_CK(ctx, ssb::unpack_launch(b, 1, rows, cols, dst, ctx->stream));
+    ctx->launches += 3;
+    return SS_OK;
+}
+
+ss_status ss_components(ss_ctx* ctx, const uint8_t* mask, int rows, int cols, int min_area, int32_t* labels,
+                        ss_extent* extents_host, int64_t cap, int64_t* n_out) {
+    if (!ctx) return SS_EVALIDATION;
+    if (min_area < 1) return fail(ctx, SS_EVALIDATION, "min_component_area must be >= 1");
+    if (rows < 1 || cols < 1) {
+        if (n_out) *n_out = 0;
+        return SS_OK;
+    }
+    const int W = (cols + 31) / 32;
+    SS_WS(bits, uint32_t, "comp.bits", static_cast<size_t>(rows) * W);
+    SS_WS(ncomp, int, "comp.n", 1);
+    const long long dcap = cap > 0 ? cap : 1;
+    SS_WS(ext, long long, "comp.ext", static_cast<size_t>(5 * dcap));
+    SS_CK(ctx, ssb::pack_u8_launch(mask, 1, rows, cols, bits, ctx->stream));
+    ctx->launches += 1;
+    ss_status s = run_ccl(ctx, bits, 1, rows, cols, min_area, worst_pool(rows, cols), ncomp, dcap, ext, nullptr,
+                          nullptr, nullptr, 1.0, labels, nullptr);
+    if (s != SS_OK) return s;
+    int n = 0;
+    SS_CK(ctx, cudaMemcpyAsync(&n, ncomp, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (n_out) *n_out = n;
+    if (n > cap) return fail(ctx, SS_ECAPACITY, "component capacity too small: " + std::to_string(n));
+    if (n > 0 && extents_host)
+        SS_CK(ctx, cudaMemcpy(extents_host, ext, sizeof(ss_extent) * static_cast<size_t>(n), cudaMemcpyDeviceToHost));
+    return SS_OK;
+}
+
+ss_status ss_detect_batch(ss_ctx* ctx, const float* tf, int n_plots, int rows, int cols, const uint64_t* start_seq,
+                          double sample_rate_hz, const ss_detector_cfg* cfg, const ss_batch_out* out) {
+    if (!ctx || !cfg || !out) return SS_EVALIDATION;
+    ss_status s = check_cfg(ctx, *cfg, cols);
+    if (s != SS_OK) return s;
+    if (rows < 1 || cols < 1 || n_plots < 0) return fail(ctx, SS_EVALIDATION, "empty TF plot");
+    if (!(sample_rate_hz > 0.0)) return fail(ctx, SS_EVALIDATION, "sample_rate_hz must be positive");
+    if (n_plots == 0) return SS_OK;
+    SS_WS(psd, float, "det.psd", static_cast<size_t>(n_plots) * cols);
+    SS_WS(seq, unsigned long long, "det.seq", n_plots);
+    std::vector<unsigned long long> hseq(static_cast<size_t>(n_plots), 0ull);
+    if (start_seq)
+        for (int p = 0; p < n_plots; ++p) hseq[p] = start_seq[p];
+    SS_CK(ctx, cudaMemcpyAsync(seq, hseq.data(), sizeof(unsigned long long) * n_plots, cudaMemcpyHostToDevice,
+                               ctx->stream));
+    float* praw = out->psd_raw ? out->psd_raw : psd;
+    s = detect_device(ctx, tf, n_plots, rows, cols, seq, sample_rate_hz, *cfg, praw, false, *out);
+    if (s != SS_OK) return s;
+    if (out->n_boxes && out->box_capacity >= 0) {
+        std::vector<int> nb(static_cast<size_t>(n_plots));
+        SS_CK(ctx, cudaMemcpy(nb.data(), out->n_boxes, sizeof(int) * n_plots, cudaMemcpyDeviceToHost));
+        for (int v : nb)
+            if (v > out->box_capacity) return fail(ctx, SS_ECAPACITY, "box capacity too small: " + std::to_string(v));
+    }
+    return SS_OK;
+}
+
+ss_status ss_sense_batch(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int rows, int n_plots, uint64_t first_seq,
+                         double sample_rate_hz, const ss_detector_cfg* cfg, float* tf_out, const ss_batch_out* out) {
+    if (!ctx || !cfg || !out) return SS_EVALIDATION;
+    if (n_fft < 8 || !is_pow2(n_fft))
+        return fail(ctx, SS_EVALIDATION, "FFT size must be a power of two >= 8, got " + std::to_string(n_fft));
+    if (n_fft > 8192) return fail(ctx, SS_EUNSUPPORTED, "device FFT supports n_fft <= 8192");
+    if (rows < 1) return fail(ctx, SS_EVALIDATION, "plot_rows must be >= 1");
+    if (!(sample_rate_hz > 0.0)) return fail(ctx, SS_EVALIDATION, "sample_rate_hz must be positive");
+    if (fmt != SS_FMT_F32 && fmt != SS_FMT_I16) return fail(ctx, SS_EVALIDATION, "unknown sample format");
+    ss_status s = check_cfg(ctx, *cfg, n_fft);
+    if (s != SS_OK) return s;
+    if (n_plots <= 0) return SS_OK;
+    const size_t nsamp = static_cast<size_t>(n_plots) * rows * n_fft;
+    const size_t sbytes = fmt == SS_FMT_F32 ? 8 : 4;
+    const void* diq = iq;
+    if (!is_device_ptr(iq) || reinterpret_cast<uintptr_t>(iq) % 16 != 0) {
+        SS_WS(stage, unsigned char, "sense.iq", nsamp * sbytes);
+        SS_CK(ctx, cudaMemcpyAsync(stage, iq, nsamp * sbytes, cudaMemcpyDefault, ctx->stream));
+        diq = stage;
+    }
+    const int cols = n_fft;
+    float* tf = tf_out;
+    if (!tf) {
+        SS_WS(t, float, "sense.tf", nsamp);
+        tf = t;
+    }
+    // outputs: device pointers used directly, host pointers staged
+    ss_batch_out dev = *out;
+    const bool host_out = (out->psd_raw && !is_device_ptr(out->psd_raw)) || (out->boxes && !is_device_ptr(out->boxes)) ||
+                          (out->n_boxes && !is_device_ptr(out->n_boxes)) ||
+                          (out->bin_boxes && !is_device_ptr(out->bin_boxes)) ||
+                          (out->floor_thr && !is_device_ptr(out->floor_thr)) ||
+                          (out->psd_smoothed && !is_device_ptr(out->psd_smoothed)) ||
+                          (out->active && !is_device_ptr(out->active)) ||
+                          (out->n_active && !is_device_ptr(out->n_active));
+    const long long K = out->box_capacity > 0 ? out->box_capacity : 0;
+    if (host_out) {
+        SS_WS(a1, float, "sense.o.raw", static_cast<size_t>(n_plots) * cols);
+        SS_WS(a2, float, "sense.o.sm", static_cast<size_t>(n_plots) * cols);
+        SS_WS(a3, float, "sense.o.ft", static_cast<size_t>(n_plots) * 2);
+        SS_WS(a4, int32_t, "sense.o.act", static_cast<size_t>(n_plots) * cols);
+        SS_WS(a5, int32_t, "sense.o.nact", n_plots);
+        SS_WS(a6, ss_box, "sense.o.box", static_cast<size_t>(n_plots) * (K ? K : 1));
+        SS_WS(a7, ss_bin_box, "sense.o.bbox", static_cast<size_t>(n_plots) * (K ? K : 1));
+        SS_WS(a8, int32_t, "sense.o.nbox", n_plots);
+        dev.psd_raw = a1;
+        dev.psd_smoothed = a2;
+        dev.floor_thr = a3;
+        dev.active = a4;
+        dev.n_active = a5;
+        dev.boxes = a6;
+        dev.bin_boxes = a7;
+        dev.n_boxes = a8;
+    }
+    SS_WS(psd, float, "det.psd", static_cast<size_t>(n_plots) * cols);
+    float* praw = dev.psd_raw ? dev.psd_raw : psd;
+    const double2* tw = nullptr;
+    s = twiddles(ctx, n_fft, &tw);
+    if (s != SS_OK) return s;
+    ssb::FftLaunch L;
+    L.logn = ilog2(n_fft);
+    L.fmt = fmt;
+    L.psd = true;
+    L.iq = diq;
+    L.tf = tf;
+    L.psd_out = praw;
+    L.tw = tw;
+    L.total_rows = static_cast<long long>(rows) * n_plots;
+    L.rows_per_plot = rows;
+    L.n_plots = n_plots;
+    L.num_sms = ctx->num_sms;
+    SS_CK(ctx, ssb::fft_mag_launch(L, ctx->stream));
+    ctx->launches += 1;
+    SS_WS(seq, unsigned long long, "det.seq", n_plots);
+    std::vector<unsigned long long> hseq(static_cast<size_t>(n_plots));
+    for (int p = 0; p < n_plots; ++p) hseq[p] = first_seq + static_cast<unsigned long long>(p) * rows;
+    SS_CK(ctx, cudaMemcpyAsync(seq, hseq.data(), sizeof(unsigned long long) * n_plots, cudaMemcpyHostToDevice,
+                               ctx->stream));
+    s = detect_device(ctx, tf, n_plots, rows, cols, seq, sample_rate_hz, *cfg, praw, true, dev);
+    if (s != SS_OK) return s;
+    if (host_out) {
+        auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+            if (!dst) return cudaSuccess;
+            return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream);
+        };
+        SS_CK(ctx, cp(out->psd_raw, dev.psd_raw, sizeof(float) * n_plots * cols));
+        SS_CK(ctx, cp(out->psd_smoothed, dev.psd_smoothed, sizeof(float) * n_plots * cols));
+        SS_CK(ctx, cp(out->floor_thr, dev.floor_thr, sizeof(float) * n_plots * 2));
+        SS_CK(ctx, cp(out->active, dev.active, sizeof(int32_t) * n_plots * cols));
+        SS_CK(ctx, cp(out->n_active, dev.n_active, sizeof(int32_t) * n_plots));
+        SS_CK(ctx, cp(out->boxes, dev.boxes, sizeof(ss_box) * n_plots * K));
+        SS_CK(ctx, cp(out->bin_boxes, dev.bin_boxes, sizeof(ss_bin_box) * n_plots * K));
+        SS_CK(ctx, cp(out->n_boxes, dev.n_boxes, sizeof(int32_t) * n_plots));
+        SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    if (out->n_boxes) {
+        std::vector<int> nb(static_cast<size_t>(n_plots));
+        SS_CK(ctx, cudaMemcpy(nb.data(), out->n_boxes, sizeof(int) * n_plots, cudaMemcpyDefault));
+        for (int v : nb)
+            if (v > K) return fail(ctx, SS_ECAPACITY, "box capacity too small: " + std::to_string(v));
+    }
+    return SS_OK;
+}
+
+ss_status ss_test_libm(ss_ctx* ctx, const float* x, int64_t n, int which, int variant, float* out) {
+    if (!ctx) return SS_EVALIDATION;
+    const bool fma = variant < 0 ? ctx->fma_variant : variant != 0;
+    SS_CK(ctx, ssb::libm_test_launch(x, n, which, fma, out, ctx->stream));
+    ctx->launches += 1;
+    return SS_OK;
+}
+
+int64_t ss_fft_twiddle_count(int n_fft) {
+    if (n_fft < 8 || !is_pow2(n_fft) || n_fft > 8192) return -1;
+    std::vector<double2> t;
+    ssb::fft_twiddles(ilog2(n_fft), t);
+    return static_cast<int64_t>(t.size());
+}
+
+ss_status ss_fft_twiddles(int n_fft, double* out_re_im) {
+    if (n_fft < 8 || !is_pow2(n_fft) || n_fft > 8192) return SS_EVALIDATION;
+    std::vector<double2> t;
+    ssb::fft_twiddles(ilog2(n_fft), t);
+    std::memcpy(out_re_im, t.data(), sizeof(double2) * t.size());
+    return SS_OK;
+}
+
+} // extern "C"

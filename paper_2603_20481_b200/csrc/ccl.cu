@@ -1,0 +1,317 @@
+// ccl.cu -- K6: 4-connected component extents on bit-packed masks.
+//
+// Replaces detector::resolve_components / component_extents /
+// label_components and the box conversion (proj/src/detector.cpp:494-635).
+// Run-based union-find, batched over plots:
+//   1 count   : runs starting per row (start bits = x & ~(x<<1 | carry))
+//   2 scan    : per-plot exclusive row offsets; 3 per-plot pool bases
+//   4 emit    : runs in row-major order of their start pixel -> pool
+//   5 union   : each run unites with the overlapping runs of the row above
+//               (4-connectivity = shared column, :543-555); lock-free
+//               union-by-min (CAS on roots), so every root is the smallest run
+//               index of its component = its first row-major pixel
+//   6 flatten : parent -> root; area, max_t, min_f, max_f by atomics
+//   7 compact : roots with area >= min_area, numbered densely in root order
+//               (= first-pixel order, area filter before numbering: :570-593)
+//               -> extents, half-open bin boxes (:622-624) and physical boxes
+//               in double (:626-635)
+// Capacity: the run pool is sized by the caller; a plot whose runs do not fit
+// is flagged (plot_ok = 0, *overflow = 1) and the host re-runs it alone with
+// an exact-size pool (capi.cu).
+#include "common.cuh"
+#include "internal.h"
+
+#include <climits>
+
+namespace ssb {
+
+__device__ __forceinline__ uint32_t start_bits(const uint32_t* row, int w) {
+    const uint32_t x = row[w];
+    const uint32_t carry = w > 0 ? (row[w - 1] >> 31) : 0u;
+    return x & ~((x << 1) | carry);
+}
+
+__global__ void count_runs_kernel(const uint32_t* __restrict__ bits, int rows, int W, int* row_runs) {
+    const int p = blockIdx.y;
+    const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    const uint32_t* row = bits + (static_cast<long long>(p) * rows + r) * W;
+    int cnt = 0;
+    for (int w = lane; w < W; w += 32) cnt += __popc(start_bits(row, w));
+    cnt = warp_sum(cnt);
+    if (lane == 0) row_runs[static_cast<long long>(p) * rows + r] = cnt;
+}
+
+__global__ void scan_rows_kernel(const int* row_runs, int rows, int* row_off) {
+    __shared__ int red[32];
+    __shared__ int carry_s;
+    const int p = blockIdx.x;
+    const int* in = row_runs + static_cast<long long>(p) * rows;
+    int* out = row_off + static_cast<long long>(p) * (rows + 1);
+    if (threadIdx.x == 0) carry_s = 0;
+    __syncthreads();
+    for (int base = 0; base < rows; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        const int v = i < rows ? in[i] : 0;
+        const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+        const int inc = warp_incl_scan(v);
+        if (l == 31) red[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            const int nw = blockDim.x >> 5;
+            int x = l < nw ? red[l] : 0;
+            x = warp_incl_scan(x);
+            if (l < nw) red[l] = x;
+        }
+        __syncthreads();
+        const int carry = carry_s;
+        const int excl = carry + (w > 0 ? red[w - 1] : 0) + inc - v;
+        if (i < rows) out[i] = excl;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry_s = excl + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[rows] = carry_s;
+}
+
+__global__ void plot_base_kernel(const int* row_off, int n_plots, int rows, long long pool_cap,
+                                 long long* plot_base, int* plot_ok, int* overflow) {
+    if (threadIdx.x != 0) return;
+    long long acc = 0;
+    int of = 0;
+    for (int p = 0; p < n_plots; ++p) {
+        const long long total = row_off[static_cast<long long>(p) * (rows + 1) + rows];
+        plot_base[p] = acc;
+        const int ok = acc + total <= pool_cap ? 1 : 0;
+        plot_ok[p] = ok;
+        if (ok) acc += total;
+        else of = 1;
+    }
+    *overflow = of;
+}
+
+__global__ void emit_runs_kernel(const uint32_t* __restrict__ bits, int rows, int cols, const int* row_off,
+                                 const long long* plot_base, const int* plot_ok, CclWorkspace ws) {
+    const int W = (cols + 31) / 32;
+    const int p = blockIdx.y;
+    const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= rows || !plot_ok[p]) return;
+    const uint32_t* row = bits + (static_cast<long long>(p) * rows + r) * W;
+    long long idx0 = plot_base[p] + row_off[static_cast<long long>(p) * (rows + 1) + r];
+    for (int c0 = 0; c0 < W; c0 += 32) {
+        const int w = c0 + lane;
+        const uint32_t x = w < W ? row[w] : 0u;
+        uint32_t S = w < W ? start_bits(row, w) : 0u;
+        const int n = __popc(S);
+        const int inc = warp_incl_scan(n);
+        const int tot = __shfl_sync(0xffffffffu, inc, 31);
+        long long idx = idx0 + inc - n;
+        while (S) {
+            const int s = __ffs(S) - 1;
+            S &= S - 1;
+            const uint32_t z = s == 31 ? 0u : (~x & (0xffffffffu << (s + 1)));
+            int e;
+            if (z) {
+                e = 32 * w + __ffs(z) - 1;
+            } else {
+                int ww = w + 1;
+                while (ww < W && row[ww] == 0xffffffffu) ++ww;
+                e = ww < W ? 32 * ww + __ffs(~row[ww]) - 1 : 32 * W;
+            }
+            if (e > cols) e = cols;
+            ws.run_begin[idx] = 32 * w + s;
+            ws.run_end[idx] = e;
+            ws.run_row[idx] = r;
+            ws.parent[idx] = static_cast<int>(idx);
+            ws.area[idx] = 0ull;
+            ws.min_f[idx] = INT_MAX;
+            ws.max_f[idx] = -1;
+            ws.max_t[idx] = -1;
+            ws.dense[idx] = -1;
+            ++idx;
+        }
+        idx0 += tot;
+    }
+}
+
+__device__ __forceinline__ int uf_find(int* parent, int x) {
+    for (;;) {
+        const int p = __ldcg(parent + x);
+        if (p == x) return x;
+        const int gp = __ldcg(parent + p);
+        if (gp != p) parent[x] = gp;  // path halving; any ancestor is a valid parent
+        x = p;
+    }
+}
+
+__device__ __forceinline__ void uf_unite(int* parent, int a, int b) {
+    for (;;) {
+        a = uf_find(parent, a);
+        b = uf_find(parent, b);
+        if (a == b) return;
+        if (a < b) {
+            const int t = a;
+            a = b;
+            b = t;
+        }
+        const int old = atomicCAS(parent + a, a, b);  // hook the larger root under the smaller
+        if (old == a) return;
+        a = old;
+    }
+}
+
+__global__ void union_kernel(int rows, const int* row_off, const long long* plot_base, const int* plot_ok,
+                             CclWorkspace ws) {
+    const int p = blockIdx.y;
+    const int r = blockIdx.x * 8 + (threadIdx.x >> 5) + 1;
+    const int lane = threadIdx.x & 31;
+    if (r >= rows || !plot_ok[p]) return;
+    const int* off = row_off + static_cast<long long>(p) * (rows + 1);
+    const long long base = plot_base[p];
+    const long long prev_b = base + off[r - 1], cur_b = base + off[r], cur_e = base + off[r + 1];
+    for (long long i = cur_b + lane; i < cur_e; i += 32) {
+        const int b = ws.run_begin[i], e = ws.run_end[i];
+        long long lo = prev_b, hi = cur_b;
+        while (lo < hi) {
+            const long long mid = (lo + hi) >> 1;
+            if (ws.run_end[mid] > b) hi = mid;
+            else lo = mid + 1;
+        }
+        for (long long q = lo; q < cur_b && ws.run_begin[q] < e; ++q)
+            uf_unite(ws.parent, static_cast<int>(i), static_cast<int>(q));
+    }
+}
+
+__global__ void flatten_kernel(int rows, const int* row_off, const long long* plot_base, const int* plot_ok,
+                               CclWorkspace ws) {
+    const int p = blockIdx.y;
+    if (!plot_ok[p]) return;
+    const long long base = plot_base[p];
+    const long long n = row_off[static_cast<long long>(p) * (rows + 1) + rows];
+    for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = base + k;
+        const int root = uf_find(ws.parent, static_cast<int>(i));
+        ws.parent[i] = root;
+        const int b = ws.run_begin[i], e = ws.run_end[i];
+        atomicAdd(ws.area + root, static_cast<unsigned long long>(e - b));
+        atomicMax(ws.max_t + root, ws.run_row[i]);
+        atomicMin(ws.min_f + root, b);
+        atomicMax(ws.max_f + root, e - 1);
+    }
+}
+
+__global__ void compact_kernel(int rows, int cols, const int* row_off, const long long* plot_base,
+                               const int* plot_ok, CclWorkspace ws, CclLaunch L) {
+    __shared__ int red[32];
+    __shared__ int carry_s;
+    const int p = blockIdx.x;
+    if (!plot_ok[p]) {
+        if (threadIdx.x == 0) L.n_comp[p] = -1;
+        return;
+    }
+    const long long base = plot_base[p];
+    const long long n = row_off[static_cast<long long>(p) * (rows + 1) + rows];
+    const double fs = L.fs;
+    const double dt = __ddiv_rn(static_cast<double>(cols), fs);
+    const double df = __ddiv_rn(fs, static_cast<double>(cols));
+    const double seq = L.start_seq ? static_cast<double>(L.start_seq[p]) : 0.0;
+    if (threadIdx.x == 0) carry_s = 0;
+    __syncthreads();
+    for (long long c0 = 0; c0 < n; c0 += blockDim.x) {
+        const long long k = c0 + threadIdx.x;
+        const long long i = base + k;
+        int flag = 0;
+        if (k < n) flag = (ws.parent[i] == static_cast<int>(i) && ws.area[i] >= static_cast<unsigned long long>(L.min_area)) ? 1 : 0;
+        const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+        const int inc = warp_incl_scan(flag);
+        if (l == 31) red[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            const int nw = blockDim.x >> 5;
+            int x = l < nw ? red[l] : 0;
+            x = warp_incl_scan(x);
+            if (l < nw) red[l] = x;
+        }
+        __syncthreads();
+        const int carry = carry_s;
+        const int id = carry + (w > 0 ? red[w - 1] : 0) + inc - flag;
+        if (flag) {
+            ws.dense[i] = id;
+            if (id < L.cap) {
+                const long long o = static_cast<long long>(p) * L.cap + id;
+                const int min_t = ws.run_row[i], max_t = ws.max_t[i];
+                const int min_f = ws.min_f[i], max_f = ws.max_f[i];
+                if (L.extents) {
+                    long long* e = L.extents + 5 * o;
+                    e[0] = min_t;
+                    e[1] = max_t;
+                    e[2] = min_f;
+                    e[3] = max_f;
+                    e[4] = static_cast<long long>(ws.area[i]);
+                }
+                if (L.bin_boxes) {
+                    int* bb = L.bin_boxes + 4 * o;
+                    bb[0] = min_t;
+                    bb[1] = max_t + 1;
+                    bb[2] = min_f;
+                    bb[3] = max_f + 1;
+                }
+                if (L.boxes) {
+                    double* bx = L.boxes + 4 * o;
+                    bx[0] = __dmul_rn(static_cast<double>(min_f - cols / 2), df);
+                    bx[1] = __dmul_rn(static_cast<double>(max_f + 1 - cols / 2), df);
+                    bx[2] = __dmul_rn(__dadd_rn(seq, static_cast<double>(min_t)), dt);
+                    bx[3] = __dmul_rn(__dadd_rn(seq, static_cast<double>(max_t + 1)), dt);
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry_s = id + flag;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) L.n_comp[p] = carry_s;
+}
+
+__global__ void labels_kernel(int rows, int cols, const int* row_off, CclWorkspace ws, int32_t* labels) {
+    const long long n = row_off[rows];
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int id = ws.dense[ws.parent[i]];
+        if (id < 0) continue;
+        int32_t* row = labels + static_cast<long long>(ws.run_row[i]) * cols;
+        for (int c = ws.run_begin[i]; c < ws.run_end[i]; ++c) row[c] = id + 1;
+    }
+}
+
+cudaError_t ccl_launch(const CclLaunch& L, cudaStream_t st) {
+    if (L.n_plots <= 0 || L.rows <= 0 || L.cols <= 0) return cudaSuccess;
+    const int W = (L.cols + 31) / 32;
+    const CclWorkspace& ws = L.ws;
+    dim3 rgrid((L.rows + 7) / 8, L.n_plots);
+    count_runs_kernel<<<rgrid, 256, 0, st>>>(L.bits, L.rows, W, ws.row_runs);
+    scan_rows_kernel<<<L.n_plots, 1024, 0, st>>>(ws.row_runs, L.rows, ws.row_off);
+    plot_base_kernel<<<1, 32, 0, st>>>(ws.row_off, L.n_plots, L.rows, ws.pool_cap, ws.plot_base, ws.plot_ok,
+                                       ws.overflow);
+    emit_runs_kernel<<<rgrid, 256, 0, st>>>(L.bits, L.rows, L.cols, ws.row_off, ws.plot_base, ws.plot_ok, ws);
+    if (L.rows > 1) {
+        dim3 ugrid((L.rows - 1 + 7) / 8, L.n_plots);
+        union_kernel<<<ugrid, 256, 0, st>>>(L.rows, ws.row_off, ws.plot_base, ws.plot_ok, ws);
+    }
+    int per_plot = 4096 / (L.n_plots > 0 ? L.n_plots : 1);
+    if (per_plot < 2) per_plot = 2;
+    if (per_plot > 64) per_plot = 64;
+    dim3 fgrid(per_plot, L.n_plots);
+    flatten_kernel<<<fgrid, 256, 0, st>>>(L.rows, ws.row_off, ws.plot_base, ws.plot_ok, ws);
+    compact_kernel<<<L.n_plots, 512, 0, st>>>(L.rows, L.cols, ws.row_off, ws.plot_base, ws.plot_ok, ws, L);
+    if (L.labels) {
+        cudaMemsetAsync(L.labels, 0, sizeof(int32_t) * static_cast<size_t>(L.rows) * L.cols, st);
+        // single-plot use: plot 0's runs start at pool index 0
+        labels_kernel<<<256, 256, 0, st>>>(L.rows, L.cols, ws.row_off, ws, L.labels);
+    }
+    return cudaGetLastError();
+}
+
+} // namespace ssb

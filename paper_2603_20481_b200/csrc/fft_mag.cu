@@ -1,0 +1,519 @@
+// fft_mag.cu -- K1: IQ rows -> DC-centred FFT-magnitude TF rows (+ exact PSD).
+//
+// Replaces frontend::fft_row / make_plot / make_plots
+// (proj/src/frontend.cpp:127-183) and, fused, the column sum of
+// detector::estimate_psd_into (proj/src/detector.cpp:170-184).
+//
+// Arithmetic: the SSFFT-1 specification -- FP64 Stockham DIT
+// autosort, radix-16 passes + one radix-2^(log2N mod 4) pass, table twiddles,
+// explicit-rounding butterflies -- then out[k] = float(sqrt(fma(re, re,
+// im*im))) of bin (k + N/2) mod N, exactly the expression GCC emits for
+// proj/src/frontend.cpp:147 (vmulsd im*im; vfmadd re*re+.; vsqrtsd; cvtsd2ss).
+// The oracle's FFTW shim (oracle/fftw_shim.c) implements the same spec on the
+// CPU, so TF plots are bit-identical.
+//
+// Layout / schedule (B200): 256 threads (512 for N = 8192) per CTA, 16 complex
+// doubles per thread in registers; G = 256/(N/16) rows per CTA iteration.
+// The next iteration's raw IQ rows (contiguous, G*N samples) are fetched by
+// one TMA 1-D bulk copy into a shared stage buffer behind an mbarrier while
+// the current rows are transformed; the two inter-pass exchanges go through a
+// padded shared buffer (idx + idx/16: conflict-free 16-byte accesses).  In
+// PSD mode one CTA owns one whole plot and walks its rows in order, so the
+// per-column sum of x^2 runs in the reference's exact row order in registers
+// (acc = fma(x, x, acc): x^2 is exact, fusion is bit-neutral).
+#include "common.cuh"
+#include "internal.h"
+
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+namespace ssb {
+
+// ---------------------------------------------------------------- butterflies
+
+__device__ __forceinline__ void dft2(cd* v) {
+    const cd a = v[0], b = v[1];
+    v[0] = c_add(a, b);
+    v[1] = c_sub(a, b);
+}
+
+template <int S>
+__device__ __forceinline__ void dft4s(cd* v) {
+    const cd t0 = c_add(v[0], v[2 * S]);
+    const cd t1 = c_sub(v[0], v[2 * S]);
+    const cd t2 = c_add(v[S], v[3 * S]);
+    const cd t3 = c_sub(v[S], v[3 * S]);
+    v[0] = c_add(t0, t2);
+    v[2 * S] = c_sub(t0, t2);
+    v[S] = {__dadd_rn(t1.re, t3.im), __dsub_rn(t1.im, t3.re)};
+    v[3 * S] = {__dsub_rn(t1.re, t3.im), __dadd_rn(t1.im, t3.re)};
+}
+
+__device__ __forceinline__ void dft8(cd* v) {
+    cd e[4] = {v[0], v[2], v[4], v[6]};
+    cd o[4] = {v[1], v[3], v[5], v[7]};
+    dft4s<1>(e);
+    dft4s<1>(o);
+    o[1] = c_w8(o[1]);
+    o[2] = c_mi(o[2]);
+    o[3] = c_w83(o[3]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        v[k] = c_add(e[k], o[k]);
+        v[k + 4] = c_sub(e[k], o[k]);
+    }
+}
+
+// 4x4 decomposition; y[n1*4+k2] after the first DFT4 layer.
+__device__ __forceinline__ void dft16(cd* v) {
+    cd y[16];
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) {
+        cd t[4] = {v[n1], v[n1 + 4], v[n1 + 8], v[n1 + 12]};
+        dft4s<1>(t);
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) y[n1 * 4 + k2] = t[k2];
+    }
+    const cd w1 = {kC1, -kS1};
+    const cd w3 = {kS1, -kC1};
+    const cd w9 = {-kC1, kS1};
+    y[5] = c_mul(y[5], w1);
+    y[6] = c_w8(y[6]);
+    y[7] = c_mul(y[7], w3);
+    y[9] = c_w8(y[9]);
+    y[10] = c_mi(y[10]);
+    y[11] = c_w83(y[11]);
+    y[13] = c_mul(y[13], w3);
+    y[14] = c_w83(y[14]);
+    y[15] = c_mul(y[15], w9);
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) {
+        cd t[4] = {y[k2], y[4 + k2], y[8 + k2], y[12 + k2]};
+        dft4s<1>(t);
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) v[k2 + 4 * k1] = t[k1];
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void dft_r(cd* v) {
+    if constexpr (R == 2) dft2(v);
+    else if constexpr (R == 4) dft4s<1>(v);
+    else if constexpr (R == 8) dft8(v);
+    else dft16(v);
+}
+
+// ------------------------------------------------------------------ plan
+
+template <int LOGN>
+struct FftPlan {
+    static constexpr int N = 1 << LOGN;
+    static constexpr int P = N >= 16 ? 16 : N;      // points per thread
+    static constexpr int TPR = N / P;               // threads per row
+    static constexpr int NT = TPR > 256 ? TPR : 256; // threads per CTA
+    static constexpr int G = NT / TPR;              // rows per iteration
+    static constexpr int NP = (LOGN == 3) ? 1 : (LOGN / 4 + (LOGN % 4 ? 1 : 0));
+    static constexpr int SROW = N + N / 16;          // padded smem row (elements)
+    __host__ __device__ static constexpr int radix(int p) {
+        return (LOGN == 3) ? 8 : (p < LOGN / 4 ? 16 : (1 << (LOGN % 4)));
+    }
+    __host__ __device__ static constexpr int ns(int p) {
+        int s = 1;
+        for (int q = 0; q < p; ++q) s *= radix(q);
+        return s;
+    }
+    // offset of pass p's twiddle block in the per-N table
+    __host__ __device__ static constexpr int tw_off(int p) {
+        int o = 0;
+        for (int q = 1; q < p; ++q) o += (radix(q) - 1) * ns(q);
+        return o;
+    }
+    __host__ __device__ static constexpr int tw_size() { return tw_off(NP); }
+};
+
+__device__ __forceinline__ int pad_idx(int i) { return i + (i >> 4); }
+
+// Twiddle + butterflies of pass p on register data already holding this
+// pass's inputs: butterfly b_u = j + TPR*u owns v[u*R .. u*R+R-1].
+template <int LOGN, int PASS>
+__device__ __forceinline__ void run_pass(cd* v, int j, const double2* __restrict__ tw) {
+    using PL = FftPlan<LOGN>;
+    constexpr int R = PL::radix(PASS);
+    constexpr int NS = PL::ns(PASS);
+    constexpr int U = PL::P / R;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if constexpr (NS > 1) {
+            const int b = j + PL::TPR * u;
+            const int k = b % NS;
+            const double2* t = tw + PL::tw_off(PASS) + k;
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                const double2 w = __ldg(t + (r - 1) * NS);
+                v[u * R + r] = c_mul(v[u * R + r], cd{w.x, w.y});
+            }
+        }
+        dft_r<R>(v + u * R);
+    }
+}
+
+// Store pass PASS's outputs into smem (padded), then load pass PASS+1's inputs.
+template <int LOGN, int PASS>
+__device__ __forceinline__ void exchange(cd* v, int j, double2* buf) {
+    using PL = FftPlan<LOGN>;
+    constexpr int R = PL::radix(PASS);
+    constexpr int NS = PL::ns(PASS);
+    constexpr int U = PL::P / R;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int b = j + PL::TPR * u;
+        const int k = b % NS;
+        const int base = (b - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[pad_idx(base + r * NS)] = make_double2(v[u * R + r].re, v[u * R + r].im);
+    }
+    __syncthreads();
+    constexpr int R2 = PL::radix(PASS + 1);
+    constexpr int U2 = PL::P / R2;
+#pragma unroll
+    for (int u = 0; u < U2; ++u) {
+        const int b = j + PL::TPR * u;
+#pragma unroll
+        for (int r = 0; r < R2; ++r) {
+            const double2 x = buf[pad_idx(b + r * (PL::N / R2))];
+            v[u * R2 + r] = {x.x, x.y};
+        }
+    }
+    __syncthreads();
+}
+
+template <int LOGN, int PASS>
+__device__ __forceinline__ void passes_from(cd* v, int j, const double2* tw, double2* buf) {
+    using PL = FftPlan<LOGN>;
+    run_pass<LOGN, PASS>(v, j, tw);
+    if constexpr (PASS + 1 < PL::NP) {
+        exchange<LOGN, PASS>(v, j, buf);
+        passes_from<LOGN, PASS + 1>(v, j, tw, buf);
+    }
+}
+
+// |X| rounded to float, bit-identical to float(sqrt(fma(re, re, im*im))).
+// Fast path: float rsqrt seed + one Newton step in double gives sqrt(q) to
+// < 2^10 double ulps; when that estimate is > 2^13 ulps away from a float
+// rounding midpoint, rounding it to float equals rounding the correctly
+// rounded double sqrt.  Otherwise (p ~ 2^-15) and outside [2^-120, 2^120],
+// fall back to the IEEE __dsqrt_rn.  DESIGN.md §3.3 has the error budget.
+__device__ __forceinline__ float mag_f32(double re, double im) {
+    const double q = __fma_rn(re, re, __dmul_rn(im, im));
+    if (q >= 0x1p-120 && q <= 0x1p120) {
+        const float yf = rsqrtf(__double2float_rn(q));
+        const double y = static_cast<double>(yf);
+        const double s0 = __dmul_rn(q, y);
+        const double d = __fma_rn(-s0, s0, q);
+        const double s1 = __fma_rn(d, __dmul_rn(0.5, y), s0);
+        const uint32_t low = static_cast<uint32_t>(__double_as_longlong(s1)) & 0x1FFFFFFFu;
+        const int dist = static_cast<int>(low) - (1 << 28);
+        if (dist > 8192 || dist < -8192) return __double2float_rn(s1);
+    }
+    return __double2float_rn(__dsqrt_rn(q));
+}
+
+// ------------------------------------------------------------------ kernel
+
+struct FftArgs {
+    const void* iq;      // n_rows_total * N samples, f32 or i16 interleaved
+    float* tf;           // n_rows_total * N floats, may be null in PSD mode
+    float* psd;          // n_plots * N (PSD mode)
+    const double2* tw;   // per-N pass twiddle table
+    long long total_rows;
+    int rows_per_plot;   // PSD mode: T
+};
+
+template <int LOGN, int FMT, bool PSD>
+__global__ void __launch_bounds__(FftPlan<LOGN>::NT, (LOGN >= 13 ? 1 : 2))
+fft_mag_kernel(FftArgs a) {
+    using PL = FftPlan<LOGN>;
+    constexpr int N = PL::N;
+    constexpr int G = PL::G;
+    constexpr int SAMPLE_BYTES = FMT == 0 ? 8 : 4;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double2* buf = reinterpret_cast<double2*>(smem_raw);                          // G * SROW
+    unsigned char* stage = smem_raw + sizeof(double2) * G * PL::SROW;             // G*N samples
+    float* magbuf = reinterpret_cast<float*>(stage + SAMPLE_BYTES * G * N);       // G*N (G>1, PSD)
+    __shared__ __align__(8) uint64_t bar;
+
+    const int tid = threadIdx.x;
+    const int g = tid / PL::TPR;
+    const int j = tid % PL::TPR;
+    double2* mybuf = buf + g * PL::SROW;
+
+    // iteration space
+    long long it_begin, it_end, it_step, row_base;
+    if constexpr (PSD) {
+        row_base = static_cast<long long>(blockIdx.x) * a.rows_per_plot;
+        it_begin = 0;
+        it_end = (a.rows_per_plot + G - 1) / G;
+        it_step = 1;
+    } else {
+        row_base = 0;
+        it_begin = blockIdx.x;
+        it_end = (a.total_rows + G - 1) / G;
+        it_step = gridDim.x;
+    }
+    const long long row_limit = PSD ? row_base + a.rows_per_plot : a.total_rows;
+
+    auto issue = [&](long long it) {
+        const long long r0 = row_base + it * G;
+        long long nr = row_limit - r0;
+        if (nr > G) nr = G;
+        const uint32_t bytes = static_cast<uint32_t>(nr * N * SAMPLE_BYTES);
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bar, bytes);
+        bulk_g2s(stage, static_cast<const unsigned char*>(a.iq) + r0 * N * SAMPLE_BYTES, bytes, &bar);
+    };
+
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0 && it_begin < it_end) issue(it_begin);
+
+    // PSD accumulators: G == 1 -> per (u, r) column owned by this thread;
+    // G > 1 -> columns tid + NT*i, i < N/NT (>= 1 when N >= NT; else tid < N).
+    constexpr int NACC = PSD ? (G == 1 ? PL::P : (N >= PL::NT ? N / PL::NT : 1)) : 1;
+    double acc[NACC];
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+
+    uint32_t phase = 0;
+    for (long long it = it_begin; it < it_end; it += it_step) {
+        const long long r0 = row_base + it * G;
+        const long long row = r0 + g;
+        const bool valid = row < row_limit;
+
+        mbar_wait(&bar, phase);
+        phase ^= 1;
+
+        // pass-0 inputs from the stage
+        cd v[16];
+        {
+            constexpr int R0 = PL::radix(0);
+            constexpr int U0 = PL::P / R0;
+#pragma unroll
+            for (int u = 0; u < U0; ++u) {
+                const int b = j + PL::TPR * u;
+#pragma unroll
+                for (int r = 0; r < R0; ++r) {
+                    const int s = g * N + b + r * (N / R0);
+                    if constexpr (FMT == 0) {
+                        const float2 x = valid ? reinterpret_cast<const float2*>(stage)[s] : make_float2(0.f, 0.f);
+                        v[u * R0 + r] = {static_cast<double>(x.x), static_cast<double>(x.y)};
+                    } else {
+                        const short2 x = valid ? reinterpret_cast<const short2*>(stage)[s] : make_short2(0, 0);
+                        // frontend.cpp:383: raw * (1.0f/32768) (exact), promoted to double
+                        v[u * R0 + r] = {static_cast<double>(__fmul_rn(static_cast<float>(x.x), 1.0f / 32768.0f)),
+                                         static_cast<double>(__fmul_rn(static_cast<float>(x.y), 1.0f / 32768.0f))};
+                    }
+                }
+            }
+        }
+        __syncthreads();  // stage consumed by every thread
+        if (tid == 0 && it + it_step < it_end) issue(it + it_step);
+
+        passes_from<LOGN, 0>(v, j, a.tw, mybuf);
+
+        // epilogue: outputs of the last pass, index q = b + r*NS_last
+        constexpr int RL = PL::radix(PL::NP - 1);
+        constexpr int NSL = PL::ns(PL::NP - 1);
+        constexpr int UL = PL::P / RL;
+        if constexpr (G == 1) {
+            float* out = a.tf ? a.tf + row * N : nullptr;
+#pragma unroll
+            for (int u = 0; u < UL; ++u) {
+#pragma unroll
+                for (int r = 0; r < RL; ++r) {
+                    const int q = j + PL::TPR * u + r * NSL;
+                    const int k = (q + N / 2) & (N - 1);
+                    const float m = mag_f32(v[u * RL + r].re, v[u * RL + r].im);
+                    if (valid && out) out[k] = m;
+                    if constexpr (PSD) {
+                        if (valid) {
+                            const double md = static_cast<double>(m);
+                            acc[u * RL + r] = __fma_rn(md, md, acc[u * RL + r]);
+                        }
+                    }
+                }
+            }
+        } else {
+            // stage magnitudes so stores are row-contiguous and PSD runs in row order
+            float* mrow = magbuf + g * N;
+#pragma unroll
+            for (int u = 0; u < UL; ++u) {
+#pragma unroll
+                for (int r = 0; r < RL; ++r) {
+                    const int q = j + PL::TPR * u + r * NSL;
+                    const int k = (q + N / 2) & (N - 1);
+                    mrow[k] = mag_f32(v[u * RL + r].re, v[u * RL + r].im);
+                }
+            }
+            __syncthreads();
+            long long nvalid = row_limit - r0;
+            if (nvalid > G) nvalid = G;
+            if (a.tf) {
+                float* out = a.tf + r0 * N;
+                const int total = static_cast<int>(nvalid) * N;
+                for (int e = tid; e < total; e += PL::NT) out[e] = magbuf[e];
+            }
+            if constexpr (PSD) {
+#pragma unroll
+                for (int i = 0; i < NACC; ++i) {
+                    const int c = tid + PL::NT * i;
+                    if (c < N) {
+                        for (int gg = 0; gg < nvalid; ++gg) {
+                            const double md = static_cast<double>(magbuf[gg * N + c]);
+                            acc[i] = __fma_rn(md, md, acc[i]);
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+
+    if constexpr (PSD) {
+        const double inv_rows = __ddiv_rn(1.0, static_cast<double>(a.rows_per_plot));
+        float* psd = a.psd + static_cast<long long>(blockIdx.x) * N;
+        if constexpr (G == 1) {
+            constexpr int RL = PL::radix(PL::NP - 1);
+            constexpr int NSL = PL::ns(PL::NP - 1);
+            constexpr int UL = PL::P / RL;
+#pragma unroll
+            for (int u = 0; u < UL; ++u)
+#pragma unroll
+                for (int r = 0; r < RL; ++r) {
+                    const int q = j + PL::TPR * u + r * NSL;
+                    const int k = (q + N / 2) & (N - 1);
+                    psd[k] = __double2float_rn(__dmul_rn(acc[u * RL + r], inv_rows));
+                }
+        } else {
+#pragma unroll
+            for (int i = 0; i < NACC; ++i) {
+                const int c = tid + PL::NT * i;
+                if (c < N) psd[c] = __double2float_rn(__dmul_rn(acc[i], inv_rows));
+            }
+        }
+    }
+}
+
+} // namespace ssb
+
+// ------------------------------------------------------------------ host side
+
+namespace ssb {
+
+// SSFFT-1 canonical twiddles tw[e] = (cos t, -sin t), t = (2 pi e)/N, expanded
+// into the per-pass layout the kernel reads: pass p (Ns > 1) block holds
+// tw[r*k*N/(Ns*R)] at (r-1)*Ns + k.
+template <int LOGN>
+static void build_tw(std::vector<double2>& out) {
+    using PL = FftPlan<LOGN>;
+    constexpr int N = PL::N;
+    std::vector<double2> canon(N);
+    const double two_pi = 2.0 * 3.14159265358979323846;
+    for (int e = 0; e < N; ++e) {
+        const double t = (two_pi * static_cast<double>(e)) / static_cast<double>(N);
+        canon[e] = make_double2(std::cos(t), -std::sin(t));
+    }
+    out.assign(PL::tw_size() > 0 ? PL::tw_size() : 1, make_double2(0, 0));
+    for (int p = 1; p < PL::NP; ++p) {
+        const int R = PL::radix(p), NS = PL::ns(p);
+        for (int r = 1; r < R; ++r)
+            for (int k = 0; k < NS; ++k)
+                out[PL::tw_off(p) + (r - 1) * NS + k] = canon[static_cast<size_t>(r) * k * (N / (NS * R))];
+    }
+}
+
+template <int LOGN>
+static size_t smem_bytes(int fmt) {
+    using PL = FftPlan<LOGN>;
+    const size_t sb = fmt == 0 ? 8 : 4;
+    size_t bytes = sizeof(double2) * PL::G * PL::SROW + sb * PL::G * PL::N;
+    if (PL::G > 1) bytes += sizeof(float) * PL::G * PL::N;
+    return bytes;
+}
+
+template <int LOGN, int FMT, bool PSD>
+static cudaError_t launch_one(const FftLaunch& L, cudaStream_t st) {
+    using PL = FftPlan<LOGN>;
+    auto kern = fft_mag_kernel<LOGN, FMT, PSD>;
+    const size_t smem = smem_bytes<LOGN>(FMT);
+    static bool attr_done = false;  // per instantiation
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    FftArgs a;
+    a.iq = L.iq;
+    a.tf = L.tf;
+    a.psd = L.psd_out;
+    a.tw = L.tw;
+    a.total_rows = L.total_rows;
+    a.rows_per_plot = L.rows_per_plot;
+    long long grid;
+    if (PSD) {
+        grid = L.n_plots;
+    } else {
+        const long long iters = (L.total_rows + PL::G - 1) / PL::G;
+        const long long cap = static_cast<long long>(L.num_sms) * (LOGN >= 13 ? 1 : 2);
+        grid = iters < cap ? iters : cap;
+    }
+    if (grid <= 0) return cudaSuccess;
+    kern<<<static_cast<unsigned>(grid), PL::NT, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int LOGN>
+static cudaError_t dispatch_fmt(const FftLaunch& L, cudaStream_t st) {
+    if (L.fmt == 0) return L.psd ? launch_one<LOGN, 0, true>(L, st) : launch_one<LOGN, 0, false>(L, st);
+    return L.psd ? launch_one<LOGN, 1, true>(L, st) : launch_one<LOGN, 1, false>(L, st);
+}
+
+cudaError_t fft_mag_launch(const FftLaunch& L, cudaStream_t st) {
+    switch (L.logn) {
+    case 3: return dispatch_fmt<3>(L, st);
+    case 4: return dispatch_fmt<4>(L, st);
+    case 5: return dispatch_fmt<5>(L, st);
+    case 6: return dispatch_fmt<6>(L, st);
+    case 7: return dispatch_fmt<7>(L, st);
+    case 8: return dispatch_fmt<8>(L, st);
+    case 9: return dispatch_fmt<9>(L, st);
+    case 10: return dispatch_fmt<10>(L, st);
+    case 11: return dispatch_fmt<11>(L, st);
+    case 12: return dispatch_fmt<12>(L, st);
+    case 13: return dispatch_fmt<13>(L, st);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+void fft_twiddles(int logn, std::vector<double2>& out) {
+    switch (logn) {
+    case 3: build_tw<3>(out); break;
+    case 4: build_tw<4>(out); break;
+    case 5: build_tw<5>(out); break;
+    case 6: build_tw<6>(out); break;
+    case 7: build_tw<7>(out); break;
+    case 8: build_tw<8>(out); break;
+    case 9: build_tw<9>(out); break;
+    case 10: build_tw<10>(out); break;
+    case 11: build_tw<11>(out); break;
+    case 12: build_tw<12>(out); break;
+    case 13: build_tw<13>(out); break;
+    default: out.clear();
+    }
+}
+
+} // namespace ssb

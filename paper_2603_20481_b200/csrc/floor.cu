@@ -1,0 +1,259 @@
+// floor.cu -- K2 column PSD (stage form) and K3 noise floor + column pruning.
+//
+// K3 replaces detector::smooth_and_floor + prune_columns
+// (proj/src/detector.cpp:210-255), one CTA per plot:
+//   db[k]   = raw > 0 ? 10.0f * log10f(raw) : -3000.0f        (glibc log10f port)
+//   sdb[i]  = float( sum_{j=-h..h} acc + w_j * (double)db[mirror(i+j)] )
+//             -- a rounded multiply then a rounded add, in j order (:203-204)
+//   s[i]    = powf(10.0f, sdb[i] / 10.0f)                      (glibc powf port)
+//   floor   = lowest strict local minimum (plateau counted once at its first
+//             index, :229-242), else the global minimum (:243)
+//   thr     = float(double(floor) * pow(10, margin/10))        (:246-247)
+//   active  = { k : raw[k] >= thr } ascending                  (:250-255)
+// The SG weights come from the host (host_consts.cpp restates :84-142 with the
+// three fused updates GCC emits); pow(10, margin/10) is a host-libm constant.
+#include "common.cuh"
+#include "glibc_libm.cuh"
+#include "internal.h"
+
+#include <cfloat>
+
+namespace ssb {
+
+constexpr int kFloorThreads = 512;
+
+__device__ __forceinline__ int mirror_index(int i, int n) {
+    if (i < 0) return -i;
+    if (i >= n) return 2 * (n - 1) - i;
+    return i;
+}
+
+__device__ __forceinline__ float block_min(float v, float* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    const int nw = (blockDim.x + 31) >> 5;
+    v = (threadIdx.x < nw) ? red[threadIdx.x] : INFINITY;
+    if (w == 0) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (l == 0) red[0] = v;
+    }
+    __syncthreads();
+    const float r = red[0];
+    __syncthreads();
+    return r;
+}
+
+// Exclusive block scan of one int per thread; returns the exclusive prefix and
+// writes the total to *total.
+__device__ __forceinline__ int block_excl_scan(int v, int* red, int* total) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int inc = warp_incl_scan(v);
+    __syncthreads();
+    if (l == 31) red[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        const int nw = (blockDim.x + 31) >> 5;
+        int x = l < nw ? red[l] : 0;
+        x = warp_incl_scan(x);
+        if (l < nw) red[l] = x;
+    }
+    __syncthreads();
+    const int before = (w > 0 ? red[w - 1] : 0) + inc - v;
+    *total = red[((blockDim.x + 31) >> 5) - 1];
+    __syncthreads();
+    return before;
+}
+
+__device__ __forceinline__ double fir_at(const float* db, const double* w, int i, int n, int h) {
+    double acc = 0.0;
+    for (int j = -h; j <= h; ++j)
+        acc = __dadd_rn(acc, __dmul_rn(w[j + h], static_cast<double>(db[mirror_index(i + j, n)])));
+    return acc;
+}
+
+__global__ void __launch_bounds__(kFloorThreads) floor_kernel(FloorLaunch a) {
+    extern __shared__ double fl_smem[];
+    const int n = a.n;
+    const int h = (a.window - 1) / 2;
+    double* w = fl_smem;
+    float* db = reinterpret_cast<float*>(w + a.window);
+    float* s = db + n;
+    __shared__ float red_f[32];
+    __shared__ int red_i[32];
+
+    const int p = blockIdx.x;
+    const float* raw = a.raw + static_cast<long long>(p) * n;
+    const int tid = threadIdx.x, nt = blockDim.x;
+
+    for (int i = tid; i < a.window; i += nt) w[i] = a.weights[i];
+    for (int k = tid; k < n; k += nt) {
+        const float r = raw[k];
+        db[k] = r > 0.0f ? __fmul_rn(10.0f, glibc_log10f(r, a.fma_variant)) : -3000.0f;
+    }
+    __syncthreads();
+    bool my_nan = false;
+    for (int i = tid; i < n; i += nt) {
+        const float sdb = __double2float_rn(fir_at(db, w, i, n, h));
+        const float sv = glibc_powf10(__fdiv_rn(sdb, 10.0f), a.fma_variant);
+        s[i] = sv;
+        a.smoothed[static_cast<long long>(p) * n + i] = sv;
+        my_nan |= (sv != sv);
+    }
+    const bool any_nan = __syncthreads_or(my_nan);
+
+    // strict local minima, plateaus counted once at their first index
+    float best = INFINITY;
+    for (int i = 1 + tid; i < n - 1; i += nt) {
+        const float si = s[i];
+        const bool visited = (i == 1) || !(si == s[i - 1]);
+        if (!visited) continue;
+        int j = i;
+        while (j + 1 < n && s[j + 1] == si) ++j;
+        const bool left_up = s[i - 1] > si;
+        const bool right_up = (j + 1 < n) && s[j + 1] > si;
+        if (left_up && right_up && si < best) best = si;
+    }
+    float fl = block_min(best, red_f);
+    if (!(fl < INFINITY)) {
+        // no strict local minimum: std::min_element (first smallest under '<')
+        if (!any_nan) {
+            float m = INFINITY;
+            for (int i = tid; i < n; i += nt) m = fminf(m, s[i]);
+            fl = block_min(m, red_f);
+        } else {
+            __shared__ float seq_min;
+            if (tid == 0) {
+                float m = s[0];
+                for (int i = 1; i < n; ++i)
+                    if (s[i] < m) m = s[i];
+                seq_min = m;
+            }
+            __syncthreads();
+            fl = seq_min;
+        }
+    }
+    const float thr = __double2float_rn(__dmul_rn(static_cast<double>(fl), a.pow10_margin));
+    if (tid == 0) {
+        a.floor_thr[2 * p + 0] = fl;
+        a.floor_thr[2 * p + 1] = thr;
+    }
+
+    // prune: contiguous chunk per thread, block scan for the ascending compaction
+    const int chunk = (n + nt - 1) / nt;
+    const int k0 = tid * chunk;
+    const int k1 = min(n, k0 + chunk);
+    int cnt = 0;
+    for (int k = k0; k < k1; ++k) cnt += raw[k] >= thr ? 1 : 0;
+    int total = 0;
+    int off = block_excl_scan(cnt, red_i, &total);
+    int* act = a.active + static_cast<long long>(p) * n;
+    for (int k = k0; k < k1; ++k)
+        if (raw[k] >= thr) act[off++] = k;
+    if (tid == 0) a.n_active[p] = total;
+    if (a.active_bits) {
+        const int W = (n + 31) / 32;
+        uint32_t* bits = a.active_bits + static_cast<long long>(p) * W;
+        for (int wd = tid; wd < W; wd += nt) {
+            uint32_t b = 0;
+            for (int q = 0; q < 32; ++q) {
+                const int k = wd * 32 + q;
+                if (k < n && raw[k] >= thr) b |= 1u << q;
+            }
+            bits[wd] = b;
+        }
+    }
+}
+
+cudaError_t floor_launch(const FloorLaunch& L, cudaStream_t st) {
+    if (L.n_plots <= 0) return cudaSuccess;
+    const size_t smem = sizeof(double) * L.window + sizeof(float) * 2 * L.n;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(floor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+    }
+    floor_kernel<<<L.n_plots, kFloorThreads, smem, st>>>(L);
+    return cudaGetLastError();
+}
+
+// Stage form of savgol_smooth (detector.cpp:192-208): one CTA.
+__global__ void __launch_bounds__(kFloorThreads) savgol_kernel(const float* v, int n, int window,
+                                                               const double* weights, float* out) {
+    extern __shared__ double sg_smem[];
+    double* w = sg_smem;
+    float* vals = reinterpret_cast<float*>(w + window);
+    for (int i = threadIdx.x; i < window; i += blockDim.x) w[i] = weights[i];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) vals[i] = v[i];
+    __syncthreads();
+    const int h = (window - 1) / 2;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = __double2float_rn(fir_at(vals, w, i, n, h));
+}
+
+cudaError_t savgol_launch(const float* v, int n, int window, const double* weights, float* out,
+                          cudaStream_t st) {
+    const size_t smem = sizeof(double) * window + sizeof(float) * n;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(savgol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+    }
+    savgol_kernel<<<1, kFloorThreads, smem, st>>>(v, n, window, weights, out);
+    return cudaGetLastError();
+}
+
+// Stage form of estimate_psd_into (detector.cpp:170-184): one thread per
+// column, rows in order, 8 loads in flight.
+__global__ void psd_cols_kernel(const float* __restrict__ tf, int rows, int cols, int c0, int c1,
+                                float* __restrict__ out) {
+    const int p = blockIdx.y;
+    const int c = c0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= c1) return;
+    const float* base = tf + static_cast<long long>(p) * rows * cols + c;
+    double acc = 0.0;
+    int r = 0;
+    for (; r + 8 <= rows; r += 8) {
+        float x[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) x[q] = __ldg(base + static_cast<long long>(r + q) * cols);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const double d = static_cast<double>(x[q]);
+            acc = __fma_rn(d, d, acc);
+        }
+    }
+    for (; r < rows; ++r) {
+        const double d = static_cast<double>(__ldg(base + static_cast<long long>(r) * cols));
+        acc = __fma_rn(d, d, acc);
+    }
+    const double inv = __ddiv_rn(1.0, static_cast<double>(rows));
+    out[static_cast<long long>(p) * (c1 - c0) + (c - c0)] = __double2float_rn(__dmul_rn(acc, inv));
+}
+
+cudaError_t psd_cols_launch(const float* tf, int n_plots, int rows, int cols, int c0, int c1,
+                            float* out, cudaStream_t st) {
+    const int w = c1 - c0;
+    if (w <= 0 || n_plots <= 0) return cudaSuccess;
+    dim3 grid((w + 127) / 128, n_plots);
+    psd_cols_kernel<<<grid, 128, 0, st>>>(tf, rows, cols, c0, c1, out);
+    return cudaGetLastError();
+}
+
+__global__ void libm_test_kernel(const float* x, long long n, int which, bool fma_variant, float* out) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        out[i] = which == 0 ? glibc_log10f(x[i], fma_variant) : glibc_powf10(x[i], fma_variant);
+}
+
+cudaError_t libm_test_launch(const float* x, long long n, int which, bool fma_variant, float* out,
+                             cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    libm_test_kernel<<<148 * 8, 256, 0, st>>>(x, n, which, fma_variant, out);
+    return cudaGetLastError();
+}
+
+} // namespace ssb

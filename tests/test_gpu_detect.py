@@ -1,0 +1,136 @@
+"""GPU parity end to end: IQ -> TF plot -> PSD/floor/prune -> Otsu -> morphology
+-> CCL -> boxes through the fused C-ABI pipeline (ss_sense_batch), against the
+reference's make_plots + detect run on identical bytes rendered by the
+reference's own signals::synthesize.  Every output is compared bit for bit."""
+import numpy as np
+import pytest
+
+from paper_2603_20481_b200 import signals
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(det, exp, tf_got=None, tf_exp=None):
+    if tf_got is not None:
+        assert np.array_equal(tf_got.view(np.uint32), tf_exp.view(np.uint32))
+    assert np.array_equal(det.psd.raw.view(np.uint32), exp["raw"].view(np.uint32))
+    assert np.array_equal(det.psd.smoothed.view(np.uint32), exp["smoothed"].view(np.uint32))
+    assert np.float32(det.psd.noise_floor) == np.float32(exp["noise_floor"])
+    assert np.float32(det.psd.threshold) == np.float32(exp["threshold"])
+    assert np.array_equal(det.active_columns, exp["active"])
+    assert np.array_equal(det.bin_boxes, exp["bin_boxes"])
+    assert np.array_equal(det.boxes.view(np.uint64), exp["boxes"].view(np.uint64))
+
+
+def _run(ss, ref, sc, n_fft, rows, fmt=0):
+    iq, _ = ref.synthesize(signals.scenario_json(sc))
+    fs = sc["sample_rate_hz"]
+    dets, tf = ss.sense(iq, fs, n_fft, rows, return_tf=True)
+    exp_tf = ref.make_plots(iq, fs, n_fft, rows)
+    assert len(dets) == len(exp_tf) > 0
+    nb = 0
+    for p, det in enumerate(dets):
+        exp = ref.detect(exp_tf[p], start_seq=p * rows, fs=fs)
+        _check(det, exp, tf[p], exp_tf[p])
+        nb += len(det.boxes)
+    return nb
+
+
+def test_paper_config_T500(ss, ref):
+    """(T, F) = (500, 1024) @ 100 MS/s -- the acceptance suite grid (acceptance.cpp:93)."""
+    sc = signals.paper_scenario(rows=2000)
+    assert _run(ss, ref, sc, 1024, 500) > 0
+
+
+def test_paper_config_T2000(ss, ref):
+    """(T, F) = (2000, 1024): the paper's real-time configuration."""
+    sc = signals.paper_scenario(rows=4000)
+    assert _run(ss, ref, sc, 1024, 2000) > 0
+
+
+@pytest.mark.parametrize("capture", [0, 1])
+def test_c5_rect_capture(ss, ref, capture):
+    """BASELINE config 5 in reference-parity mode: 100 ms fp32 @ 100 MS/s, F = 4096
+    rectangular, hop 4096 -> T = 2441 (tail dropped)."""
+    sc = signals.c5_scenario(capture)
+    _run(ss, ref, sc, 4096, 2441)
+
+
+def test_c5_short_plots(ss, ref):
+    """Config-5 captures cut into T = 500 plots (20.48 ms at F = 4096): more bursts clear the prune."""
+    sc = signals.c5_scenario(5, duration_s=0.1)
+    assert _run(ss, ref, sc, 4096, 500) > 0
+
+
+def test_single_burst_iou(ss, ref):
+    """test_detector.cpp:608-650: one 20 dB burst in a (128, 256) plot -> one box, IoU >= 0.6."""
+    fs = 1e6
+    bw = 100e3
+    snr = 20.0
+    sc = dict(sample_rate_hz=fs, duration_s=0.0328, noise_power=1.0, seed=77,
+              signals=[dict(kind="ofdm-like", center_freq_hz=120e3, bandwidth_hz=bw, t_start_s=0.008,
+                            duration_s=0.016, power=10 ** (snr / 10) * (1.0 / fs) * bw)])
+    iq, truth = ref.synthesize(signals.scenario_json(sc))
+    dets = ss.sense(iq, fs, 256, 128)
+    assert len(dets) == 1 and len(dets[0].boxes) == 1
+    assert ref.iou(dets[0].boxes[0], truth[0, :4]) >= 0.6
+    _run(ss, ref, sc, 256, 128)
+
+
+def test_noise_only(ss, ref):
+    """test_detector.cpp:582-606: noise only -> no boxes, <= 5 % active columns."""
+    sc = dict(sample_rate_hz=1e6, duration_s=0.1, noise_power=1.0, seed=2024, signals=[])
+    iq, _ = ref.synthesize(signals.scenario_json(sc))
+    dets = ss.sense(iq, 1e6, 256, 128)
+    assert len(dets) >= 3
+    assert all(len(d.boxes) == 0 for d in dets)
+    assert sum(len(d.active_columns) for d in dets) / (len(dets) * 256) <= 0.05
+    _run(ss, ref, sc, 256, 128)
+
+
+def test_int16_path(ss, ref):
+    """int16 IQ (quantised with the reference's rule) through the fused pipeline."""
+    sc = signals.paper_scenario(rows=1000)
+    iq, _ = ref.synthesize(signals.scenario_json(sc))
+    v = np.clip(np.asarray(iq).view(np.float32) * np.float32(2.0 ** -6) * np.float32(32768.0), -32768, 32767)
+    q = np.rint(v).astype(np.int16)
+    dets, tf = ss.sense(q, 100e6, 1024, 500, fmt=1, return_tf=True)
+    as_f32 = (q.astype(np.float32) * np.float32(1 / 32768)).view(np.complex64)
+    exp_tf = ref.make_plots(as_f32, 100e6, 1024, 500)
+    for p, det in enumerate(dets):
+        _check(det, ref.detect(exp_tf[p], start_seq=p * 500, fs=100e6), tf[p], exp_tf[p])
+
+
+def test_detect_batch_matches_sense(ss, ref):
+    sc = signals.paper_scenario(rows=1500)
+    iq, _ = ref.synthesize(signals.scenario_json(sc))
+    exp_tf = ref.make_plots(iq, 100e6, 1024, 500)
+    dets = ss.detect_batch(exp_tf, 100e6, start_seq=[0, 500, 1000])
+    for p, det in enumerate(dets):
+        _check(det, ref.detect(exp_tf[p], start_seq=p * 500, fs=100e6))
+
+
+def test_config_variants(ss, ref):
+    """Non-default DetectorConfig: window/order/margin/min_area/vertical line opening."""
+    sc = signals.paper_scenario(rows=1000)
+    iq, _ = ref.synthesize(signals.scenario_json(sc))
+    tf = ref.make_plots(iq, 100e6, 1024, 500)
+    for cfg in [ss.DetectorConfig(savgol_window=15, savgol_order=2, psd_margin_db=1.5, min_component_area=9,
+                                  one_d_opening_along_time=True),
+                ss.DetectorConfig(savgol_window=51, savgol_order=4, psd_margin_db=0.5, min_component_area=1)]:
+        dets = ss.detect_batch(tf, 100e6, cfg, start_seq=[0, 500])
+        for p, det in enumerate(dets):
+            exp = ref.detect(tf[p], start_seq=p * 500, fs=100e6, window=cfg.savgol_window,
+                             order=cfg.savgol_order, margin_db=cfg.psd_margin_db,
+                             min_area=cfg.min_component_area, along_time=cfg.one_d_opening_along_time)
+            _check(det, exp)
+
+
+def test_config_validation(ss):
+    tf = np.ones((1, 10, 16), np.float32)
+    with pytest.raises(ss.ValidationError):
+        ss.detect_batch(tf, 1e6)                        # window 31 > 16 columns
+    with pytest.raises(ss.ValidationError):
+        ss.detect_batch(np.ones((1, 10, 64), np.float32), 1e6, ss.DetectorConfig(savgol_window=30))
+    with pytest.raises(ss.ValidationError):
+        ss.detect_batch(np.ones((1, 10, 64), np.float32), 1e6, ss.DetectorConfig(min_component_area=0))

@@ -1,0 +1,192 @@
+"""GPU parity, stage by stage, against the reference built as the oracle
+(oracle/_ref/libspecsense_ref.so): every comparison is bit-exact, with the
+reference's own contracts from proj/tests/test_detector.cpp re-run on the
+device path."""
+import numpy as np
+import pytest
+
+from _masks import burst_plot, random_blob_mask, random_mask, random_plot
+
+pytestmark = pytest.mark.gpu
+
+
+def test_psd_exact(ss, ref):
+    # test_detector.cpp:87-120
+    assert np.all(ss.estimate_psd(np.zeros((16, 8), np.float32)) == 0)
+    p = np.zeros((10, 6), np.float32)
+    p[:, 3] = 2.5
+    assert np.array_equal(ss.estimate_psd(p), np.array([0, 0, 0, 6.25, 0, 0], np.float32))
+    rng = np.random.default_rng(17)
+    for rows, cols in [(64, 128), (2441, 300), (1, 5), (2000, 1024)]:
+        tf = random_plot(rng, rows, cols)
+        assert np.array_equal(ss.estimate_psd(tf), ref.estimate_psd(tf))
+    tf = random_plot(rng, 32, 40)
+    assert np.array_equal(ss.estimate_psd_into(tf, 7, 18), ref.estimate_psd(tf)[7:18])
+    with pytest.raises(ss.ValidationError):
+        ss.estimate_psd_into(tf, 5, 5)
+
+
+@pytest.mark.parametrize("window,order", [(5, 2), (7, 3), (9, 4), (31, 3), (5, 1), (21, 6)])
+def test_savgol_exact(ss, ref, window, order):
+    rng = np.random.default_rng(23 + window)
+    v = rng.uniform(-10, 10, 257).astype(np.float32)
+    assert np.array_equal(ss.savgol_smooth(v, window, order), ref.savgol_smooth(v, window, order))
+
+
+def test_savgol_validation(ss):
+    v = np.ones(40, np.float32)
+    for w, o in [(6, 2), (3, 2), (5, 5), (51, 3)]:
+        with pytest.raises(ss.ValidationError):
+            ss.savgol_smooth(v, w, o)
+
+
+def _floor_cases(rng):
+    yield np.full(32, 2.0, np.float32)                       # constant -> global minimum
+    yield np.array([1 + abs(i - 16) * 0.5 for i in range(33)], np.float32)
+    yield np.maximum(0.2, 2 + np.cos(np.arange(64) * 0.45) - 1.2 * (np.arange(64) > 40)).astype(np.float32)
+    yield np.zeros(64, np.float32)                           # raw == 0 -> -3000 dB
+    z = rng.uniform(0.5, 4, 512).astype(np.float32)
+    z[100:140] = 0
+    yield z
+    for n in (64, 1024, 4096, 8192):
+        yield (rng.exponential(1.0, n) * 4096).astype(np.float32)
+    b = (rng.exponential(1.0, 4096) * 50 + 4096).astype(np.float32)
+    b[1000:1300] *= 8
+    yield b
+
+
+@pytest.mark.parametrize("margin", [3.0, 1.0, 6.0, 0.0])
+def test_floor_and_prune_exact(ss, ref, margin):
+    rng = np.random.default_rng(31)
+    for i, raw in enumerate(_floor_cases(rng)):
+        for window, order in ([(5, 2), (31, 3)] if len(raw) >= 31 else [(5, 2)]):
+            cfg = ss.DetectorConfig(savgol_window=window, savgol_order=order, psd_margin_db=margin)
+            prof = ss.PsdProfile(raw=raw)
+            act = ss.smooth_and_floor(prof, cfg)
+            sm, fl, thr, eact = ref.floor_prune(raw, window, order, margin)
+            assert np.array_equal(prof.smoothed.view(np.uint32), sm.view(np.uint32)), (i, window)
+            assert np.float32(prof.noise_floor).view(np.uint32) == np.float32(fl).view(np.uint32)
+            assert np.float32(prof.threshold).view(np.uint32) == np.float32(thr).view(np.uint32)
+            assert np.array_equal(act, eact)
+
+
+def test_otsu_exact(ss, ref):
+    # test_detector.cpp:249-287 (+ acceptance.cpp:359-384, 1000 columns)
+    v = np.r_[np.zeros(1000), np.full(1000, 10.0)].astype(np.float32)
+    ok, thr = ss.otsu_threshold(v)
+    assert ok and 0 < thr < 10
+    assert ss.otsu_threshold(np.full(100, 3.0, np.float32))[0] is False
+    with pytest.raises(ss.ValidationError):
+        ss.otsu_threshold(np.zeros(0, np.float32))
+    rng = np.random.default_rng(41)
+    for trial in range(300):
+        n = int(rng.integers(1, 700))
+        if trial % 3 == 0:
+            v = rng.random(n)
+        elif trial % 3 == 1:
+            v = np.abs(rng.normal(2.0, 0.7, n))
+        else:
+            v = np.where(np.arange(n) % 4 == 0, 5 + rng.random(n), rng.random(n))
+        v = v.astype(np.float32)
+        got = ss.otsu_threshold(v)
+        exp = ref.otsu_threshold(v)
+        assert got[0] == exp[0]
+        if exp[0]:
+            assert np.float32(got[1]).view(np.uint32) == np.float32(exp[1]).view(np.uint32), trial
+
+
+def test_binarize_exact(ss, ref):
+    rng = np.random.default_rng(47)
+    assert not ss.binarize(random_plot(rng, 12, 10), []).any()
+    p = np.zeros((10, 3), np.float32)
+    p[5:, 1] = 10
+    m = ss.binarize(p, [1])
+    assert np.array_equal(m[:, 1], (np.arange(10) >= 5).astype(np.uint8)) and not m[:, [0, 2]].any()
+    for rows, cols in [(40, 24), (2441, 96), (7, 1), (100, 33), (500, 1024)]:
+        tf = random_plot(rng, rows, cols)
+        tf[:, min(5, cols - 1)] = 1.5  # a constant column
+        act = np.sort(rng.choice(cols, size=max(1, cols // 2), replace=False)).astype(np.int32)
+        assert np.array_equal(ss.binarize(tf, act), ref.binarize_columns(tf, act))
+    # slice composition (test_detector.cpp:323-336)
+    tf = random_plot(rng, 30, 32)
+    act = [2, 3, 7, 11, 12, 13, 20, 28, 31]
+    whole = ref.binarize_columns(tf, act)
+    m = np.zeros((30, 32), np.uint8)
+    for c0, c1 in [(0, 10), (10, 25), (25, 32)]:
+        m = ss.binarize_columns(tf, act, c0, c1, m)
+    assert np.array_equal(m, whole)
+    with pytest.raises(ss.ValidationError):
+        ss.binarize(tf, [40])
+
+
+SES = [(3, 3), (1, 3), (3, 1), (5, 3)]
+
+
+def test_morphology_exact(ss, ref, ora):
+    rng = np.random.default_rng(61)
+    for trial in range(20):
+        m = random_mask(rng, 14, 18, 0.4) if trial % 2 else random_blob_mask(rng, 20, 37)
+        for se in SES:
+            for op in range(4):
+                got = ss.morphology(m, op, se)
+                assert np.array_equal(got, ref.morphology_cols(m, op, se)), (trial, se, op)
+                assert np.array_equal(got, ora.morphology(m, op, se))
+    # column-range form (test_detector.cpp:400-417)
+    for trial in range(10):
+        m = random_blob_mask(rng, 24, 37)
+        for op in range(4):
+            whole = ss.morphology(m, op, (3, 3))
+            d = np.zeros_like(m)
+            for c0, c1 in [(0, 13), (13, 29), (29, 37)]:
+                d = ss.morphology_cols(m, d, op, (3, 3), c0, c1)
+            assert np.array_equal(d, whole)
+    with pytest.raises(ss.ValidationError):
+        ss.morphology(np.zeros((6, 6), np.uint8), 0, (2, 3))
+
+
+@pytest.mark.parametrize("along_time", [False, True])
+def test_consolidate_exact(ss, ref, along_time):
+    rng = np.random.default_rng(79)
+    cases = [np.zeros((8, 8), np.uint8), np.ones((8, 8), np.uint8)]
+    cases += [random_blob_mask(rng, 22, 26) for _ in range(20)]
+    cases += [random_mask(rng, 37, 70, 0.5) for _ in range(5)]
+    cases += [random_blob_mask(rng, 300, 1024), random_mask(rng, 2441, 4096, 0.3), random_mask(rng, 1, 5, 0.9),
+              random_mask(rng, 3, 1, 1.0), random_blob_mask(rng, 64, 8192)]
+    for i, m in enumerate(cases):
+        assert np.array_equal(ss.consolidate(m, along_time), ref.consolidate(m, along_time)), i
+
+
+def test_components_exact(ss, ref):
+    # test_detector.cpp:477-541
+    m = np.zeros((4, 4), np.uint8)
+    m[1, 1] = m[2, 2] = 1
+    ext, lab = ss.label_components(m, 1)
+    assert len(ext) == 2 and lab[1, 1] != lab[2, 2]
+    rng = np.random.default_rng(83)
+    cases = []
+    for trial in range(60):
+        cases.append((random_mask(rng, 18, 22, 0.45) if trial % 2 == 0 else random_blob_mask(rng, 18, 22),
+                      trial % 3 + 1))
+    cases += [(random_mask(rng, 500, 1024, 0.5), 4), (random_blob_mask(rng, 2441, 4096), 4),
+              (np.ones((33, 70), np.uint8), 1), (np.zeros((5, 5), np.uint8), 1), (random_mask(rng, 1, 64, 0.5), 2),
+              (random_mask(rng, 64, 1, 0.5), 1)]
+    for i, (m, area) in enumerate(cases):
+        ext, lab = ss.label_components(m, area)
+        eext, elab = ref.label_components(m, area)
+        assert np.array_equal(ext, eext), i
+        assert np.array_equal(lab, elab), i
+        assert np.array_equal(ss.component_extents(m, area), eext)
+
+
+def test_detect_exact_small(ss, ref):
+    rng = np.random.default_rng(2024)
+    for rows, cols in [(128, 256), (200, 256), (500, 1024), (64, 31)]:
+        tf = burst_plot(rng, rows, cols)
+        got = ss.detect(tf, sample_rate_hz=1e6, start_seq=7)
+        exp = ref.detect(tf, start_seq=7, fs=1e6)
+        assert np.array_equal(got.psd.raw, exp["raw"])
+        assert np.array_equal(got.psd.smoothed, exp["smoothed"])
+        assert got.psd.noise_floor == exp["noise_floor"] and got.psd.threshold == exp["threshold"]
+        assert np.array_equal(got.active_columns, exp["active"])
+        assert np.array_equal(got.bin_boxes, exp["bin_boxes"])
+        assert np.array_equal(got.boxes, exp["boxes"])
