@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""Benchmark: spectrum-occupancy frames/s on B200 (and the reference CPU arm).
+
+Workload (BASELINE.json config 5, reference-parity mode "C5r"):
+one frame = one 100 ms capture of complex fp32 IQ at 100 MS/s -> a rectangular,
+hop-4096, F = 4096 TF plot (T = 2441 rows, 1,664 tail samples dropped exactly as
+proj/src/frontend.cpp:177) -> PSD / SG floor / prune -> per-column Otsu ->
+close3x3/open3x3/open1x3 -> 4-connected components -> boxes.  A step is one
+batch of `--batch` captures through ss_sense_batch (the fused C-ABI call).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Under torchrun each rank processes its own captures (weak scaling); boxes
+are gathered to every rank with one NCCL all_gather per step (the path's only
+exchange); time = max over ranks of CUDA-event time.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FS = 100e6
+N_FFT = 4096
+CAPTURE_S = 0.1
+ROWS = int(CAPTURE_S * FS) // N_FFT            # 2441
+SAMPLES = ROWS * N_FFT                         # processed samples per capture
+ALG_BYTES = SAMPLES * 8 + ROWS * N_FFT * 4     # K1 algorithmic bytes per capture (read IQ, write TF)
+ALG_FLOP64 = ROWS * 5 * N_FFT * 12             # conventional 5 N log2 N per row
+FP64_PEAK_TFLOPS = 33.9                        # measured DFMA peak, tools/fp64_peak.cu (profiles/fp64_peak.txt)
+METRIC = "spectrum-occupancy frames/s (config 5: 100 ms fp32 IQ capture @ 100 MS/s -> 2441x4096 TF plot -> boxes)"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=5)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        if not self.lines:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except (ValueError, IndexError):
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_reference(n_captures_total: int, threads: int, seconds_budget: float, seed: int = 2603):
+    """The reference's CPU path (oracle/_ref: the unmodified reference sources +
+    the FFTW-API shim) on host cores: make_plot + detect per capture, one
+    capture per std::thread at a time, all `threads` threads."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import numpy as np
+    import torch
+
+    from paper_2603_20481_b200 import signals
+    from _oracle import ref
+
+    R = ref()
+    # a few distinct captures, cycled (MemorySource-style)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    caps = [signals.synthesize_torch(signals.c5_scenario(i), device=dev)[:SAMPLES].cpu().numpy()
+            for i in range(4)]
+    iq = np.concatenate(caps)
+    # calibrate: one capture per thread
+    t0 = time.perf_counter()
+    R.bench_detect(iq, FS, N_FFT, ROWS, threads, threads)
+    one_round = time.perf_counter() - t0
+    rounds = max(1, int(seconds_budget / max(one_round, 1e-3)))
+    n = min(n_captures_total, rounds * threads) if n_captures_total else rounds * threads
+    boxes, secs = R.bench_detect(iq, FS, N_FFT, ROWS, n, threads)
+    return n / secs, n, secs, boxes
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    vals = []
+    total_caps, total_s = 0, 0.0
+    for i in range(args.warmup + args.steps):
+        v, n, secs, _ = cpu_reference(0, threads, args.ref_step_seconds)
+        if i >= args.warmup:
+            vals.append(v)
+            total_caps += n
+            total_s += secs
+    value = total_caps / total_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded config-5 bursts)",
+        "config": {"workload": "C5r: 100 ms fp32 IQ @ 100 MS/s, F=4096 rect hop 4096, T=2441",
+                   "captures_per_step": total_caps // max(args.steps, 1)},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "reference",
+                         "sample": f"{total_caps} captures over {args.steps} steps, make_plot+detect per capture "
+                                   f"(reference sources + FFTW-API shim; FFTW absent)"},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_20481_b200 import _native as NAT, signals, specsense as ss
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
+    ctx = ss.Context.get(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    lib = ctx.lib
+    B = args.batch
+    K = args.box_capacity
+
+    # ---- inputs: D distinct seeded captures, tiled to B captures, resident in HBM
+    D = min(args.distinct, B)
+    caps = [signals.synthesize_torch(signals.c5_scenario(1000 * rank + i), device="cuda")[:SAMPLES]
+            for i in range(D)]
+    iq = torch.empty(B * SAMPLES, dtype=torch.complex64, device="cuda")
+    for b in range(B):
+        iq[b * SAMPLES:(b + 1) * SAMPLES] = caps[b % D]
+    del caps
+    tf = torch.empty(B * SAMPLES, dtype=torch.float32, device="cuda")
+    outs = dict(
+        psd_raw=torch.empty((B, N_FFT), dtype=torch.float32, device="cuda"),
+        psd_smoothed=torch.empty((B, N_FFT), dtype=torch.float32, device="cuda"),
+        floor_thr=torch.empty((B, 2), dtype=torch.float32, device="cuda"),
+        active=torch.empty((B, N_FFT), dtype=torch.int32, device="cuda"),
+        n_active=torch.empty(B, dtype=torch.int32, device="cuda"),
+        boxes=torch.empty((B, K, 4), dtype=torch.float64, device="cuda"),
+        bin_boxes=torch.empty((B, K, 4), dtype=torch.int32, device="cuda"),
+        n_boxes=torch.empty(B, dtype=torch.int32, device="cuda"),
+    )
+    bout = NAT.BatchOut(*(C.c_void_p(v.data_ptr()) for v in outs.values()), K)
+    cfg = ss.DetectorConfig().c()
+    gathered = None
+    if ws > 1:
+        gathered = torch.empty((ws, B, K, 4), dtype=torch.float64, device="cuda")
+        gathered_n = torch.empty((ws, B), dtype=torch.int32, device="cuda")
+
+    def step(src_ptr, out):
+        ctx.check(lib.ss_sense_batch(ctx.h, C.c_void_p(src_ptr), NAT.SS_FMT_F32, N_FFT, ROWS, B,
+                                     C.c_uint64(0), C.c_double(FS), C.byref(cfg), C.c_void_p(tf.data_ptr()),
+                                     C.byref(out)))
+        if ws > 1:
+            dist.all_gather_into_tensor(gathered_n, outs["n_boxes"])
+            dist.all_gather_into_tensor(gathered, outs["boxes"])
+
+    for _ in range(args.warmup):
+        step(iq.data_ptr(), bout)
+    torch.cuda.synchronize()
+
+    # ---- timed: device-resident inputs (value)
+    lib.ss_enable_stage_timing(ctx.h, 1)
+    l0 = ctx.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step(iq.data_ptr(), bout)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    elapsed = ev0.elapsed_time(ev1) / 1e3
+    launches = ctx.launches() - l0
+    st = (C.c_double * 8)()
+    lib.ss_stage_times(ctx.h, st)
+    lib.ss_enable_stage_timing(ctx.h, 0)
+    if ws > 1:
+        t = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    sec_per_step = elapsed / args.steps
+    value = ws * B / sec_per_step
+    stage_names = ["k1_fft_mag_psd", "k2_psd", "k3_floor", "k4_binarize", "k5_consolidate", "k6_ccl", "h2d", "d2h"]
+    stage_ms = {n: st[i] / args.steps for i, n in enumerate(stage_names) if st[i] > 0}
+    k1_ms = stage_ms.get("k1_fft_mag_psd", float("nan"))
+    hbm_peak, peak_kind = _peaks()
+    achieved = B * ALG_BYTES / (k1_ms / 1e3) / 1e9
+    traffic = None
+    tp = ROOT / "profiles" / "k1_traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get("bytes_per_capture")
+        traffic = traffic * B if traffic else None
+
+    # ---- e2e: host (pinned) IQ in, host boxes out, through the same C-ABI call
+    Be = min(B, args.e2e_batch)
+    host_iq = torch.empty(Be * SAMPLES, dtype=torch.complex64, pin_memory=True)
+    host_iq.copy_(iq[: Be * SAMPLES])
+    host_out = {k: torch.empty((Be,) + tuple(v.shape[1:]), dtype=v.dtype, pin_memory=True) for k, v in outs.items()}
+    hout = NAT.BatchOut(*(C.c_void_p(v.data_ptr()) for v in host_out.values()), K)
+
+    def e2e_step():
+        ctx.check(lib.ss_sense_batch(ctx.h, C.c_void_p(host_iq.data_ptr()), NAT.SS_FMT_F32, N_FFT, ROWS, Be,
+                                     C.c_uint64(0), C.c_double(FS), C.byref(cfg), None, C.byref(hout)))
+
+    for _ in range(max(1, args.warmup // 2)):
+        e2e_step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_el = e0.elapsed_time(e1) / 1e3
+    if ws > 1:
+        t = torch.tensor([e2e_el], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_el = float(t.item())
+    e2e_val = ws * Be / (e2e_el / args.steps)
+    d2h = sum(v.numel() * v.element_size() for v in host_out.values())
+
+    # parity spot check of the timed outputs (device path == e2e path)
+    nb_dev = outs["n_boxes"][:Be].cpu()
+    assert torch.equal(nb_dev, host_out["n_boxes"]), "e2e and device-resident results differ"
+
+    # ---- CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        v, n, secs, _ = cpu_reference(0, threads, args.cpu_seconds)
+        cpu = {"value": v, "unit": "frames/s", "cores": threads, "kind": "reference",
+               "sample": f"{n} C5r captures (make_plot + detect each, one capture per thread) in {secs:.1f} s; "
+                         "reference sources + builder FFTW-API shim (FFTW absent)"}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * sec_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded config-5 captures (16 rectangular bursts, 5-40 MHz, 0.1-5 ms, 0-20 dB) on unit AWGN",
+            "config": {"workload": "C5r: 100 ms fp32 IQ @ 100 MS/s, F=4096 rect hop 4096 (T=2441), default DetectorConfig",
+                       "captures_per_step_per_gpu": B, "distinct_captures": D,
+                       "l2": f"inputs > L2 ({B * SAMPLES * 8 / 1e9:.1f} GB IQ per step, no flush needed)",
+                       "parallelism": f"capture-sharded x{ws}"},
+            "iq_gbps": value * SAMPLES * 32 / 1e9,
+            "stage_ms_per_step": stage_ms,
+            "roofline": {"bound": "hbm", "kernel": "k1_fft_mag_psd", "achieved": achieved, "peak": hbm_peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
+                         "alg_bytes_per_capture": ALG_BYTES,
+                         "fp64_tflops": B * ALG_FLOP64 / (k1_ms / 1e3) / 1e12, "fp64_peak_tflops": FP64_PEAK_TFLOPS},
+            "e2e": {"value": e2e_val, "unit": "frames/s", "h2d_bytes_per_step": Be * SAMPLES * 8,
+                    "d2h_bytes_per_step": d2h, "captures_per_step": Be},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=296, help="captures per step per GPU")
+    ap.add_argument("--distinct", type=int, default=8)
+    ap.add_argument("--e2e-batch", type=int, default=64)
+    ap.add_argument("--box-capacity", type=int, default=2048)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=8.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

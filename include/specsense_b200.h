@@ -101,11 +101,18 @@ void ss_close(ss_ctx* ctx);
 const char* ss_last_error(const ss_ctx* ctx);
 int ss_abi_version(void);
 void ss_default_detector_cfg(ss_detector_cfg* cfg);
-/* Enqueue subsequent work on `stream` (a cudaStream_t; NULL = the context's own). */
+/* Enqueue subsequent work on `stream` (a cudaStream_t; NULL = CUDA's legacy
+   default stream).  A new context uses its own non-blocking stream. */
 ss_status ss_set_stream(ss_ctx* ctx, void* stream);
 ss_status ss_synchronize(ss_ctx* ctx);
 /* Device kernel launches issued by this context so far (instrumentation). */
 int64_t ss_launch_count(const ss_ctx* ctx);
+/* Per-stage CUDA-event timing of the batch pipelines (on the context stream):
+   ss_enable_stage_timing resets the accumulators; ss_stage_times returns the
+   accumulated milliseconds of [K1 fft_mag, K2 psd, K3 floor, K4 binarize,
+   K5 consolidate, K6 ccl, H2D staging, D2H results] in ms8[0..7]. */
+ss_status ss_enable_stage_timing(ss_ctx* ctx, int on);
+ss_status ss_stage_times(const ss_ctx* ctx, double* ms8);
 
 /* ---- frontend --------------------------------------------------------- */
 /* frontend::make_plot / make_plots (frontend.cpp:157-183) over n_plots

@@ -51,6 +51,8 @@ SIGNATURES = {
     "ss_set_stream": (_I, [_P, _P]),
     "ss_synchronize": (_I, [_P]),
     "ss_launch_count": (C.c_int64, [_P]),
+    "ss_enable_stage_timing": (_I, [_P, _I]),
+    "ss_stage_times": (_I, [_P, C.POINTER(C.c_double)]),
     "ss_tf_plots": (_I, [_P, _P, _I, _I, _I, _I, _P]),
     "ss_psd_cols": (_I, [_P, _P, _I, _I, _I, _I, _P]),
     "ss_savgol_smooth": (_I, [_P, _P, _I, _I, _I, _P]),

@@ -38,6 +38,11 @@ struct ss_ctx {
     std::map<std::pair<int, int>, double*> sg;        // per (window, order)
     std::map<std::string, DevBuf> ws;                 // grow-only workspace
     int64_t launches = 0;
+    // optional per-stage timing (CUDA events on the context stream)
+    bool timing = false;
+    cudaEvent_t ev[2 * 8] = {};
+    bool ev_used[8] = {};
+    double stage_ms[8] = {};
 };
 
 namespace {
@@ -86,6 +91,27 @@ T* wsbuf(ss_ctx* c, const char* name, size_t count, ss_status* st) {
         var = wsbuf<T>(ctx, name, (count), &st_);     \
         if (!var) return st_;                         \
     } while (0)
+
+// stage ids for ss_stage_times: 0 K1 fft_mag(+PSD), 1 K2 psd_cols, 2 K3 floor,
+// 3 K4 binarize, 4 K5 consolidate, 5 K6 ccl, 6 H2D, 7 D2H
+void tmark(ss_ctx* ctx, int stage, int end) {
+    if (!ctx->timing) return;
+    cudaEvent_t& e = ctx->ev[2 * stage + end];
+    if (!e) cudaEventCreate(&e);
+    cudaEventRecord(e, ctx->stream);
+    if (end) ctx->ev_used[stage] = true;
+}
+
+// call after the stream is synchronised
+void tcollect(ss_ctx* ctx) {
+    if (!ctx->timing) return;
+    for (int i = 0; i < 8; ++i) {
+        if (!ctx->ev_used[i]) continue;
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, ctx->ev[2 * i], ctx->ev[2 * i + 1]) == cudaSuccess) ctx->stage_ms[i] += ms;
+        ctx->ev_used[i] = false;
+    }
+}
 
 ss_status twiddles(ss_ctx* ctx, int n_fft, const double2** out) {
     const int lg = ilog2(n_fft);
@@ -221,7 +247,9 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
     ss_status s = weights(ctx, cfg.savgol_window, cfg.savgol_order, &wts);
     if (s != SS_OK) return s;
     if (!psd_ready) {
+        tmark(ctx, 1, 0);
         SS_CK(ctx, ssb::psd_cols_launch(tf, n_plots, rows, cols, 0, cols, psd, ctx->stream));
+        tmark(ctx, 1, 1);
         ctx->launches += 1;
     }
     SS_WS(sm, float, "det.smoothed", static_cast<size_t>(n_plots) * cols);
@@ -244,7 +272,9 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
     F.active = out_dev.active ? out_dev.active : act;
     F.n_active = out_dev.n_active ? out_dev.n_active : nact;
     F.active_bits = abits;
+    tmark(ctx, 2, 0);
     SS_CK(ctx, ssb::floor_launch(F, ctx->stream));
+    tmark(ctx, 2, 1);
     ssb::BinarizeLaunch B;
     B.tf = tf;
     B.n_plots = n_plots;
@@ -252,14 +282,19 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
     B.cols = cols;
     B.active_bits = abits;
     B.mask_bits = m0;
+    tmark(ctx, 3, 0);
     SS_CK(ctx, ssb::binarize_launch(B, ctx->stream));
+    tmark(ctx, 3, 1);
+    tmark(ctx, 4, 0);
     SS_CK(ctx, ssb::consolidate_bits_launch(m0, n_plots, rows, cols, cfg.one_d_opening_along_time != 0, m1,
                                             ctx->stream));
+    tmark(ctx, 4, 1);
     ctx->launches += 3;
     const long long cap = out_dev.box_capacity > 0 ? out_dev.box_capacity : 0;
     SS_WS(ncomp, int, "det.n_comp", n_plots);
     int* overflow_h = nullptr;
     SS_CK(ctx, cudaMallocHost(&overflow_h, sizeof(int)));
+    tmark(ctx, 5, 0);
     s = run_ccl(ctx, m1, n_plots, rows, cols, cfg.min_component_area, default_pool(n_plots, rows, cols),
                 out_dev.n_boxes ? out_dev.n_boxes : ncomp, cap, nullptr,
                 reinterpret_cast<int*>(out_dev.bin_boxes), reinterpret_cast<double*>(out_dev.boxes), seq_dev, fs,
@@ -268,7 +303,9 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
         cudaFreeHost(overflow_h);
         return s;
     }
+    tmark(ctx, 5, 1);
     SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    tcollect(ctx);
     const int overflow = *overflow_h;
     cudaFreeHost(overflow_h);
     if (overflow) {
@@ -334,6 +371,8 @@ void ss_close(ss_ctx* ctx) {
     for (auto& kv : ctx->tw) cudaFree(kv.second);
     for (auto& kv : ctx->sg) cudaFree(kv.second);
     for (auto& kv : ctx->ws) cudaFree(kv.second.p);
+    for (cudaEvent_t e : ctx->ev)
+        if (e) cudaEventDestroy(e);
     cudaStreamDestroy(ctx->own);
     delete ctx;
 }
@@ -342,7 +381,7 @@ const char* ss_last_error(const ss_ctx* ctx) { return ctx ? ctx->err.c_str() : "
 
 ss_status ss_set_stream(ss_ctx* ctx, void* stream) {
     if (!ctx) return SS_EVALIDATION;
-    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+    ctx->stream = static_cast<cudaStream_t>(stream);  // NULL: the legacy default stream
     return SS_OK;
 }
 
@@ -353,6 +392,19 @@ ss_status ss_synchronize(ss_ctx* ctx) {
 }
 
 int64_t ss_launch_count(const ss_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+ss_status ss_enable_stage_timing(ss_ctx* ctx, int on) {
+    if (!ctx) return SS_EVALIDATION;
+    ctx->timing = on != 0;
+    for (double& v : ctx->stage_ms) v = 0.0;
+    return SS_OK;
+}
+
+ss_status ss_stage_times(const ss_ctx* ctx, double* ms8) {
+    if (!ctx || !ms8) return SS_EVALIDATION;
+    for (int i = 0; i < 8; ++i) ms8[i] = ctx->stage_ms[i];
+    return SS_OK;
+}
 
 ss_status ss_tf_plots(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int rows, int n_plots, float* tf) {
     if (!ctx) return SS_EVALIDATION;
@@ -596,7 +648,9 @@ ss_status ss_sense_batch(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int
     const void* diq = iq;
     if (!is_device_ptr(iq) || reinterpret_cast<uintptr_t>(iq) % 16 != 0) {
         SS_WS(stage, unsigned char, "sense.iq", nsamp * sbytes);
+        tmark(ctx, 6, 0);
         SS_CK(ctx, cudaMemcpyAsync(stage, iq, nsamp * sbytes, cudaMemcpyDefault, ctx->stream));
+        tmark(ctx, 6, 1);
         diq = stage;
     }
     const int cols = n_fft;
@@ -650,7 +704,9 @@ ss_status ss_sense_batch(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int
     L.rows_per_plot = rows;
     L.n_plots = n_plots;
     L.num_sms = ctx->num_sms;
+    tmark(ctx, 0, 0);
     SS_CK(ctx, ssb::fft_mag_launch(L, ctx->stream));
+    tmark(ctx, 0, 1);
     ctx->launches += 1;
     SS_WS(seq, unsigned long long, "det.seq", n_plots);
     std::vector<unsigned long long> hseq(static_cast<size_t>(n_plots));
@@ -660,6 +716,7 @@ ss_status ss_sense_batch(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int
     s = detect_device(ctx, tf, n_plots, rows, cols, seq, sample_rate_hz, *cfg, praw, true, dev);
     if (s != SS_OK) return s;
     if (host_out) {
+        tmark(ctx, 7, 0);
         auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
             if (!dst) return cudaSuccess;
             return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream);
@@ -672,7 +729,9 @@ ss_status ss_sense_batch(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int
         SS_CK(ctx, cp(out->boxes, dev.boxes, sizeof(ss_box) * n_plots * K));
         SS_CK(ctx, cp(out->bin_boxes, dev.bin_boxes, sizeof(ss_bin_box) * n_plots * K));
         SS_CK(ctx, cp(out->n_boxes, dev.n_boxes, sizeof(int32_t) * n_plots));
+        tmark(ctx, 7, 1);
         SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
+        tcollect(ctx);
     }
     if (out->n_boxes) {
         std::vector<int> nb(static_cast<size_t>(n_plots));

@@ -146,6 +146,16 @@ __device__ __forceinline__ int uf_find(int* parent, int x) {
     }
 }
 
+// Read-only find for the flatten pass: every thread writes only its own
+// parent entry there, so no path-halving store can overwrite a finished one.
+__device__ __forceinline__ int uf_root(const int* parent, int x) {
+    for (;;) {
+        const int p = __ldcg(parent + x);
+        if (p == x) return x;
+        x = p;
+    }
+}
+
 __device__ __forceinline__ void uf_unite(int* parent, int a, int b) {
     for (;;) {
         a = uf_find(parent, a);
@@ -193,7 +203,7 @@ __global__ void flatten_kernel(int rows, const int* row_off, const long long* pl
     for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
          k += static_cast<long long>(gridDim.x) * blockDim.x) {
         const long long i = base + k;
-        const int root = uf_find(ws.parent, static_cast<int>(i));
+        const int root = uf_root(ws.parent, static_cast<int>(i));
         ws.parent[i] = root;
         const int b = ws.run_begin[i], e = ws.run_end[i];
         atomicAdd(ws.area + root, static_cast<unsigned long long>(e - b));

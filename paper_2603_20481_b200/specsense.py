@@ -91,7 +91,12 @@ class Context:
 
 
 def _ctx() -> Context:
-    return Context.get(0)
+    """The device-0 context, bound to torch's current stream so the H2D/D2H
+    copies torch issues and our kernels are ordered on one stream."""
+    ctx = Context.get(0)
+    torch = _torch()
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    return ctx
 
 
 def _dev(a: np.ndarray, dtype=None):
