@@ -135,6 +135,10 @@ ss_status ss_savgol_smooth(ss_ctx* ctx, const float* values, int n, int window, 
    *n_active (HOST int). */
 ss_status ss_floor(ss_ctx* ctx, const float* raw, int n, const ss_detector_cfg* cfg,
                    float* smoothed, float* floor_thr, int32_t* active, int32_t* n_active);
+/* prune_columns (detector.cpp:250-255): active = {k : raw[k] >= threshold}
+   ascending; *n_active (HOST). */
+ss_status ss_prune(ss_ctx* ctx, const float* raw, int n, float threshold, int32_t* active,
+                   int32_t* n_active);
 /* otsu_threshold (detector.cpp:257-271); *valid, *threshold are HOST. */
 ss_status ss_otsu(ss_ctx* ctx, const float* values, int n, int32_t* valid, float* threshold);
 /* binarize_columns (detector.cpp:273-335): writes columns [c0, c1) of the

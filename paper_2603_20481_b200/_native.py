@@ -9,7 +9,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libspecsense_b200.so"
+_LIB_PATH = Path(os.environ.get("SSB_LIB_PATH") or Path(__file__).resolve().parent / "_lib" / "libspecsense_b200.so")
 
 SS_OK, SS_EVALIDATION, SS_EFORMAT, SS_ECUDA, SS_ENOMEM, SS_EUNSUPPORTED, SS_ECAPACITY = range(7)
 SS_FMT_F32, SS_FMT_I16 = 0, 1
@@ -57,6 +57,7 @@ SIGNATURES = {
     "ss_psd_cols": (_I, [_P, _P, _I, _I, _I, _I, _P]),
     "ss_savgol_smooth": (_I, [_P, _P, _I, _I, _I, _P]),
     "ss_floor": (_I, [_P, _P, _I, C.POINTER(DetectorCfg), _P, _P, _P, C.POINTER(C.c_int32)]),
+    "ss_prune": (_I, [_P, _P, _I, C.c_float, _P, C.POINTER(C.c_int32)]),
     "ss_otsu": (_I, [_P, _P, _I, C.POINTER(C.c_int32), C.POINTER(C.c_float)]),
     "ss_binarize_cols": (_I, [_P, _P, _I, _I, _P, _I, _I, _I, _P]),
     "ss_morph_cols": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _P]),

@@ -16,13 +16,14 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-LIB = PKG / "_lib"
+LIB = Path(os.environ.get("SSB_BUILD_DIR", PKG / "_lib"))
 OBJ = LIB / "obj"
 SO = LIB / "libspecsense_b200.so"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
+EXTRA = os.environ.get("SSB_NVCC_EXTRA", "").split()
+NVCC_FLAGS = EXTRA + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
               "-Xptxas", "-v", f"-I{ROOT / 'include'}", f"-I{CSRC}"] + ARCH
 CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra",
              f"-I{ROOT / 'include'}", f"-I{CSRC}", "-I/usr/local/cuda/include"]

@@ -231,11 +231,214 @@ __global__ void __launch_bounds__(kBinThreads) binarize_kernel(BinarizeLaunch a)
     }
 }
 
+bool binarize_tile_ok(const BinarizeLaunch& L);
+cudaError_t binarize_tile_launch(const BinarizeLaunch& L, cudaStream_t st);
+
 cudaError_t binarize_launch(const BinarizeLaunch& L, cudaStream_t st) {
     if (L.n_plots <= 0 || L.rows <= 0 || L.cols <= 0) return cudaSuccess;
+    if (binarize_tile_ok(L) && !L.col_valid) return binarize_tile_launch(L, st);
     const int W = (L.cols + 31) / 32;
     dim3 grid(W, L.n_plots);
     binarize_kernel<<<grid, kBinThreads, 0, st>>>(L);
+    return cudaGetLastError();
+}
+
+} // namespace ssb
+
+// ---------------------------------------------------------------------------
+// binarize_tile_kernel: the batch path for plots of <= kTileMaxRows rows.
+// One CTA per (plot, 8-column group): the group's T x 8 values (32 bytes per
+// row) are pulled into shared memory once with cp.async (LDGSTS, 16-byte,
+// L1-bypassing; the whole column block in flight at once), and sweeps A/B/C
+// run from shared memory -- one HBM read of the active columns in total.
+// The output byte (8 mask bits) lands in the bit-packed mask word in place
+// (little-endian: byte g of word w = columns 32w + 8g .. +7).
+constexpr int kTileCols = 8;
+constexpr int kTileMaxRows = 6144;
+
+namespace ssb {
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaunch a) {
+    extern __shared__ __align__(16) float bt_vals[];      // rows x 8
+    __shared__ uint32_t hist[kTileCols * kHistStride];
+    __shared__ float s_lo[kBinWarps][kTileCols], s_hi[kBinWarps][kTileCols];
+    __shared__ float c_lo[kTileCols], c_scale[kTileCols], c_thr[kTileCols];
+    __shared__ double c_span[kTileCols];
+    __shared__ int c_use[kTileCols];
+
+    const int grp = blockIdx.x;          // 8-column group
+    const int p = blockIdx.y;
+    const int rows = a.rows, cols = a.cols;
+    const int W = (cols + 31) / 32;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t abyte = (a.active_bits[static_cast<long long>(p) * W + grp / 4] >> (8 * (grp & 3))) & 0xffu;
+    uint8_t* mbytes = reinterpret_cast<uint8_t*>(a.mask_bits + static_cast<long long>(p) * rows * W);
+    const int col0 = grp * kTileCols;
+    if (abyte == 0) {
+        for (int r = tid; r < rows; r += kBinThreads) mbytes[static_cast<long long>(r) * W * 4 + grp] = 0;
+        return;
+    }
+    // ---- load the T x 8 block (2 x 16 B per row)
+    const float* src = a.tf + static_cast<long long>(p) * rows * cols + col0;
+    for (int e = tid; e < 2 * rows; e += kBinThreads) {
+        const int r = e >> 1, h = e & 1;
+        cp_async16(bt_vals + r * kTileCols + 4 * h, src + static_cast<long long>(r) * cols + 4 * h);
+    }
+    for (int i = tid; i < kTileCols * kHistStride; i += kBinThreads) hist[i] = 0;
+    cp_async_wait_all();
+    __syncthreads();
+
+    // ---- sweep A: column c = tid & 7 over rows tid>>3, +32 ...
+    const int c = tid & 7;
+    float lo = INFINITY, hi = -INFINITY;
+    for (int r = tid >> 3; r < rows; r += kBinThreads / kTileCols) {
+        const float x = bt_vals[r * kTileCols + c];
+        lo = (x < lo) ? x : lo;
+        hi = (hi < x) ? x : hi;
+    }
+    // reduce the 4 lanes of a warp sharing column c (lane, lane^8, lane^16, lane^24)
+#pragma unroll
+    for (int o = 8; o < 32; o <<= 1) {
+        const float ol = __shfl_xor_sync(0xffffffffu, lo, o), oh = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = (ol < lo) ? ol : lo;
+        hi = (hi < oh) ? oh : hi;
+    }
+    if (lane < kTileCols) {
+        s_lo[warp][lane] = lo;
+        s_hi[warp][lane] = hi;
+    }
+    __syncthreads();
+    if (tid < kTileCols) {
+        float l = s_lo[0][tid], h = s_hi[0][tid];
+        for (int q = 1; q < kBinWarps; ++q) {
+            l = (s_lo[q][tid] < l) ? s_lo[q][tid] : l;
+            h = (h < s_hi[q][tid]) ? s_hi[q][tid] : h;
+        }
+        const float scale = __fdiv_rn(256.0f, __fsub_rn(h, l));
+        const bool valid = h > l && isfinite(scale);
+        const bool act = (col0 + tid < cols) && ((abyte >> tid) & 1u);
+        c_lo[tid] = l;
+        c_scale[tid] = scale;
+        c_span[tid] = __dsub_rn(static_cast<double>(h), static_cast<double>(l));
+        c_use[tid] = (act && valid) ? 1 : 0;
+        c_thr[tid] = INFINITY;
+    }
+    __syncthreads();
+
+    // ---- sweep B: histograms from shared memory
+    if (c_use[c]) {
+        const float clo = c_lo[c], csc = c_scale[c];
+        uint32_t* h = hist + c * kHistStride;
+        for (int r = tid >> 3; r < rows; r += kBinThreads / kTileCols) {
+            int b = __float2int_rz(__fmul_rn(__fsub_rn(bt_vals[r * kTileCols + c], clo), csc));
+            b = b > 255 ? 255 : b;
+            atomicAdd(h + b, 1u);
+        }
+    }
+    __syncthreads();
+
+    // ---- Otsu: warp w handles column w
+    if (warp < kTileCols && c_use[warp]) {
+        const int cc = warp;
+        const uint32_t* h = hist + cc * kHistStride;
+        unsigned long long cnt[8], wsum[8];
+        unsigned long long lc = 0, ls = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int bin = lane * 8 + q;
+            lc += h[bin];
+            ls += static_cast<unsigned long long>(bin) * h[bin];
+            cnt[q] = lc;
+            wsum[q] = ls;
+        }
+        unsigned long long pc = lc, ps = ls;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long tc = __shfl_up_sync(0xffffffffu, pc, o);
+            const unsigned long long ts = __shfl_up_sync(0xffffffffu, ps, o);
+            if (lane >= o) {
+                pc += tc;
+                ps += ts;
+            }
+        }
+        const unsigned long long total = __shfl_sync(0xffffffffu, pc, 31);
+        const double sum_all = static_cast<double>(__shfl_sync(0xffffffffu, ps, 31));
+        pc -= lc;
+        ps -= ls;
+        double best_v = -1.0;
+        int best_i = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const unsigned long long w0 = pc + cnt[q];
+            const unsigned long long w1 = total - w0;
+            const double sum0 = static_cast<double>(ps + wsum[q]);
+            double var = 0.0;
+            if (w0 > 0 && w1 > 0) {
+                const double mu0 = __ddiv_rn(sum0, static_cast<double>(w0));
+                const double mu1 = __ddiv_rn(__dsub_rn(sum_all, sum0), static_cast<double>(w1));
+                const double d = __dsub_rn(mu0, mu1);
+                var = __dmul_rn(__dmul_rn(__dmul_rn(static_cast<double>(w0), static_cast<double>(w1)), d), d);
+            }
+            if (var > best_v) {
+                best_v = var;
+                best_i = lane * 8 + q;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, best_v, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+            if (ov > best_v || (ov == best_v && oi < best_i)) {
+                best_v = ov;
+                best_i = oi;
+            }
+        }
+        if (lane == 0) {
+            const double lod = static_cast<double>(c_lo[cc]);
+            const double e = __ddiv_rn(__dmul_rn(static_cast<double>(best_i) + 1.0, c_span[cc]), 256.0);
+            c_thr[cc] = __double2float_rn(__dadd_rn(lod, e));
+        }
+    }
+    __syncthreads();
+    if (a.col_thr && tid < kTileCols && col0 + tid < cols)
+        a.col_thr[static_cast<long long>(p) * cols + col0 + tid] = c_thr[tid];
+
+    // ---- sweep C: one row per thread, 8 compares -> one mask byte
+    float thr[kTileCols];
+#pragma unroll
+    for (int q = 0; q < kTileCols; ++q) thr[q] = c_thr[q];
+    for (int r = tid; r < rows; r += kBinThreads) {
+        const float4 x0 = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols);
+        const float4 x1 = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols + 4);
+        const uint32_t b = (x0.x > thr[0] ? 1u : 0u) | (x0.y > thr[1] ? 2u : 0u) | (x0.z > thr[2] ? 4u : 0u) |
+                           (x0.w > thr[3] ? 8u : 0u) | (x1.x > thr[4] ? 16u : 0u) | (x1.y > thr[5] ? 32u : 0u) |
+                           (x1.z > thr[6] ? 64u : 0u) | (x1.w > thr[7] ? 128u : 0u);
+        mbytes[static_cast<long long>(r) * W * 4 + grp] = static_cast<uint8_t>(b);
+    }
+}
+
+bool binarize_tile_ok(const BinarizeLaunch& L) {
+    return L.mask_bits && !L.mask_u8 && L.cols % 32 == 0 && L.rows <= kTileMaxRows && L.rows > 0;
+}
+
+cudaError_t binarize_tile_launch(const BinarizeLaunch& L, cudaStream_t st) {
+    const size_t smem = sizeof(float) * kTileCols * static_cast<size_t>(L.rows);
+    static int attr_set = 0;
+    if (attr_set < static_cast<int>(smem)) {
+        cudaError_t e = cudaFuncSetAttribute(binarize_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kTileCols * kTileMaxRows * static_cast<int>(sizeof(float)));
+        if (e != cudaSuccess) return e;
+        attr_set = kTileCols * kTileMaxRows * static_cast<int>(sizeof(float));
+    }
+    dim3 grid(L.cols / kTileCols, L.n_plots);
+    binarize_tile_kernel<<<grid, kBinThreads, smem, st>>>(L);
     return cudaGetLastError();
 }
 

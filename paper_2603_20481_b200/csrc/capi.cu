@@ -487,6 +487,23 @@ ss_status ss_floor(ss_ctx* ctx, const float* raw, int n, const ss_detector_cfg* 
     return SS_OK;
 }
 
+ss_status ss_prune(ss_ctx* ctx, const float* raw, int n, float threshold, int32_t* active, int32_t* n_active) {
+    if (!ctx) return SS_EVALIDATION;
+    if (n < 0) return fail(ctx, SS_EVALIDATION, "negative PSD length");
+    if (n == 0) {
+        if (n_active) *n_active = 0;
+        return SS_OK;
+    }
+    SS_WS(nact, int, "prune.n_active", 1);
+    SS_CK(ctx, ssb::prune_launch(raw, n, threshold, active, nact, ctx->stream));
+    ctx->launches += 1;
+    int h = 0;
+    SS_CK(ctx, cudaMemcpyAsync(&h, nact, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (n_active) *n_active = h;
+    return SS_OK;
+}
+
 ss_status ss_otsu(ss_ctx* ctx, const float* values, int n, int32_t* valid, float* threshold) {
     if (!ctx) return SS_EVALIDATION;
     if (n < 1) return fail(ctx, SS_EVALIDATION, "otsu on an empty column");

@@ -123,10 +123,13 @@ struct FftPlan {
         for (int q = 0; q < p; ++q) s *= radix(q);
         return s;
     }
-    // offset of pass p's twiddle block in the per-N table
+    // Twiddle block of pass p >= 1 (Ns > 1): (R-1)*Ns entries, tw[r*k*s] at
+    // (r-1)*Ns + k with s = N/(Ns*R) -- a pass-major re-layout of the
+    // canonical table so a warp's 32 lanes read 32 consecutive entries.
+    __host__ __device__ static constexpr int tw_block(int p) { return (radix(p) - 1) * ns(p); }
     __host__ __device__ static constexpr int tw_off(int p) {
         int o = 0;
-        for (int q = 1; q < p; ++q) o += (radix(q) - 1) * ns(q);
+        for (int q = 1; q < p; ++q) o += tw_block(q);
         return o;
     }
     __host__ __device__ static constexpr int tw_size() { return tw_off(NP); }
@@ -198,25 +201,36 @@ __device__ __forceinline__ void passes_from(cd* v, int j, const double2* tw, dou
     }
 }
 
+__device__ __forceinline__ double rsqrt_seed(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    return y;
+}
+
 // |X| rounded to float, bit-identical to float(sqrt(fma(re, re, im*im))).
-// Fast path: float rsqrt seed + one Newton step in double gives sqrt(q) to
-// < 2^10 double ulps; when that estimate is > 2^13 ulps away from a float
-// rounding midpoint, rounding it to float equals rounding the correctly
-// rounded double sqrt.  Otherwise (p ~ 2^-15) and outside [2^-120, 2^120],
-// fall back to the IEEE __dsqrt_rn.  DESIGN.md §3.3 has the error budget.
-__device__ __forceinline__ float mag_f32(double re, double im) {
+// Fast path: MUFU.RSQ64H seed (rel. err <= 2^-20, measured) + one Newton
+// step in double gives sqrt(q) within 2^12.6 double ulps; when that estimate
+// is more than 2^16 ulps from a float rounding midpoint (low 29 mantissa bits
+// vs 2^28), rounding it to float equals rounding the correctly rounded double
+// sqrt (no midpoint lies between them).  Otherwise (p ~ 2^-12) and for q outside
+// [2^-120, 2^120], the IEEE __dsqrt_rn + F2F.  *fbits gets the float's bits;
+// returns true on the fast path (result a normal float).
+__device__ __forceinline__ bool mag_bits(double re, double im, uint32_t* fbits) {
     const double q = __fma_rn(re, re, __dmul_rn(im, im));
     if (q >= 0x1p-120 && q <= 0x1p120) {
-        const float yf = rsqrtf(__double2float_rn(q));
-        const double y = static_cast<double>(yf);
+        const double y = rsqrt_seed(q);
         const double s0 = __dmul_rn(q, y);
         const double d = __fma_rn(-s0, s0, q);
         const double s1 = __fma_rn(d, __dmul_rn(0.5, y), s0);
-        const uint32_t low = static_cast<uint32_t>(__double_as_longlong(s1)) & 0x1FFFFFFFu;
-        const int dist = static_cast<int>(low) - (1 << 28);
-        if (dist > 8192 || dist < -8192) return __double2float_rn(s1);
+        const uint32_t low29 = static_cast<uint32_t>(__double2loint(s1)) & 0x1FFFFFFFu;
+        const int dist = static_cast<int>(low29) - (1 << 28);
+        if (dist > 65536 || dist < -65536) {
+            *fbits = __float_as_uint(__double2float_rn(s1));
+            return true;
+        }
     }
-    return __double2float_rn(__dsqrt_rn(q));
+    *fbits = __float_as_uint(__double2float_rn(__dsqrt_rn(q)));
+    return false;
 }
 
 // ------------------------------------------------------------------ kernel
@@ -301,20 +315,26 @@ fft_mag_kernel(FftArgs a) {
         {
             constexpr int R0 = PL::radix(0);
             constexpr int U0 = PL::P / R0;
+            if constexpr (FMT == 0) {
 #pragma unroll
-            for (int u = 0; u < U0; ++u) {
-                const int b = j + PL::TPR * u;
+                for (int u = 0; u < U0; ++u)
 #pragma unroll
-                for (int r = 0; r < R0; ++r) {
-                    const int s = g * N + b + r * (N / R0);
-                    if constexpr (FMT == 0) {
+                    for (int r = 0; r < R0; ++r) {
+                        const int s = g * N + j + PL::TPR * u + r * (N / R0);
                         const float2 x = valid ? reinterpret_cast<const float2*>(stage)[s] : make_float2(0.f, 0.f);
                         v[u * R0 + r] = {static_cast<double>(x.x), static_cast<double>(x.y)};
-                    } else {
+                    }
+            } else {
+#pragma unroll
+                for (int u = 0; u < U0; ++u) {
+                    const int b = j + PL::TPR * u;
+#pragma unroll
+                    for (int r = 0; r < R0; ++r) {
+                        const int s = g * N + b + r * (N / R0);
                         const short2 x = valid ? reinterpret_cast<const short2*>(stage)[s] : make_short2(0, 0);
                         // frontend.cpp:383: raw * (1.0f/32768) (exact), promoted to double
-                        v[u * R0 + r] = {static_cast<double>(__fmul_rn(static_cast<float>(x.x), 1.0f / 32768.0f)),
-                                         static_cast<double>(__fmul_rn(static_cast<float>(x.y), 1.0f / 32768.0f))};
+                        v[u * R0 + r] = {__dmul_rn(static_cast<double>(x.x), 0x1p-15),
+                                         __dmul_rn(static_cast<double>(x.y), 0x1p-15)};
                     }
                 }
             }
@@ -336,11 +356,13 @@ fft_mag_kernel(FftArgs a) {
                 for (int r = 0; r < RL; ++r) {
                     const int q = j + PL::TPR * u + r * NSL;
                     const int k = (q + N / 2) & (N - 1);
-                    const float m = mag_f32(v[u * RL + r].re, v[u * RL + r].im);
-                    if (valid && out) out[k] = m;
+                    uint32_t mb;
+                    const bool fast = mag_bits(v[u * RL + r].re, v[u * RL + r].im, &mb);
+                    if (valid && out) out[k] = __uint_as_float(mb);
                     if constexpr (PSD) {
                         if (valid) {
-                            const double md = static_cast<double>(m);
+                            (void)fast;
+                            const double md = static_cast<double>(__uint_as_float(mb));
                             acc[u * RL + r] = __fma_rn(md, md, acc[u * RL + r]);
                         }
                     }
@@ -355,7 +377,9 @@ fft_mag_kernel(FftArgs a) {
                 for (int r = 0; r < RL; ++r) {
                     const int q = j + PL::TPR * u + r * NSL;
                     const int k = (q + N / 2) & (N - 1);
-                    mrow[k] = mag_f32(v[u * RL + r].re, v[u * RL + r].im);
+                    uint32_t mb;
+                    mag_bits(v[u * RL + r].re, v[u * RL + r].im, &mb);
+                    mrow[k] = __uint_as_float(mb);
                 }
             }
             __syncthreads();
@@ -429,9 +453,10 @@ static void build_tw(std::vector<double2>& out) {
     out.assign(PL::tw_size() > 0 ? PL::tw_size() : 1, make_double2(0, 0));
     for (int p = 1; p < PL::NP; ++p) {
         const int R = PL::radix(p), NS = PL::ns(p);
+        const size_t s = static_cast<size_t>(N / (NS * R));
+        double2* blk = out.data() + PL::tw_off(p);
         for (int r = 1; r < R; ++r)
-            for (int k = 0; k < NS; ++k)
-                out[PL::tw_off(p) + (r - 1) * NS + k] = canon[static_cast<size_t>(r) * k * (N / (NS * R))];
+            for (int k = 0; k < NS; ++k) blk[(r - 1) * NS + k] = canon[r * k * s];
     }
 }
 

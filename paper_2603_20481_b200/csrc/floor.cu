@@ -243,6 +243,29 @@ cudaError_t psd_cols_launch(const float* tf, int n_plots, int rows, int cols, in
     return cudaGetLastError();
 }
 
+// prune_columns (detector.cpp:250-255) against a given threshold: one CTA,
+// ascending compaction by block scan.
+__global__ void __launch_bounds__(kFloorThreads) prune_kernel(const float* raw, int n, float thr, int* active,
+                                                               int* n_active) {
+    __shared__ int red_i[32];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int chunk = (n + nt - 1) / nt;
+    const int k0 = tid * chunk;
+    const int k1 = min(n, k0 + chunk);
+    int cnt = 0;
+    for (int k = k0; k < k1; ++k) cnt += raw[k] >= thr ? 1 : 0;
+    int total = 0;
+    int off = block_excl_scan(cnt, red_i, &total);
+    for (int k = k0; k < k1; ++k)
+        if (raw[k] >= thr) active[off++] = k;
+    if (tid == 0) *n_active = total;
+}
+
+cudaError_t prune_launch(const float* raw, int n, float thr, int* active, int* n_active, cudaStream_t st) {
+    prune_kernel<<<1, kFloorThreads, 0, st>>>(raw, n, thr, active, n_active);
+    return cudaGetLastError();
+}
+
 __global__ void libm_test_kernel(const float* x, long long n, int which, bool fma_variant, float* out) {
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x)

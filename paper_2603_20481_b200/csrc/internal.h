@@ -46,6 +46,7 @@ struct FloorLaunch {
     uint32_t* active_bits = nullptr;  // n_plots x W (W = ceil(n/32)), may be null
 };
 cudaError_t floor_launch(const FloorLaunch& L, cudaStream_t st);
+cudaError_t prune_launch(const float* raw, int n, float thr, int* active, int* n_active, cudaStream_t st);
 cudaError_t savgol_launch(const float* v, int n, int window, const double* weights, float* out,
                           cudaStream_t st);
 cudaError_t libm_test_launch(const float* x, long long n, int which, bool fma_variant, float* out,
