@@ -231,12 +231,11 @@ __global__ void __launch_bounds__(kBinThreads) binarize_kernel(BinarizeLaunch a)
     }
 }
 
-bool binarize_tile_ok(const BinarizeLaunch& L);
 cudaError_t binarize_tile_launch(const BinarizeLaunch& L, cudaStream_t st);
 
 cudaError_t binarize_launch(const BinarizeLaunch& L, cudaStream_t st) {
     if (L.n_plots <= 0 || L.rows <= 0 || L.cols <= 0) return cudaSuccess;
-    if (binarize_tile_ok(L) && !L.col_valid) return binarize_tile_launch(L, st);
+    if (L.mask_planes) return binarize_tile_launch(L, st);  // caller checked binarize_tile_ok
     const int W = (L.cols + 31) / 32;
     dim3 grid(W, L.n_plots);
     binarize_kernel<<<grid, kBinThreads, 0, st>>>(L);
@@ -279,10 +278,10 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     const int W = (cols + 31) / 32;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t abyte = (a.active_bits[static_cast<long long>(p) * W + grp / 4] >> (8 * (grp & 3))) & 0xffu;
-    uint8_t* mbytes = reinterpret_cast<uint8_t*>(a.mask_bits + static_cast<long long>(p) * rows * W);
+    uint8_t* plane = a.mask_planes + (static_cast<long long>(p) * (cols / kTileCols) + grp) * rows;
     const int col0 = grp * kTileCols;
     if (abyte == 0) {
-        for (int r = tid; r < rows; r += kBinThreads) mbytes[static_cast<long long>(r) * W * 4 + grp] = 0;
+        for (int r = tid; r < rows; r += kBinThreads) plane[r] = 0;
         return;
     }
     // ---- load the T x 8 block (2 x 16 B per row)
@@ -420,13 +419,11 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
         const uint32_t b = (x0.x > thr[0] ? 1u : 0u) | (x0.y > thr[1] ? 2u : 0u) | (x0.z > thr[2] ? 4u : 0u) |
                            (x0.w > thr[3] ? 8u : 0u) | (x1.x > thr[4] ? 16u : 0u) | (x1.y > thr[5] ? 32u : 0u) |
                            (x1.z > thr[6] ? 64u : 0u) | (x1.w > thr[7] ? 128u : 0u);
-        mbytes[static_cast<long long>(r) * W * 4 + grp] = static_cast<uint8_t>(b);
+        plane[r] = static_cast<uint8_t>(b);
     }
 }
 
-bool binarize_tile_ok(const BinarizeLaunch& L) {
-    return L.mask_bits && !L.mask_u8 && L.cols % 32 == 0 && L.rows <= kTileMaxRows && L.rows > 0;
-}
+bool binarize_tile_ok(int rows, int cols) { return cols % 32 == 0 && rows <= kTileMaxRows && rows > 0; }
 
 cudaError_t binarize_tile_launch(const BinarizeLaunch& L, cudaStream_t st) {
     const size_t smem = sizeof(float) * kTileCols * static_cast<size_t>(L.rows);

@@ -215,22 +215,30 @@ __device__ __forceinline__ double rsqrt_seed(double x) {
 // sqrt (no midpoint lies between them).  Otherwise (p ~ 2^-12) and for q outside
 // [2^-120, 2^120], the IEEE __dsqrt_rn + F2F.  *fbits gets the float's bits;
 // returns true on the fast path (result a normal float).
-__device__ __forceinline__ bool mag_bits(double re, double im, uint32_t* fbits) {
-    const double q = __fma_rn(re, re, __dmul_rn(im, im));
-    if (q >= 0x1p-120 && q <= 0x1p120) {
+// Magnitudes of the thread's P outputs, branch-free on the fast path; lanes
+// flagged in the warp-uniform slow pass redo theirs with __dsqrt_rn.
+template <int P>
+__device__ __forceinline__ void mags(const cd* v, float* m) {
+    uint32_t slow = 0;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+        const double q = __fma_rn(v[i].re, v[i].re, __dmul_rn(v[i].im, v[i].im));
         const double y = rsqrt_seed(q);
         const double s0 = __dmul_rn(q, y);
         const double d = __fma_rn(-s0, s0, q);
         const double s1 = __fma_rn(d, __dmul_rn(0.5, y), s0);
         const uint32_t low29 = static_cast<uint32_t>(__double2loint(s1)) & 0x1FFFFFFFu;
         const int dist = static_cast<int>(low29) - (1 << 28);
-        if (dist > 65536 || dist < -65536) {
-            *fbits = __float_as_uint(__double2float_rn(s1));
-            return true;
-        }
+        const bool ok = q >= 0x1p-120 && q <= 0x1p120 && (dist > 65536 || dist < -65536);
+        m[i] = __double2float_rn(s1);
+        slow |= ok ? 0u : (1u << i);
     }
-    *fbits = __float_as_uint(__double2float_rn(__dsqrt_rn(q)));
-    return false;
+    if (__any_sync(0xffffffffu, slow != 0)) {
+#pragma unroll
+        for (int i = 0; i < P; ++i)
+            if ((slow >> i) & 1u)
+                m[i] = __double2float_rn(__dsqrt_rn(__fma_rn(v[i].re, v[i].re, __dmul_rn(v[i].im, v[i].im))));
+    }
 }
 
 // ------------------------------------------------------------------ kernel
@@ -348,6 +356,8 @@ fft_mag_kernel(FftArgs a) {
         constexpr int RL = PL::radix(PL::NP - 1);
         constexpr int NSL = PL::ns(PL::NP - 1);
         constexpr int UL = PL::P / RL;
+        float m[PL::P];
+        mags<PL::P>(v, m);
         if constexpr (G == 1) {
             float* out = a.tf ? a.tf + row * N : nullptr;
 #pragma unroll
@@ -356,13 +366,10 @@ fft_mag_kernel(FftArgs a) {
                 for (int r = 0; r < RL; ++r) {
                     const int q = j + PL::TPR * u + r * NSL;
                     const int k = (q + N / 2) & (N - 1);
-                    uint32_t mb;
-                    const bool fast = mag_bits(v[u * RL + r].re, v[u * RL + r].im, &mb);
-                    if (valid && out) out[k] = __uint_as_float(mb);
+                    if (valid && out) out[k] = m[u * RL + r];
                     if constexpr (PSD) {
                         if (valid) {
-                            (void)fast;
-                            const double md = static_cast<double>(__uint_as_float(mb));
+                            const double md = static_cast<double>(m[u * RL + r]);
                             acc[u * RL + r] = __fma_rn(md, md, acc[u * RL + r]);
                         }
                     }
@@ -377,9 +384,7 @@ fft_mag_kernel(FftArgs a) {
                 for (int r = 0; r < RL; ++r) {
                     const int q = j + PL::TPR * u + r * NSL;
                     const int k = (q + N / 2) & (N - 1);
-                    uint32_t mb;
-                    mag_bits(v[u * RL + r].re, v[u * RL + r].im, &mb);
-                    mrow[k] = __uint_as_float(mb);
+                    mrow[k] = m[u * RL + r];
                 }
             }
             __syncthreads();

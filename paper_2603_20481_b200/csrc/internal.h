@@ -64,12 +64,15 @@ struct BinarizeLaunch {
     int cols = 0;
     const uint32_t* active_bits = nullptr;  // n_plots x W
     uint32_t* mask_bits = nullptr;      // n_plots x rows x W (bit mode) or null
+    uint8_t* mask_planes = nullptr;     // n_plots x (cols/8) x rows byte planes (tile path) or null
     uint8_t* mask_u8 = nullptr;         // rows x cols (u8 mode, columns [c0,c1)) or null
     int c0 = 0, c1 = 0;                 // u8 mode column range
     float* col_thr = nullptr;           // optional n_plots x cols thresholds (+inf inactive)
     int* col_valid = nullptr;           // optional n_plots x cols: active && non-constant
 };
 cudaError_t binarize_launch(const BinarizeLaunch& L, cudaStream_t st);
+// true when the smem-resident tile kernel (byte-plane output) handles this shape
+bool binarize_tile_ok(int rows, int cols);
 
 // ---- K5 morph.cu
 cudaError_t pack_u8_launch(const uint8_t* m, int n_plots, int rows, int cols, uint32_t* bits,
@@ -77,8 +80,10 @@ cudaError_t pack_u8_launch(const uint8_t* m, int n_plots, int rows, int cols, ui
 cudaError_t unpack_launch(const uint32_t* bits, int n_plots, int rows, int cols, uint8_t* m,
                           cudaStream_t st);
 // close 3x3 -> open 3x3 -> open 1x3 (3x1 if along_time), bit-packed, fused.
-cudaError_t consolidate_bits_launch(const uint32_t* in, int n_plots, int rows, int cols,
-                                    bool along_time, uint32_t* out, cudaStream_t st);
+// Input: row-major bit words `in`, or (when in_planes != null) the byte planes
+// [p][cols/8][rows] the binarize tile kernel writes.
+cudaError_t consolidate_bits_launch(const uint32_t* in, const uint8_t* in_planes, int n_plots, int rows,
+                                    int cols, bool along_time, uint32_t* out, cudaStream_t st);
 // Generic single-plot u8 morphology of columns [c0, c1) (stage API): op 0 erode,
 // 1 dilate, 2 open, 3 close; tmp: rows x cols scratch.
 cudaError_t morph_u8_launch(const uint8_t* src, int rows, int cols, int op, int se_rows, int se_cols,

@@ -70,129 +70,162 @@ cudaError_t unpack_launch(const uint32_t* bits, int n_plots, int rows, int cols,
 
 // ------------------------------------------------------------- fused chain
 
-struct MorphTile {
-    uint32_t* a;   // [NR][W] current image
-    uint32_t* b;   // [NR][W] vertical-pass temp
-    int NR, W, cols, rows, row0;  // row0: global row of buffer row 0
-    uint32_t last_mask;           // valid bits of the last word
+// One CTA: TR output rows x all W words, buffers of NR = TR + 2H rows.
+// W is a template parameter so the (row, word) decomposition of the thread
+// index is shifts, not divisions.  The two buffer edge rows are never
+// recomputed: the invalid band grows one row per vertical step, which the H
+// halo rows absorb (H = number of vertical steps).  Rows outside the image
+// are re-zeroed after every step (only tiles at the image edges have any).
+template <int WC>
+struct Tile {
+    int Wr;  // runtime word count when WC == 0
+    __device__ __forceinline__ int W() const { return WC ? WC : Wr; }
+    __device__ __forceinline__ int RPI() const { return W() >= kMorphThreads ? 1 : kMorphThreads / W(); }
+    uint32_t* a;
+    uint32_t* b;
+    int NR, row0, rows;
+    uint32_t last_mask;
+    int out_top, out_bot;  // buffer rows [0,out_top) and [out_bot,NR) lie outside the image
+
+    __device__ __forceinline__ void vpass(bool erode) const {
+        const int w = threadIdx.x % W();
+        for (int i = 1 + static_cast<int>(threadIdx.x) / W(); i < NR - 1; i += RPI()) {
+            const uint32_t u = a[(i - 1) * W() + w], c = a[i * W() + w], d = a[(i + 1) * W() + w];
+            b[i * W() + w] = erode ? (u & c & d) : (u | c | d);
+        }
+    }
+    __device__ __forceinline__ void hpass(const uint32_t* src, uint32_t* dst, bool erode) const {
+        const int w = threadIdx.x % W();
+        for (int i = 1 + static_cast<int>(threadIdx.x) / W(); i < NR - 1; i += RPI()) {
+            const uint32_t* row = src + i * W();
+            const uint32_t x = row[w];
+            const uint32_t prev = w > 0 ? row[w - 1] : 0u;
+            const uint32_t next = w + 1 < W() ? row[w + 1] : 0u;
+            const uint32_t left = (x << 1) | (prev >> 31);  // column c-1 at bit c
+            const uint32_t right = (x >> 1) | (next << 31); // column c+1 at bit c
+            uint32_t y = erode ? (x & left & right) : (x | left | right);
+            if (w == W() - 1) y &= last_mask;
+            dst[i * W() + w] = y;
+        }
+    }
+    __device__ __forceinline__ void copy_back() const {
+        const int w = threadIdx.x % W();
+        for (int i = 1 + static_cast<int>(threadIdx.x) / W(); i < NR - 1; i += RPI()) a[i * W() + w] = b[i * W() + w];
+    }
+    __device__ __forceinline__ void clip() const {
+        if (out_top == 0 && out_bot == NR) return;
+        const int w = threadIdx.x % W();
+        for (int i = static_cast<int>(threadIdx.x) / W(); i < NR; i += RPI())
+            if (i < out_top || i >= out_bot) a[i * W() + w] = 0u;
+    }
+    // one erosion / dilation: 3x3 (vert && horiz), 3x1 (vert), 1x3 (horiz)
+    __device__ __forceinline__ void step(bool erode, bool vert, bool horiz) const {
+        if (vert) {
+            vpass(erode);
+            __syncthreads();
+            if (horiz) hpass(b, a, erode);
+            else copy_back();
+        } else {
+            hpass(a, b, erode);
+            __syncthreads();
+            copy_back();
+        }
+        __syncthreads();
+        clip();
+        __syncthreads();
+    }
 };
 
-// Vertical pass a -> b over buffer rows [1, NR-1).
-__device__ __forceinline__ void vpass(const MorphTile& t, bool erode) {
-    const int n = (t.NR - 2) * t.W;
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-        const int i = 1 + e / t.W, w = e % t.W;
-        const uint32_t u = t.a[(i - 1) * t.W + w], c = t.a[i * t.W + w], d = t.a[(i + 1) * t.W + w];
-        t.b[i * t.W + w] = erode ? (u & c & d) : (u | c | d);
-    }
-}
-
-// Horizontal pass src -> dst over buffer rows [1, NR-1), out-of-image columns 0.
-__device__ __forceinline__ void hpass(const MorphTile& t, const uint32_t* src, uint32_t* dst, bool erode) {
-    const int n = (t.NR - 2) * t.W;
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-        const int i = 1 + e / t.W, w = e % t.W;
-        const uint32_t* row = src + i * t.W;
-        const uint32_t x = row[w];
-        const uint32_t prev = w > 0 ? row[w - 1] : 0u;
-        const uint32_t next = w + 1 < t.W ? row[w + 1] : 0u;
-        const uint32_t left = (x << 1) | (prev >> 31);   // column c-1 at bit c
-        uint32_t right = (x >> 1) | (next << 31);         // column c+1 at bit c
-        if (w == t.W - 1) right &= t.last_mask >> 1;      // column `cols` is off-image
-        uint32_t y = erode ? (x & left & right) : (x | left | right);
-        if (w == t.W - 1) y &= t.last_mask;
-        dst[i * t.W + w] = y;
-    }
-}
-
-// Re-zero buffer rows outside the image (and the two buffer edge rows, whose
-// neighbourhoods were not available).
-__device__ __forceinline__ void clip_rows(const MorphTile& t, uint32_t* img) {
-    const int n = t.NR * t.W;
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-        const int i = e / t.W;
-        const int g = t.row0 + i;
-        if (g < 0 || g >= t.rows || i == 0 || i == t.NR - 1) img[e] = 0u;
-    }
-}
-
-// one erosion / dilation with a 3x3 (vert && horiz), 3x1 (vert) or 1x3 (horiz) element
-__device__ __forceinline__ void step(const MorphTile& t, bool erode, bool vert, bool horiz) {
-    if (vert && horiz) {
-        vpass(t, erode);
-        __syncthreads();
-        hpass(t, t.b, t.a, erode);
-    } else if (vert) {
-        vpass(t, erode);
-        __syncthreads();
-        const int n = (t.NR - 2) * t.W;
-        for (int e = threadIdx.x; e < n; e += blockDim.x) t.a[t.W + e] = t.b[t.W + e];
-    } else {
-        hpass(t, t.a, t.b, erode);
-        __syncthreads();
-        const int n = (t.NR - 2) * t.W;
-        for (int e = threadIdx.x; e < n; e += blockDim.x) t.a[t.W + e] = t.b[t.W + e];
-    }
-    __syncthreads();
-    clip_rows(t, t.a);
-    __syncthreads();
-}
-
+template <int WC>
 __global__ void __launch_bounds__(kMorphThreads)
-consolidate_bits_kernel(const uint32_t* __restrict__ in, int rows, int cols, int tile_rows, int halo,
-                        bool along_time, uint32_t* __restrict__ out) {
+consolidate_bits_kernel(const uint32_t* __restrict__ in, const uint8_t* __restrict__ planes, int rows, int cols,
+                        int tile_rows, int halo, bool along_time, uint32_t* __restrict__ out) {
     extern __shared__ uint32_t mo_smem[];
-    const int W = (cols + 31) / 32;
     const int p = blockIdx.y;
     const int r0 = blockIdx.x * tile_rows;
     if (r0 >= rows) return;
-    MorphTile t;
+    Tile<WC> t;
+    t.Wr = (cols + 31) / 32;
+    const int W = t.W();
     t.NR = tile_rows + 2 * halo;
-    t.W = W;
-    t.cols = cols;
-    t.rows = rows;
     t.row0 = r0 - halo;
+    t.rows = rows;
     t.last_mask = (cols & 31) ? ((1u << (cols & 31)) - 1u) : 0xffffffffu;
+    t.out_top = t.row0 < 0 ? -t.row0 : 0;
+    t.out_bot = rows - t.row0 < t.NR ? rows - t.row0 : t.NR;
     t.a = mo_smem;
     t.b = mo_smem + t.NR * W;
-    const uint32_t* src = in + static_cast<long long>(p) * rows * W;
-    for (int e = threadIdx.x; e < t.NR * W; e += blockDim.x) {
-        const int g = t.row0 + e / W;
-        t.a[e] = (g >= 0 && g < rows) ? src[static_cast<long long>(g) * W + (e % W)] : 0u;
-        t.b[e] = 0u;
+    const int w = threadIdx.x % W;
+    if (planes) {
+        // byte planes [p][4W][rows]: lanes walk rows so each plane read is contiguous
+        const uint8_t* pl = planes + static_cast<long long>(p) * 4 * W * rows;
+        for (int e = threadIdx.x; e < W * t.NR; e += kMorphThreads) {
+            const int ww = e / t.NR, i = e - ww * t.NR;
+            const int g = t.row0 + i;
+            uint32_t word = 0u;
+            if (g >= 0 && g < rows) {
+                const uint8_t* b = pl + static_cast<long long>(4 * ww) * rows + g;
+                word = static_cast<uint32_t>(b[0]) | (static_cast<uint32_t>(b[rows]) << 8) |
+                       (static_cast<uint32_t>(b[2 * static_cast<long long>(rows)]) << 16) |
+                       (static_cast<uint32_t>(b[3 * static_cast<long long>(rows)]) << 24);
+            }
+            t.a[i * W + ww] = word;
+        }
+    } else {
+        const uint32_t* src = in + static_cast<long long>(p) * rows * W;
+        for (int i = static_cast<int>(threadIdx.x) / W; i < t.NR; i += t.RPI()) {
+            const int g = t.row0 + i;
+            t.a[i * W + w] = (g >= 0 && g < rows) ? src[static_cast<long long>(g) * W + w] : 0u;
+        }
     }
     __syncthreads();
-    // close 3x3: dilate, erode
-    step(t, false, true, true);
-    step(t, true, true, true);
-    // open 3x3: erode, dilate
-    step(t, true, true, true);
-    step(t, false, true, true);
-    // open with the line element: 1x3 along frequency, or 3x1 along time
-    step(t, true, along_time, !along_time);
-    step(t, false, along_time, !along_time);
+    t.step(false, true, true);  // close 3x3: dilate, erode
+    t.step(true, true, true);
+    t.step(true, true, true);   // open 3x3: erode, dilate
+    t.step(false, true, true);
+    t.step(true, along_time, !along_time);  // open with the line element
+    t.step(false, along_time, !along_time);
     uint32_t* dst = out + static_cast<long long>(p) * rows * W;
-    const int nout = min(tile_rows, rows - r0) * W;
-    for (int e = threadIdx.x; e < nout; e += blockDim.x)
-        dst[static_cast<long long>(r0) * W + e] = t.a[(halo + e / W) * W + (e % W)];
+    const int nrow = min(tile_rows, rows - r0);
+    for (int i = static_cast<int>(threadIdx.x) / W; i < nrow; i += t.RPI())
+        dst[static_cast<long long>(r0 + i) * W + w] = t.a[(halo + i) * W + w];
 }
 
-cudaError_t consolidate_bits_launch(const uint32_t* in, int n_plots, int rows, int cols, bool along_time,
-                                    uint32_t* out, cudaStream_t st) {
-    if (n_plots <= 0 || rows <= 0 || cols <= 0) return cudaSuccess;
-    const int W = (cols + 31) / 32;
+template <int WC>
+static cudaError_t consolidate_w(const uint32_t* in, const uint8_t* planes, int n_plots, int rows, int cols,
+                                 bool along_time, uint32_t* out, cudaStream_t st) {
+    const int W = WC ? WC : (cols + 31) / 32;
     const int halo = along_time ? 6 : 4;
-    int tile_rows = W <= 64 ? 128 : (W <= 128 ? 64 : 32);
+    // ~128 output rows per CTA for narrow masks, 32 for the widest
+    int tile_rows = W <= 32 ? 128 : (W <= 128 ? 64 : 32);
     if (tile_rows > rows) tile_rows = rows;
     const size_t smem = sizeof(uint32_t) * 2 * (tile_rows + 2 * halo) * W;
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(consolidate_bits_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        cudaError_t e = cudaFuncSetAttribute(consolidate_bits_kernel<WC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
         if (e != cudaSuccess) return e;
     }
     dim3 grid((rows + tile_rows - 1) / tile_rows, n_plots);
-    consolidate_bits_kernel<<<grid, kMorphThreads, smem, st>>>(in, rows, cols, tile_rows, halo, along_time, out);
+    consolidate_bits_kernel<WC><<<grid, kMorphThreads, smem, st>>>(in, planes, rows, cols, tile_rows, halo, along_time,
+                                                                 out);
     return cudaGetLastError();
+}
+
+cudaError_t consolidate_bits_launch(const uint32_t* in, const uint8_t* planes, int n_plots, int rows, int cols,
+                                    bool along_time, uint32_t* out, cudaStream_t st) {
+    if (n_plots <= 0 || rows <= 0 || cols <= 0) return cudaSuccess;
+    switch ((cols + 31) / 32) {
+    case 1: return consolidate_w<1>(in, planes, n_plots, rows, cols, along_time, out, st);
+    case 2: return consolidate_w<2>(in, planes, n_plots, rows, cols, along_time, out, st);
+    case 4: return consolidate_w<4>(in, planes, n_plots, rows, cols, along_time, out, st);
+    case 8: return consolidate_w<8>(in, planes, n_plots, rows, cols, along_time, out, st);
+    case 16: return consolidate_w<16>(in, planes, n_plots, rows, cols, along_time, out, st);
+    case 32: return consolidate_w<32>(in, planes, n_plots, rows, cols, along_time, out, st);
+    case 64: return consolidate_w<64>(in, planes, n_plots, rows, cols, along_time, out, st);
+    case 128: return consolidate_w<128>(in, planes, n_plots, rows, cols, along_time, out, st);
+    case 256: return consolidate_w<256>(in, planes, n_plots, rows, cols, along_time, out, st);
+    default: return consolidate_w<0>(in, planes, n_plots, rows, cols, along_time, out, st);  // any width
+    }
 }
 
 // ------------------------------------------------- generic u8 (stage API)
