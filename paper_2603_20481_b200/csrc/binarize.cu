@@ -47,8 +47,8 @@ __global__ void __launch_bounds__(kBinThreads) binarize_kernel(BinarizeLaunch a)
             for (int r = warp; r < rows; r += kBinWarps)
                 if (col_out) a.mask_u8[static_cast<long long>(r) * a.cols + col] = 0;
         } else if (a.mask_bits) {
-            uint32_t* mb = a.mask_bits + static_cast<long long>(p) * rows * W + wd;
-            for (int r = threadIdx.x; r < rows; r += kBinThreads) mb[static_cast<long long>(r) * W] = 0;
+            uint32_t* mb = a.mask_bits + (static_cast<long long>(p) * W + wd) * rows;  // word-major
+            for (int r = threadIdx.x; r < rows; r += kBinThreads) mb[r] = 0;
         }
         if (a.col_thr && threadIdx.x < 32 && in_image)
             a.col_thr[static_cast<long long>(p) * a.cols + col] = INFINITY;
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kBinThreads) binarize_kernel(BinarizeLaunch a)
             a.mask_u8[static_cast<long long>(r) * a.cols + col] = x > thr ? 1 : 0;
         }
     } else {
-        uint32_t* mb = a.mask_bits + static_cast<long long>(p) * rows * W + wd;
+        uint32_t* mb = a.mask_bits + (static_cast<long long>(p) * W + wd) * rows;  // word-major
         int r = warp;
         for (; r + 3 * kBinWarps < rows; r += 4 * kBinWarps) {
             float x[4];
@@ -220,13 +220,13 @@ __global__ void __launch_bounds__(kBinThreads) binarize_kernel(BinarizeLaunch a)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const uint32_t word = __ballot_sync(0xffffffffu, in_image && x[q] > thr);
-                if (lane == 0) mb[static_cast<long long>(r + q * kBinWarps) * W] = word;
+                if (lane == 0) mb[r + q * kBinWarps] = word;
             }
         }
         for (; r < rows; r += kBinWarps) {
             const float x = in_image ? __ldg(tf + static_cast<long long>(r) * a.cols + col) : 0.0f;
             const uint32_t word = __ballot_sync(0xffffffffu, in_image && x > thr);
-            if (lane == 0) mb[static_cast<long long>(r) * W] = word;
+            if (lane == 0) mb[r] = word;
         }
     }
 }

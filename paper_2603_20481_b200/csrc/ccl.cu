@@ -3,7 +3,8 @@
 // Replaces detector::resolve_components / component_extents /
 // label_components and the box conversion (proj/src/detector.cpp:494-635).
 // Run-based union-find, batched over plots:
-//   1 count   : runs starting per row (start bits = x & ~(x<<1 | carry))
+//   1 count   : runs starting per row (start bits = x & ~(x<<1 | carry)),
+//               one thread per row over the word-major mask
 //   2 scan    : per-plot exclusive row offsets; 3 per-plot pool bases
 //   4 emit    : runs in row-major order of their start pixel -> pool
 //   5 union   : each run unites with the overlapping runs of the row above
@@ -25,22 +26,21 @@
 
 namespace ssb {
 
-__device__ __forceinline__ uint32_t start_bits(const uint32_t* row, int w) {
-    const uint32_t x = row[w];
-    const uint32_t carry = w > 0 ? (row[w - 1] >> 31) : 0u;
-    return x & ~((x << 1) | carry);
-}
-
+// Masks are word-major (bits[p][w][r]); one thread walks one row's words,
+// so each warp reads 32 consecutive rows of a word: coalesced.
 __global__ void count_runs_kernel(const uint32_t* __restrict__ bits, int rows, int W, int* row_runs) {
     const int p = blockIdx.y;
-    const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rows) return;
-    const uint32_t* row = bits + (static_cast<long long>(p) * rows + r) * W;
+    const uint32_t* col = bits + static_cast<long long>(p) * W * rows + r;
+    uint32_t carry = 0u;
     int cnt = 0;
-    for (int w = lane; w < W; w += 32) cnt += __popc(start_bits(row, w));
-    cnt = warp_sum(cnt);
-    if (lane == 0) row_runs[static_cast<long long>(p) * rows + r] = cnt;
+    for (int w = 0; w < W; ++w) {
+        const uint32_t x = col[static_cast<long long>(w) * rows];
+        cnt += __popc(x & ~((x << 1) | carry));
+        carry = x >> 31;
+    }
+    row_runs[static_cast<long long>(p) * rows + r] = cnt;
 }
 
 __global__ void scan_rows_kernel(const int* row_runs, int rows, int* row_off) {
@@ -91,49 +91,44 @@ __global__ void plot_base_kernel(const int* row_off, int n_plots, int rows, long
     *overflow = of;
 }
 
+// Runs of one row in column order (start bits x & ~(x<<1|carry), end bits
+// ~x & (x<<1|carry) alternate), appended at the row's offset in the pool.
 __global__ void emit_runs_kernel(const uint32_t* __restrict__ bits, int rows, int cols, const int* row_off,
                                  const long long* plot_base, const int* plot_ok, CclWorkspace ws) {
     const int W = (cols + 31) / 32;
     const int p = blockIdx.y;
-    const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rows || !plot_ok[p]) return;
-    const uint32_t* row = bits + (static_cast<long long>(p) * rows + r) * W;
-    long long idx0 = plot_base[p] + row_off[static_cast<long long>(p) * (rows + 1) + r];
-    for (int c0 = 0; c0 < W; c0 += 32) {
-        const int w = c0 + lane;
-        const uint32_t x = w < W ? row[w] : 0u;
-        uint32_t S = w < W ? start_bits(row, w) : 0u;
-        const int n = __popc(S);
-        const int inc = warp_incl_scan(n);
-        const int tot = __shfl_sync(0xffffffffu, inc, 31);
-        long long idx = idx0 + inc - n;
-        while (S) {
-            const int s = __ffs(S) - 1;
-            S &= S - 1;
-            const uint32_t z = s == 31 ? 0u : (~x & (0xffffffffu << (s + 1)));
-            int e;
-            if (z) {
-                e = 32 * w + __ffs(z) - 1;
-            } else {
-                int ww = w + 1;
-                while (ww < W && row[ww] == 0xffffffffu) ++ww;
-                e = ww < W ? 32 * ww + __ffs(~row[ww]) - 1 : 32 * W;
-            }
-            if (e > cols) e = cols;
-            ws.run_begin[idx] = 32 * w + s;
-            ws.run_end[idx] = e;
-            ws.run_row[idx] = r;
-            ws.parent[idx] = static_cast<int>(idx);
-            ws.area[idx] = 0ull;
-            ws.min_f[idx] = INT_MAX;
-            ws.max_f[idx] = -1;
-            ws.max_t[idx] = -1;
-            ws.dense[idx] = -1;
-            ++idx;
+    const uint32_t* col = bits + static_cast<long long>(p) * W * rows + r;
+    long long idx = plot_base[p] + row_off[static_cast<long long>(p) * (rows + 1) + r];
+    uint32_t carry = 0u;
+    int open = -1;
+    auto put = [&](int b, int e) {
+        ws.run_begin[idx] = b;
+        ws.run_end[idx] = e;
+        ws.run_row[idx] = r;
+        ws.parent[idx] = static_cast<int>(idx);
+        ws.area[idx] = 0ull;
+        ws.min_f[idx] = INT_MAX;
+        ws.max_f[idx] = -1;
+        ws.max_t[idx] = -1;
+        ws.dense[idx] = -1;
+        ++idx;
+    };
+    for (int w = 0; w < W; ++w) {
+        const uint32_t x = col[static_cast<long long>(w) * rows];
+        const uint32_t sh = (x << 1) | carry;
+        const uint32_t starts = x & ~sh;
+        uint32_t ev = starts | (~x & sh);
+        carry = x >> 31;
+        while (ev) {
+            const int bpos = __ffs(ev) - 1;
+            ev &= ev - 1;
+            if ((starts >> bpos) & 1u) open = 32 * w + bpos;
+            else put(open, 32 * w + bpos);
         }
-        idx0 += tot;
     }
+    if (carry) put(open, cols);  // run reaching the last column (cols % 32 == 0)
 }
 
 __device__ __forceinline__ int uf_find(int* parent, int x) {
@@ -300,12 +295,12 @@ cudaError_t ccl_launch(const CclLaunch& L, cudaStream_t st) {
     if (L.n_plots <= 0 || L.rows <= 0 || L.cols <= 0) return cudaSuccess;
     const int W = (L.cols + 31) / 32;
     const CclWorkspace& ws = L.ws;
-    dim3 rgrid((L.rows + 7) / 8, L.n_plots);
-    count_runs_kernel<<<rgrid, 256, 0, st>>>(L.bits, L.rows, W, ws.row_runs);
+    dim3 tgrid((L.rows + 127) / 128, L.n_plots);
+    count_runs_kernel<<<tgrid, 128, 0, st>>>(L.bits, L.rows, W, ws.row_runs);
     scan_rows_kernel<<<L.n_plots, 1024, 0, st>>>(ws.row_runs, L.rows, ws.row_off);
     plot_base_kernel<<<1, 32, 0, st>>>(ws.row_off, L.n_plots, L.rows, ws.pool_cap, ws.plot_base, ws.plot_ok,
                                        ws.overflow);
-    emit_runs_kernel<<<rgrid, 256, 0, st>>>(L.bits, L.rows, L.cols, ws.row_off, ws.plot_base, ws.plot_ok, ws);
+    emit_runs_kernel<<<tgrid, 128, 0, st>>>(L.bits, L.rows, L.cols, ws.row_off, ws.plot_base, ws.plot_ok, ws);
     if (L.rows > 1) {
         dim3 ugrid((L.rows - 1 + 7) / 8, L.n_plots);
         union_kernel<<<ugrid, 256, 0, st>>>(L.rows, ws.row_off, ws.plot_base, ws.plot_ok, ws);

@@ -151,52 +151,65 @@ __device__ __forceinline__ void run_pass(cd* v, int j, const double2* __restrict
             const int b = j + PL::TPR * u;
             const int k = b % NS;
             const double2* t = tw + PL::tw_off(PASS) + k;
+#ifndef SSB_EXP_NO_TW
 #pragma unroll
             for (int r = 1; r < R; ++r) {
                 const double2 w = __ldg(t + (r - 1) * NS);
                 v[u * R + r] = c_mul(v[u * R + r], cd{w.x, w.y});
             }
+#else
+            (void)t;
+#endif
         }
         dft_r<R>(v + u * R);
     }
 }
 
-// Store pass PASS's outputs into smem (padded), then load pass PASS+1's inputs.
+// Store pass PASS's outputs into smem (padded), then load pass PASS+1's
+// inputs -- real parts first, then imaginary parts, through one N-double
+// buffer: half the shared memory of a complex exchange, which leaves L1 room
+// for the pass twiddle tables (the 2-phase exchange costs two extra barriers).
 template <int LOGN, int PASS>
-__device__ __forceinline__ void exchange(cd* v, int j, double2* buf) {
+__device__ __forceinline__ void exchange(cd* v, int j, double* buf) {
     using PL = FftPlan<LOGN>;
     constexpr int R = PL::radix(PASS);
     constexpr int NS = PL::ns(PASS);
     constexpr int U = PL::P / R;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        const int b = j + PL::TPR * u;
-        const int k = b % NS;
-        const int base = (b - k) * R + k;
-#pragma unroll
-        for (int r = 0; r < R; ++r) buf[pad_idx(base + r * NS)] = make_double2(v[u * R + r].re, v[u * R + r].im);
-    }
-    __syncthreads();
     constexpr int R2 = PL::radix(PASS + 1);
     constexpr int U2 = PL::P / R2;
 #pragma unroll
-    for (int u = 0; u < U2; ++u) {
-        const int b = j + PL::TPR * u;
+    for (int half = 0; half < 2; ++half) {
 #pragma unroll
-        for (int r = 0; r < R2; ++r) {
-            const double2 x = buf[pad_idx(b + r * (PL::N / R2))];
-            v[u * R2 + r] = {x.x, x.y};
+        for (int u = 0; u < U; ++u) {
+            const int b = j + PL::TPR * u;
+            const int k = b % NS;
+            const int base = (b - k) * R + k;
+#pragma unroll
+            for (int r = 0; r < R; ++r) buf[pad_idx(base + r * NS)] = half ? v[u * R + r].im : v[u * R + r].re;
         }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < U2; ++u) {
+            const int b = j + PL::TPR * u;
+#pragma unroll
+            for (int r = 0; r < R2; ++r) {
+                const double x = buf[pad_idx(b + r * (PL::N / R2))];
+                if (half) v[u * R2 + r].im = x;
+                else v[u * R2 + r].re = x;
+            }
+        }
+        __syncthreads();
     }
-    __syncthreads();
 }
 
 template <int LOGN, int PASS>
-__device__ __forceinline__ void passes_from(cd* v, int j, const double2* tw, double2* buf) {
+__device__ __forceinline__ void passes_from(cd* v, int j, const double2* tw, double* buf) {
     using PL = FftPlan<LOGN>;
     run_pass<LOGN, PASS>(v, j, tw);
     if constexpr (PASS + 1 < PL::NP) {
+#ifndef SSB_EXP_NO_XCHG
         exchange<LOGN, PASS>(v, j, buf);
+#endif
         passes_from<LOGN, PASS + 1>(v, j, tw, buf);
     }
 }
@@ -260,15 +273,15 @@ fft_mag_kernel(FftArgs a) {
     constexpr int G = PL::G;
     constexpr int SAMPLE_BYTES = FMT == 0 ? 8 : 4;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double2* buf = reinterpret_cast<double2*>(smem_raw);                          // G * SROW
-    unsigned char* stage = smem_raw + sizeof(double2) * G * PL::SROW;             // G*N samples
+    double* buf = reinterpret_cast<double*>(smem_raw);                            // G * SROW
+    unsigned char* stage = smem_raw + sizeof(double) * G * PL::SROW;              // G*N samples
     float* magbuf = reinterpret_cast<float*>(stage + SAMPLE_BYTES * G * N);       // G*N (G>1, PSD)
     __shared__ __align__(8) uint64_t bar;
 
     const int tid = threadIdx.x;
     const int g = tid / PL::TPR;
     const int j = tid % PL::TPR;
-    double2* mybuf = buf + g * PL::SROW;
+    double* mybuf = buf + g * PL::SROW;
 
     // iteration space
     long long it_begin, it_end, it_step, row_base;
@@ -357,7 +370,12 @@ fft_mag_kernel(FftArgs a) {
         constexpr int NSL = PL::ns(PL::NP - 1);
         constexpr int UL = PL::P / RL;
         float m[PL::P];
+#ifndef SSB_EXP_NO_MAG
         mags<PL::P>(v, m);
+#else
+#pragma unroll
+        for (int i = 0; i < PL::P; ++i) m[i] = static_cast<float>(v[i].re);
+#endif
         if constexpr (G == 1) {
             float* out = a.tf ? a.tf + row * N : nullptr;
 #pragma unroll
@@ -469,7 +487,7 @@ template <int LOGN>
 static size_t smem_bytes(int fmt) {
     using PL = FftPlan<LOGN>;
     const size_t sb = fmt == 0 ? 8 : 4;
-    size_t bytes = sizeof(double2) * PL::G * PL::SROW + sb * PL::G * PL::N;
+    size_t bytes = sizeof(double) * PL::G * PL::SROW + sb * PL::G * PL::N;
     if (PL::G > 1) bytes += sizeof(float) * PL::G * PL::N;
     return bytes;
 }
@@ -483,6 +501,12 @@ static cudaError_t launch_one(const FftLaunch& L, cudaStream_t st) {
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        // carve out only what the resident CTAs need; the rest stays L1 for the
+        // pass-major twiddle tables (~65 KB at N = 4096)
+        const int per_sm = static_cast<int>((smem + 1024) * (LOGN >= 13 ? 1 : 2));
+        const int pct = (per_sm * 100 + 228 * 1024 - 1) / (228 * 1024);
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
         if (e != cudaSuccess) return e;
         attr_done = true;
     }

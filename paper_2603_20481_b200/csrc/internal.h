@@ -63,7 +63,7 @@ struct BinarizeLaunch {
     int rows = 0;
     int cols = 0;
     const uint32_t* active_bits = nullptr;  // n_plots x W
-    uint32_t* mask_bits = nullptr;      // n_plots x rows x W (bit mode) or null
+    uint32_t* mask_bits = nullptr;      // n_plots x W x rows word-major bits (bit mode) or null
     uint8_t* mask_planes = nullptr;     // n_plots x (cols/8) x rows byte planes (tile path) or null
     uint8_t* mask_u8 = nullptr;         // rows x cols (u8 mode, columns [c0,c1)) or null
     int c0 = 0, c1 = 0;                 // u8 mode column range

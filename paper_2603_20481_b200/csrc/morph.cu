@@ -2,25 +2,31 @@
 //
 // Replaces detector::consolidate (proj/src/detector.cpp:482-492) and the
 // morphology primitives it composes (:345-480).  Masks are bit-packed,
-// 32 columns per uint32 word (bit b of word w = column 32w+b), rows
-// contiguous -- 1/32 of the reference's byte mask (2441 x 4096 -> 1.25 MB).
+// 32 columns per uint32 word (bit b of word w = column 32w+b) and stored
+// WORD-MAJOR: bits[p][w][r], rows contiguous -- 1/32 of the reference's byte
+// mask, and every kernel that walks it has consecutive lanes on consecutive
+// rows (coalesced global access, conflict-free shared access).
 //
-// consolidate_bits_kernel fuses the whole chain close3x3 -> open3x3 ->
-// open1x3 (3x1 when one_d_opening_along_time) in shared memory: one CTA owns a
-// tile of TR output rows across all words, loads TR + 2H rows (H = 4, or 6
-// with the vertical line), and applies the six erode/dilate steps as
-// separable vertical (row AND/OR) + horizontal (shift/carry AND/OR) word ops.
-// Outside the image counts as background for erosion and dilation alike
-// (:359-362, :393-410): out-of-image rows are re-zeroed after every step and
-// bits past the last column are masked, so each step sees exactly the
-// reference's clipped neighbourhood.
+// consolidate_kernel fuses the whole chain close3x3 -> open3x3 -> open1x3
+// (3x1 when one_d_opening_along_time) in shared memory: one CTA owns a tile of
+// 64 buffer rows (56 output rows + 4 halo rows each side; 52 + 6 for the
+// vertical line) across all W words, column-major in smem (a[w][i]), and
+// applies the six erode/dilate steps as separable vertical (row AND/OR) and
+// horizontal (shift/carry AND/OR across neighbouring words) passes.  Outside
+// the image counts as background for erosion and dilation alike (:359-362,
+// :393-410): out-of-image rows are re-zeroed after every step and bits past
+// the last column are masked, so each step sees the reference's clipped
+// neighbourhood.  The two buffer edge rows are never recomputed; the invalid
+// band grows one row per vertical step and the halo absorbs it.
 #include "common.cuh"
 #include "internal.h"
 
 namespace ssb {
 
 constexpr int kMorphThreads = 256;
+constexpr int kTileNR = 64;  // buffer rows per CTA (a power of two: thread -> (word, row) is shifts)
 
+// byte mask [p][rows][cols] -> word-major bits [p][W][rows]
 __global__ void pack_u8_kernel(const uint8_t* __restrict__ m, int rows, int cols, uint32_t* __restrict__ bits) {
     const int W = (cols + 31) / 32;
     const int p = blockIdx.y;
@@ -36,7 +42,7 @@ __global__ void pack_u8_kernel(const uint8_t* __restrict__ m, int rows, int cols
         const int c = w * 32 + lane;
         const bool b = c < cols && mp[r * cols + c] != 0;
         const uint32_t word = __ballot_sync(0xffffffffu, b);
-        if (lane == 0) bp[wi] = word;
+        if (lane == 0) bp[static_cast<long long>(w) * rows + r] = word;
     }
 }
 
@@ -57,7 +63,7 @@ __global__ void unpack_kernel(const uint32_t* __restrict__ bits, int rows, int c
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         const long long r = i / cols;
         const int c = static_cast<int>(i % cols);
-        mp[i] = (bp[r * W + (c >> 5)] >> (c & 31)) & 1u;
+        mp[i] = (bp[static_cast<long long>(c >> 5) * rows + r] >> (c & 31)) & 1u;
     }
 }
 
@@ -70,65 +76,59 @@ cudaError_t unpack_launch(const uint32_t* bits, int n_plots, int rows, int cols,
 
 // ------------------------------------------------------------- fused chain
 
-// One CTA: TR output rows x all W words, buffers of NR = TR + 2H rows.
-// W is a template parameter so the (row, word) decomposition of the thread
-// index is shifts, not divisions.  The two buffer edge rows are never
-// recomputed: the invalid band grows one row per vertical step, which the H
-// halo rows absorb (H = number of vertical steps).  Rows outside the image
-// are re-zeroed after every step (only tiles at the image edges have any).
-template <int WC>
-struct Tile {
-    int Wr;  // runtime word count when WC == 0
-    __device__ __forceinline__ int W() const { return WC ? WC : Wr; }
-    __device__ __forceinline__ int RPI() const { return W() >= kMorphThreads ? 1 : kMorphThreads / W(); }
-    uint32_t* a;
-    uint32_t* b;
-    int NR, row0, rows;
+struct MTile {
+    uint32_t* a;       // [W][kTileNR] current image (column-major)
+    uint32_t* b;       // [W][kTileNR] scratch
+    int W;
     uint32_t last_mask;
-    int out_top, out_bot;  // buffer rows [0,out_top) and [out_bot,NR) lie outside the image
+    int out_top, out_bot;  // buffer rows [0,out_top) and [out_bot,kTileNR) lie outside the image
 
+    // every thread visits (w, i) for i in [1, NR-1): e = w*NR + i
     __device__ __forceinline__ void vpass(bool erode) const {
-        const int w = threadIdx.x % W();
-        for (int i = 1 + static_cast<int>(threadIdx.x) / W(); i < NR - 1; i += RPI()) {
-            const uint32_t u = a[(i - 1) * W() + w], c = a[i * W() + w], d = a[(i + 1) * W() + w];
-            b[i * W() + w] = erode ? (u & c & d) : (u | c | d);
+        for (int e = threadIdx.x; e < W * kTileNR; e += kMorphThreads) {
+            const int i = e & (kTileNR - 1);
+            if (i == 0 || i == kTileNR - 1) continue;
+            const uint32_t u = a[e - 1], c = a[e], d = a[e + 1];
+            b[e] = erode ? (u & c & d) : (u | c | d);
         }
     }
     __device__ __forceinline__ void hpass(const uint32_t* src, uint32_t* dst, bool erode) const {
-        const int w = threadIdx.x % W();
-        for (int i = 1 + static_cast<int>(threadIdx.x) / W(); i < NR - 1; i += RPI()) {
-            const uint32_t* row = src + i * W();
-            const uint32_t x = row[w];
-            const uint32_t prev = w > 0 ? row[w - 1] : 0u;
-            const uint32_t next = w + 1 < W() ? row[w + 1] : 0u;
-            const uint32_t left = (x << 1) | (prev >> 31);  // column c-1 at bit c
-            const uint32_t right = (x >> 1) | (next << 31); // column c+1 at bit c
+        for (int e = threadIdx.x; e < W * kTileNR; e += kMorphThreads) {
+            const int w = e >> 6;  // kTileNR == 64
+            const uint32_t x = src[e];
+            const uint32_t prev = w > 0 ? src[e - kTileNR] : 0u;
+            const uint32_t next = w + 1 < W ? src[e + kTileNR] : 0u;
+            const uint32_t left = (x << 1) | (prev >> 31);   // column c-1 at bit c
+            const uint32_t right = (x >> 1) | (next << 31);  // column c+1 at bit c
             uint32_t y = erode ? (x & left & right) : (x | left | right);
-            if (w == W() - 1) y &= last_mask;
-            dst[i * W() + w] = y;
+            if (w == W - 1) y &= last_mask;
+            dst[e] = y;
         }
     }
-    __device__ __forceinline__ void copy_back() const {
-        const int w = threadIdx.x % W();
-        for (int i = 1 + static_cast<int>(threadIdx.x) / W(); i < NR - 1; i += RPI()) a[i * W() + w] = b[i * W() + w];
-    }
     __device__ __forceinline__ void clip() const {
-        if (out_top == 0 && out_bot == NR) return;
-        const int w = threadIdx.x % W();
-        for (int i = static_cast<int>(threadIdx.x) / W(); i < NR; i += RPI())
-            if (i < out_top || i >= out_bot) a[i * W() + w] = 0u;
+        if (out_top == 0 && out_bot == kTileNR) return;
+        for (int e = threadIdx.x; e < W * kTileNR; e += kMorphThreads) {
+            const int i = e & (kTileNR - 1);
+            if (i < out_top || i >= out_bot) a[e] = 0u;
+        }
     }
     // one erosion / dilation: 3x3 (vert && horiz), 3x1 (vert), 1x3 (horiz)
-    __device__ __forceinline__ void step(bool erode, bool vert, bool horiz) const {
+    __device__ __forceinline__ void step(bool erode, bool vert, bool horiz) {
         if (vert) {
             vpass(erode);
             __syncthreads();
-            if (horiz) hpass(b, a, erode);
-            else copy_back();
+            if (horiz) {
+                hpass(b, a, erode);
+            } else {
+                uint32_t* t = a;  // result is in b (edge rows: stale, invalid anyway)
+                a = b;
+                b = t;
+            }
         } else {
             hpass(a, b, erode);
-            __syncthreads();
-            copy_back();
+            uint32_t* t = a;
+            a = b;
+            b = t;
         }
         __syncthreads();
         clip();
@@ -136,47 +136,38 @@ struct Tile {
     }
 };
 
-template <int WC>
+// in_bits: word-major bits [p][W][rows], or in_planes: byte planes [p][4W][rows].
 __global__ void __launch_bounds__(kMorphThreads)
-consolidate_bits_kernel(const uint32_t* __restrict__ in, const uint8_t* __restrict__ planes, int rows, int cols,
-                        int tile_rows, int halo, bool along_time, uint32_t* __restrict__ out) {
+consolidate_kernel(const uint32_t* __restrict__ in_bits, const uint8_t* __restrict__ in_planes, int rows, int cols,
+                   int halo, bool along_time, uint32_t* __restrict__ out) {
     extern __shared__ uint32_t mo_smem[];
+    const int W = (cols + 31) / 32;
     const int p = blockIdx.y;
+    const int tile_rows = kTileNR - 2 * halo;
     const int r0 = blockIdx.x * tile_rows;
-    if (r0 >= rows) return;
-    Tile<WC> t;
-    t.Wr = (cols + 31) / 32;
-    const int W = t.W();
-    t.NR = tile_rows + 2 * halo;
-    t.row0 = r0 - halo;
-    t.rows = rows;
-    t.last_mask = (cols & 31) ? ((1u << (cols & 31)) - 1u) : 0xffffffffu;
-    t.out_top = t.row0 < 0 ? -t.row0 : 0;
-    t.out_bot = rows - t.row0 < t.NR ? rows - t.row0 : t.NR;
+    const int row0 = r0 - halo;  // global row of buffer row 0
+    MTile t;
+    t.W = W;
     t.a = mo_smem;
-    t.b = mo_smem + t.NR * W;
-    const int w = threadIdx.x % W;
-    if (planes) {
-        // byte planes [p][4W][rows]: lanes walk rows so each plane read is contiguous
-        const uint8_t* pl = planes + static_cast<long long>(p) * 4 * W * rows;
-        for (int e = threadIdx.x; e < W * t.NR; e += kMorphThreads) {
-            const int ww = e / t.NR, i = e - ww * t.NR;
-            const int g = t.row0 + i;
-            uint32_t word = 0u;
-            if (g >= 0 && g < rows) {
-                const uint8_t* b = pl + static_cast<long long>(4 * ww) * rows + g;
-                word = static_cast<uint32_t>(b[0]) | (static_cast<uint32_t>(b[rows]) << 8) |
-                       (static_cast<uint32_t>(b[2 * static_cast<long long>(rows)]) << 16) |
-                       (static_cast<uint32_t>(b[3 * static_cast<long long>(rows)]) << 24);
+    t.b = mo_smem + W * kTileNR;
+    t.last_mask = (cols & 31) ? ((1u << (cols & 31)) - 1u) : 0xffffffffu;
+    t.out_top = row0 < 0 ? -row0 : 0;
+    t.out_bot = rows - row0 < kTileNR ? rows - row0 : kTileNR;
+    for (int e = threadIdx.x; e < W * kTileNR; e += kMorphThreads) {
+        const int w = e >> 6, i = e & (kTileNR - 1);
+        const int g = row0 + i;
+        uint32_t word = 0u;
+        if (g >= 0 && g < rows) {
+            if (in_planes) {
+                const uint8_t* bp = in_planes + (static_cast<long long>(p) * 4 * W + 4 * w) * rows + g;
+                word = static_cast<uint32_t>(bp[0]) | (static_cast<uint32_t>(bp[rows]) << 8) |
+                       (static_cast<uint32_t>(bp[2 * static_cast<long long>(rows)]) << 16) |
+                       (static_cast<uint32_t>(bp[3 * static_cast<long long>(rows)]) << 24);
+            } else {
+                word = in_bits[(static_cast<long long>(p) * W + w) * rows + g];
             }
-            t.a[i * W + ww] = word;
         }
-    } else {
-        const uint32_t* src = in + static_cast<long long>(p) * rows * W;
-        for (int i = static_cast<int>(threadIdx.x) / W; i < t.NR; i += t.RPI()) {
-            const int g = t.row0 + i;
-            t.a[i * W + w] = (g >= 0 && g < rows) ? src[static_cast<long long>(g) * W + w] : 0u;
-        }
+        t.a[e] = word;
     }
     __syncthreads();
     t.step(false, true, true);  // close 3x3: dilate, erode
@@ -185,47 +176,29 @@ consolidate_bits_kernel(const uint32_t* __restrict__ in, const uint8_t* __restri
     t.step(false, true, true);
     t.step(true, along_time, !along_time);  // open with the line element
     t.step(false, along_time, !along_time);
-    uint32_t* dst = out + static_cast<long long>(p) * rows * W;
     const int nrow = min(tile_rows, rows - r0);
-    for (int i = static_cast<int>(threadIdx.x) / W; i < nrow; i += t.RPI())
-        dst[static_cast<long long>(r0 + i) * W + w] = t.a[(halo + i) * W + w];
-}
-
-template <int WC>
-static cudaError_t consolidate_w(const uint32_t* in, const uint8_t* planes, int n_plots, int rows, int cols,
-                                 bool along_time, uint32_t* out, cudaStream_t st) {
-    const int W = WC ? WC : (cols + 31) / 32;
-    const int halo = along_time ? 6 : 4;
-    // ~128 output rows per CTA for narrow masks, 32 for the widest
-    int tile_rows = W <= 32 ? 128 : (W <= 128 ? 64 : 32);
-    if (tile_rows > rows) tile_rows = rows;
-    const size_t smem = sizeof(uint32_t) * 2 * (tile_rows + 2 * halo) * W;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(consolidate_bits_kernel<WC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
+    for (int e = threadIdx.x; e < W * kTileNR; e += kMorphThreads) {
+        const int w = e >> 6, i = e & (kTileNR - 1);
+        if (i >= halo && i < halo + nrow) out[(static_cast<long long>(p) * W + w) * rows + r0 + (i - halo)] = t.a[e];
     }
-    dim3 grid((rows + tile_rows - 1) / tile_rows, n_plots);
-    consolidate_bits_kernel<WC><<<grid, kMorphThreads, smem, st>>>(in, planes, rows, cols, tile_rows, halo, along_time,
-                                                                 out);
-    return cudaGetLastError();
 }
 
 cudaError_t consolidate_bits_launch(const uint32_t* in, const uint8_t* planes, int n_plots, int rows, int cols,
                                     bool along_time, uint32_t* out, cudaStream_t st) {
     if (n_plots <= 0 || rows <= 0 || cols <= 0) return cudaSuccess;
-    switch ((cols + 31) / 32) {
-    case 1: return consolidate_w<1>(in, planes, n_plots, rows, cols, along_time, out, st);
-    case 2: return consolidate_w<2>(in, planes, n_plots, rows, cols, along_time, out, st);
-    case 4: return consolidate_w<4>(in, planes, n_plots, rows, cols, along_time, out, st);
-    case 8: return consolidate_w<8>(in, planes, n_plots, rows, cols, along_time, out, st);
-    case 16: return consolidate_w<16>(in, planes, n_plots, rows, cols, along_time, out, st);
-    case 32: return consolidate_w<32>(in, planes, n_plots, rows, cols, along_time, out, st);
-    case 64: return consolidate_w<64>(in, planes, n_plots, rows, cols, along_time, out, st);
-    case 128: return consolidate_w<128>(in, planes, n_plots, rows, cols, along_time, out, st);
-    case 256: return consolidate_w<256>(in, planes, n_plots, rows, cols, along_time, out, st);
-    default: return consolidate_w<0>(in, planes, n_plots, rows, cols, along_time, out, st);  // any width
+    const int W = (cols + 31) / 32;
+    const int halo = along_time ? 6 : 4;
+    const int tile_rows = kTileNR - 2 * halo;
+    const size_t smem = sizeof(uint32_t) * 2 * static_cast<size_t>(W) * kTileNR;
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;  // cols > 14,000: not on the device path
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(consolidate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
     }
+    dim3 grid((rows + tile_rows - 1) / tile_rows, n_plots);
+    consolidate_kernel<<<grid, kMorphThreads, smem, st>>>(in, planes, rows, cols, halo, along_time, out);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------- generic u8 (stage API)
