@@ -252,24 +252,27 @@ def run_ours(args):
         traffic = traffic * B if traffic else None
 
     # ---- e2e: host (pinned) IQ in, host boxes out, through the same C-ABI call
-    Be = min(B, args.e2e_batch)
+    Be = max(1, min(B, args.e2e_batch))
     host_iq = torch.empty(Be * SAMPLES, dtype=torch.complex64, pin_memory=True)
     host_iq.copy_(iq[: Be * SAMPLES])
     host_out = {k: torch.empty((Be,) + tuple(v.shape[1:]), dtype=v.dtype, pin_memory=True) for k, v in outs.items()}
     hout = NAT.BatchOut(*(C.c_void_p(v.data_ptr()) for v in host_out.values()), K)
 
+    if args.no_e2e:
+        Be = 0
+
     def e2e_step():
         ctx.check(lib.ss_sense_batch(ctx.h, C.c_void_p(host_iq.data_ptr()), NAT.SS_FMT_F32, N_FFT, ROWS, Be,
                                      C.c_uint64(0), C.c_double(FS), C.byref(cfg), None, C.byref(hout)))
 
-    for _ in range(max(1, args.warmup // 2)):
+    for _ in range(max(1, args.warmup // 2) if Be else 0):
         e2e_step()
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
+    for _ in range(args.steps if Be else 0):
         e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
@@ -278,12 +281,13 @@ def run_ours(args):
         t = torch.tensor([e2e_el], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_el = float(t.item())
-    e2e_val = ws * Be / (e2e_el / args.steps)
+    e2e_val = ws * Be / (e2e_el / args.steps) if Be else None
     d2h = sum(v.numel() * v.element_size() for v in host_out.values())
 
     # parity spot check of the timed outputs (device path == e2e path)
-    nb_dev = outs["n_boxes"][:Be].cpu()
-    assert torch.equal(nb_dev, host_out["n_boxes"]), "e2e and device-resident results differ"
+    if Be:
+        nb_dev = outs["n_boxes"][:Be].cpu()
+        assert torch.equal(nb_dev, host_out["n_boxes"]), "e2e and device-resident results differ"
 
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
@@ -335,6 +339,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (kernel experiments only)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

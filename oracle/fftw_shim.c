@@ -7,16 +7,18 @@
  *
  * Forward power-of-two transforms (the only kind the hot path issues:
  * proj/src/frontend.cpp:54-60 plans FFTW_FORWARD, n = 2^m >= 8, and executes at
- * :139) follow the "SSFFT-1" arithmetic specification written out in DESIGN.md
- * section 3 -- the same specification the device kernel
+ * :139) follow the "SSFFT-2" arithmetic specification written out in DESIGN.md
+ * section 3.1 -- the same specification the device kernel
  * paper_2603_20481_b200/csrc/fft_mag.cu implements independently -- so TF
  * plots are bit-identical by construction:
  *
  *   * Stockham DIT autosort, passes of radix 16, then one pass of radix
  *     2^(m mod 4) when m mod 4 != 0 (N=8: a single radix-8 pass);
  *   * pass (Ns, R): butterfly j reads src[j + r*N/R], multiplies v[r] (r >= 1)
- *     by tw[r*(j mod Ns)*N/(Ns*R)] unless Ns == 1, runs DFT_R, and writes
- *     dst[(j - j mod Ns)*R + j mod Ns + r*Ns];
+ *     by w_r unless Ns == 1, runs DFT_R, and writes
+ *     dst[(j - j mod Ns)*R + j mod Ns + r*Ns]; w_1 = tw[(j mod Ns)*N/(Ns*R)]
+ *     and w_2..w_15 come from a fixed product tree (w2 = w1 w1, w3 = w2 w1,
+ *     w4 = w2 w2, w5..7 = w4 w1..3, w8 = w4 w4, w9..15 = w8 w1..7);
  *   * tw[e] = (cos(t), -sin(t)), t = (2*pi * e) / N, glibc double cos/sin;
  *   * cmul(a, w) = (fma(a.re, w.re, -(a.im*w.im)), fma(a.re, w.im, a.im*w.re));
  *   * DFT4 / DFT8 (even-odd of two DFT4) / DFT16 (4x4 with internal twiddles)
@@ -182,8 +184,24 @@ static void ssfft_forward(int n, const cd* tw, const cd* in, cd* out, cd* scratc
             const int k = j % ns;
             cd v[16];
             for (int q = 0; q < r; ++q) v[q] = src[j + q * nr];
-            if (ns > 1)
-                for (int q = 1; q < r; ++q) v[q] = c_mul(v[q], tw[q * k * step]);
+            if (ns > 1) {
+                /* SSFFT-2: w1 = tw[k*step]; higher powers by a fixed product tree */
+                cd w[16];
+                w[1] = tw[k * step];
+                if (r > 2) w[2] = c_mul(w[1], w[1]);
+                if (r > 3) w[3] = c_mul(w[2], w[1]);
+                if (r > 4) {
+                    w[4] = c_mul(w[2], w[2]);
+                    w[5] = c_mul(w[4], w[1]);
+                    w[6] = c_mul(w[4], w[2]);
+                    w[7] = c_mul(w[4], w[3]);
+                }
+                if (r > 8) {
+                    w[8] = c_mul(w[4], w[4]);
+                    for (int q = 9; q < 16; ++q) w[q] = c_mul(w[8], w[q - 8]);
+                }
+                for (int q = 1; q < r; ++q) v[q] = c_mul(v[q], w[q]);
+            }
             dft_r(v, r);
             const int base = (j - k) * r + k;
             for (int q = 0; q < r; ++q) dst[base + q * ns] = v[q];

@@ -4,8 +4,9 @@
 // (proj/src/frontend.cpp:127-183) and, fused, the column sum of
 // detector::estimate_psd_into (proj/src/detector.cpp:170-184).
 //
-// Arithmetic: the SSFFT-1 specification -- FP64 Stockham DIT
-// autosort, radix-16 passes + one radix-2^(log2N mod 4) pass, table twiddles,
+// Arithmetic: the SSFFT-2 specification -- FP64 Stockham DIT
+// autosort, radix-16 passes + one radix-2^(log2N mod 4) pass, one table
+// twiddle per butterfly and its powers by a fixed product tree,
 // explicit-rounding butterflies -- then out[k] = float(sqrt(fma(re, re,
 // im*im))) of bin (k + N/2) mod N, exactly the expression GCC emits for
 // proj/src/frontend.cpp:147 (vmulsd im*im; vfmadd re*re+.; vsqrtsd; cvtsd2ss).
@@ -139,8 +140,10 @@ __device__ __forceinline__ int pad_idx(int i) { return i + (i >> 4); }
 
 // Twiddle + butterflies of pass p on register data already holding this
 // pass's inputs: butterfly b_u = j + TPR*u owns v[u*R .. u*R+R-1].
-template <int LOGN, int PASS>
+template <int LOGN, int PASS, bool TWS>
 __device__ __forceinline__ void run_pass(cd* v, int j, const double2* __restrict__ tw) {
+    // tw points at the CTA's shared-memory copy of the pass tables (plain
+    // loads -> LDS.128) or, for N = 8192, at the global table
     using PL = FftPlan<LOGN>;
     constexpr int R = PL::radix(PASS);
     constexpr int NS = PL::ns(PASS);
@@ -151,26 +154,60 @@ __device__ __forceinline__ void run_pass(cd* v, int j, const double2* __restrict
             const int b = j + PL::TPR * u;
             const int k = b % NS;
             const double2* t = tw + PL::tw_off(PASS) + k;
-#ifndef SSB_EXP_NO_TW
-#pragma unroll
-            for (int r = 1; r < R; ++r) {
-                const double2 w = __ldg(t + (r - 1) * NS);
-                v[u * R + r] = c_mul(v[u * R + r], cd{w.x, w.y});
+            // SSFFT-2: w1 from the table, higher powers by a fixed product
+            // tree -- one table load per butterfly instead of R-1 (the loads,
+            // not the multiplies, were the cost: DESIGN.md §4)
+            const double2 w1t = TWS ? t[0] : __ldg(t);
+            cd w[16];
+            w[1] = cd{w1t.x, w1t.y};
+            if constexpr (R > 2) w[2] = c_mul(w[1], w[1]);
+            if constexpr (R > 3) w[3] = c_mul(w[2], w[1]);
+            if constexpr (R > 4) {
+                w[4] = c_mul(w[2], w[2]);
+                w[5] = c_mul(w[4], w[1]);
+                w[6] = c_mul(w[4], w[2]);
+                w[7] = c_mul(w[4], w[3]);
             }
-#else
-            (void)t;
-#endif
+            if constexpr (R > 8) {
+                w[8] = c_mul(w[4], w[4]);
+#pragma unroll
+                for (int q = 9; q < 16; ++q) w[q] = c_mul(w[8], w[q - 8]);
+            }
+#pragma unroll
+            for (int r = 1; r < R; ++r) v[u * R + r] = c_mul(v[u * R + r], w[r]);
         }
         dft_r<R>(v + u * R);
     }
 }
 
+__device__ __forceinline__ void group_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Next-iteration TMA issue, handed to the first exchange: once every thread of
+// the group has passed its first barrier, every thread has consumed the stage.
+struct StageIssue {
+    void* stage;
+    const void* src;
+    uint32_t bytes;
+    uint64_t* bar;
+    bool go;
+    bool leader;
+    __device__ __forceinline__ void operator()() const {
+        if (go && leader) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(bar, bytes);
+            bulk_g2s(stage, src, bytes, bar);
+        }
+    }
+};
+
 // Store pass PASS's outputs into smem (padded), then load pass PASS+1's
-// inputs -- real parts first, then imaginary parts, through one N-double
-// buffer: half the shared memory of a complex exchange, which leaves L1 room
-// for the pass twiddle tables (the 2-phase exchange costs two extra barriers).
+// inputs, real parts then imaginary parts through one N-double buffer (half
+// the shared memory of a complex exchange).  Barriers are the group's named
+// barrier, so the two row groups of a CTA never wait on each other.
 template <int LOGN, int PASS>
-__device__ __forceinline__ void exchange(cd* v, int j, double* buf) {
+__device__ __forceinline__ void exchange(cd* v, int j, double* buf, int bar_id, const StageIssue& nxt) {
     using PL = FftPlan<LOGN>;
     constexpr int R = PL::radix(PASS);
     constexpr int NS = PL::ns(PASS);
@@ -187,7 +224,8 @@ __device__ __forceinline__ void exchange(cd* v, int j, double* buf) {
 #pragma unroll
             for (int r = 0; r < R; ++r) buf[pad_idx(base + r * NS)] = half ? v[u * R + r].im : v[u * R + r].re;
         }
-        __syncthreads();
+        group_sync(bar_id, PL::NT);
+        if (PASS == 0 && half == 0) nxt();
 #pragma unroll
         for (int u = 0; u < U2; ++u) {
             const int b = j + PL::TPR * u;
@@ -198,19 +236,18 @@ __device__ __forceinline__ void exchange(cd* v, int j, double* buf) {
                 else v[u * R2 + r].re = x;
             }
         }
-        __syncthreads();
+        group_sync(bar_id, PL::NT);
     }
 }
 
-template <int LOGN, int PASS>
-__device__ __forceinline__ void passes_from(cd* v, int j, const double2* tw, double* buf) {
+template <int LOGN, int PASS, bool TWS>
+__device__ __forceinline__ void passes_from(cd* v, int j, const double2* tw, double* buf, int bar_id,
+                                            const StageIssue& nxt) {
     using PL = FftPlan<LOGN>;
-    run_pass<LOGN, PASS>(v, j, tw);
+    run_pass<LOGN, PASS, TWS>(v, j, tw);
     if constexpr (PASS + 1 < PL::NP) {
-#ifndef SSB_EXP_NO_XCHG
-        exchange<LOGN, PASS>(v, j, buf);
-#endif
-        passes_from<LOGN, PASS + 1>(v, j, tw, buf);
+        exchange<LOGN, PASS>(v, j, buf, bar_id, nxt);
+        passes_from<LOGN, PASS + 1, TWS>(v, j, tw, buf, bar_id, nxt);
     }
 }
 
@@ -239,11 +276,20 @@ __device__ __forceinline__ void mags(const cd* v, float* m) {
         const double y = rsqrt_seed(q);
         const double s0 = __dmul_rn(q, y);
         const double d = __fma_rn(-s0, s0, q);
-        const double s1 = __fma_rn(d, __dmul_rn(0.5, y), s0);
-        const uint32_t low29 = static_cast<uint32_t>(__double2loint(s1)) & 0x1FFFFFFFu;
-        const int dist = static_cast<int>(low29) - (1 << 28);
-        const bool ok = q >= 0x1p-120 && q <= 0x1p120 && (dist > 65536 || dist < -65536);
-        m[i] = __double2float_rn(s1);
+        // y/2 by an exponent decrement and the range / midpoint checks and the
+        // final float rounding on the integer pipe: the FP64 pipe keeps only
+        // the 5 arithmetic ops (F2F.F32.F64 runs at 14/clk/SM, tools/pipe_probe)
+        const double h = __hiloint2double(__double2hiint(y) - (1 << 20), __double2loint(y));
+        const double s1 = __fma_rn(d, h, s0);
+        const uint32_t hi = static_cast<uint32_t>(__double2hiint(s1));
+        const uint32_t lo = static_cast<uint32_t>(__double2loint(s1));
+        const int dist = static_cast<int>(lo & 0x1FFFFFFFu) - (1 << 28);
+        const uint32_t qe = static_cast<uint32_t>(__double2hiint(q)) >> 20;  // q >= 0: biased exponent
+        const bool ok = (qe - (1023u - 120u)) <= 240u && (dist > 65536 || dist < -65536);
+        // s1 in [2^-60, 2^60]: float exponent = double exponent - 896, mantissa
+        // = top 23 bits, +1 ulp when the dropped 29 bits exceed half (no ties here)
+        const uint32_t fb = ((hi - (896u << 20)) << 3) | (lo >> 29);
+        m[i] = __uint_as_float(fb + (dist > 0 ? 1u : 0u));
         slow |= ok ? 0u : (1u << i);
     }
     if (__any_sync(0xffffffffu, slow != 0)) {
@@ -260,75 +306,118 @@ struct FftArgs {
     const void* iq;      // n_rows_total * N samples, f32 or i16 interleaved
     float* tf;           // n_rows_total * N floats, may be null in PSD mode
     float* psd;          // n_plots * N (PSD mode)
-    const double2* tw;   // per-N pass twiddle table
+    const double2* tw;   // per-N pass twiddle table (global)
     long long total_rows;
     int rows_per_plot;   // PSD mode: T
+    int n_plots;
+};
+
+// CTA = GROUPS independent row groups of NT threads.  Each group owns one plot
+// (PSD mode) or a strided set of row iterations, its own exchange buffer, TMA
+// stage, mbarrier and named barrier.  One-row-per-iteration shapes (N >= 4096)
+// keep the per-column PSD accumulators in shared memory (freeing 32 registers
+// for butterfly ILP) and read the pass twiddles through L1; multi-row shapes
+// (N <= 2048) accumulate in registers and share an smem copy of the twiddles.
+template <int LOGN>
+struct K1Shape {
+    using PL = FftPlan<LOGN>;
+    static constexpr int GROUPS = LOGN >= 13 ? 1 : 2;
+    static constexpr bool TW_SMEM = PL::G > 1;
+    static constexpr bool ACC_SMEM = PL::G == 1;
+    static constexpr int XW = 1;  // doubles per exchange element (re and im go in turn)
+    static constexpr int THREADS = PL::NT * GROUPS;
+    __host__ __device__ static constexpr size_t tw_bytes() { return TW_SMEM ? sizeof(double2) * (PL::tw_size() > 0 ? PL::tw_size() : 1) : 0; }
+    __host__ __device__ static constexpr size_t group_bytes(int sample_bytes) {
+        return sizeof(double) * XW * PL::G * PL::SROW + static_cast<size_t>(sample_bytes) * PL::G * PL::N +
+               (PL::G > 1 ? sizeof(float) * PL::G * PL::N : 0) + (ACC_SMEM ? sizeof(double) * PL::N : 0);
+    }
+    __host__ __device__ static constexpr size_t smem(int sample_bytes) { return tw_bytes() + GROUPS * group_bytes(sample_bytes); }
 };
 
 template <int LOGN, int FMT, bool PSD>
-__global__ void __launch_bounds__(FftPlan<LOGN>::NT, (LOGN >= 13 ? 1 : 2))
+__global__ void __launch_bounds__(K1Shape<LOGN>::THREADS, 1)
 fft_mag_kernel(FftArgs a) {
     using PL = FftPlan<LOGN>;
+    using KS = K1Shape<LOGN>;
     constexpr int N = PL::N;
     constexpr int G = PL::G;
     constexpr int SAMPLE_BYTES = FMT == 0 ? 8 : 4;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double* buf = reinterpret_cast<double*>(smem_raw);                            // G * SROW
-    unsigned char* stage = smem_raw + sizeof(double) * G * PL::SROW;              // G*N samples
-    float* magbuf = reinterpret_cast<float*>(stage + SAMPLE_BYTES * G * N);       // G*N (G>1, PSD)
-    __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(8) uint64_t bars[KS::GROUPS];
 
-    const int tid = threadIdx.x;
-    const int g = tid / PL::TPR;
-    const int j = tid % PL::TPR;
-    double* mybuf = buf + g * PL::SROW;
+    const int gi = static_cast<int>(threadIdx.x) / PL::NT;  // row group
+    const int lt = static_cast<int>(threadIdx.x) % PL::NT;  // thread within the group
+    const int g = lt / PL::TPR;
+    const int j = lt % PL::TPR;
+    const int bar_id = 1 + gi;
 
-    // iteration space
+    // shared twiddle tables (N <= 4096)
+    const double2* tw = a.tw;
+    if constexpr (KS::TW_SMEM) {
+        double2* st = reinterpret_cast<double2*>(smem_raw);
+        for (int e = threadIdx.x; e < PL::tw_size(); e += KS::THREADS) st[e] = a.tw[e];
+        tw = st;
+    }
+    unsigned char* gbase = smem_raw + KS::tw_bytes() + gi * KS::group_bytes(SAMPLE_BYTES);
+    double* xbuf = reinterpret_cast<double*>(gbase);                                   // G * SROW
+    unsigned char* stage = gbase + sizeof(double) * KS::XW * G * PL::SROW;             // G*N samples
+    float* magbuf = reinterpret_cast<float*>(stage + SAMPLE_BYTES * G * N);           // G*N (G > 1)
+    double* sacc = reinterpret_cast<double*>(stage + SAMPLE_BYTES * G * N);           // N (ACC_SMEM)
+    double* mybuf = xbuf + KS::XW * g * PL::SROW;
+    uint64_t* bar = &bars[gi];
+
+    // iteration space of this group
     long long it_begin, it_end, it_step, row_base;
     if constexpr (PSD) {
-        row_base = static_cast<long long>(blockIdx.x) * a.rows_per_plot;
+        const long long plot = static_cast<long long>(blockIdx.x) * KS::GROUPS + gi;
+        row_base = plot * a.rows_per_plot;
         it_begin = 0;
-        it_end = (a.rows_per_plot + G - 1) / G;
+        it_end = plot < a.n_plots ? (a.rows_per_plot + G - 1) / G : 0;
         it_step = 1;
     } else {
         row_base = 0;
-        it_begin = blockIdx.x;
+        it_begin = static_cast<long long>(blockIdx.x) * KS::GROUPS + gi;
         it_end = (a.total_rows + G - 1) / G;
-        it_step = gridDim.x;
+        it_step = static_cast<long long>(gridDim.x) * KS::GROUPS;
     }
     const long long row_limit = PSD ? row_base + a.rows_per_plot : a.total_rows;
-
-    auto issue = [&](long long it) {
+    auto chunk = [&](long long it, const void** src, uint32_t* bytes) {
         const long long r0 = row_base + it * G;
         long long nr = row_limit - r0;
         if (nr > G) nr = G;
-        const uint32_t bytes = static_cast<uint32_t>(nr * N * SAMPLE_BYTES);
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&bar, bytes);
-        bulk_g2s(stage, static_cast<const unsigned char*>(a.iq) + r0 * N * SAMPLE_BYTES, bytes, &bar);
+        *src = static_cast<const unsigned char*>(a.iq) + r0 * N * SAMPLE_BYTES;
+        *bytes = static_cast<uint32_t>(nr * N * SAMPLE_BYTES);
     };
 
-    if (tid == 0) {
-        mbar_init(&bar, 1);
+    if (lt == 0) {
+        mbar_init(bar, 1);
         fence_mbar_init();
     }
-    __syncthreads();
-    if (tid == 0 && it_begin < it_end) issue(it_begin);
+    __syncthreads();  // twiddle copy + mbarrier init visible to all groups
+    if (lt == 0 && it_begin < it_end) {
+        StageIssue first{stage, nullptr, 0u, bar, true, true};
+        chunk(it_begin, &first.src, &first.bytes);
+        first();
+    }
 
-    // PSD accumulators: G == 1 -> per (u, r) column owned by this thread;
-    // G > 1 -> columns tid + NT*i, i < N/NT (>= 1 when N >= NT; else tid < N).
-    constexpr int NACC = PSD ? (G == 1 ? PL::P : (N >= PL::NT ? N / PL::NT : 1)) : 1;
+    constexpr int NACC = (PSD && !KS::ACC_SMEM) ? (G == 1 ? PL::P : (N >= PL::NT ? N / PL::NT : 1)) : 1;
     double acc[NACC];
 #pragma unroll
     for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+    if constexpr (PSD && KS::ACC_SMEM) {
+        for (int c = lt; c < N; c += PL::NT) sacc[c] = 0.0;  // each column is owned by one thread
+    }
 
+    constexpr int RL = PL::radix(PL::NP - 1);
+    constexpr int NSL = PL::ns(PL::NP - 1);
+    constexpr int UL = PL::P / RL;
     uint32_t phase = 0;
     for (long long it = it_begin; it < it_end; it += it_step) {
         const long long r0 = row_base + it * G;
         const long long row = r0 + g;
         const bool valid = row < row_limit;
 
-        mbar_wait(&bar, phase);
+        mbar_wait(bar, phase);
         phase ^= 1;
 
         // pass-0 inputs from the stage
@@ -336,46 +425,35 @@ fft_mag_kernel(FftArgs a) {
         {
             constexpr int R0 = PL::radix(0);
             constexpr int U0 = PL::P / R0;
-            if constexpr (FMT == 0) {
 #pragma unroll
-                for (int u = 0; u < U0; ++u)
+            for (int u = 0; u < U0; ++u) {
+                const int b = j + PL::TPR * u;
 #pragma unroll
-                    for (int r = 0; r < R0; ++r) {
-                        const int s = g * N + j + PL::TPR * u + r * (N / R0);
+                for (int r = 0; r < R0; ++r) {
+                    const int s = g * N + b + r * (N / R0);
+                    if constexpr (FMT == 0) {
                         const float2 x = valid ? reinterpret_cast<const float2*>(stage)[s] : make_float2(0.f, 0.f);
                         v[u * R0 + r] = {static_cast<double>(x.x), static_cast<double>(x.y)};
-                    }
-            } else {
-#pragma unroll
-                for (int u = 0; u < U0; ++u) {
-                    const int b = j + PL::TPR * u;
-#pragma unroll
-                    for (int r = 0; r < R0; ++r) {
-                        const int s = g * N + b + r * (N / R0);
+                    } else {
                         const short2 x = valid ? reinterpret_cast<const short2*>(stage)[s] : make_short2(0, 0);
-                        // frontend.cpp:383: raw * (1.0f/32768) (exact), promoted to double
+                        // frontend.cpp:383: raw * (1.0f/32768) is exact, so (double)raw * 2^-15
                         v[u * R0 + r] = {__dmul_rn(static_cast<double>(x.x), 0x1p-15),
                                          __dmul_rn(static_cast<double>(x.y), 0x1p-15)};
                     }
                 }
             }
         }
-        __syncthreads();  // stage consumed by every thread
-        if (tid == 0 && it + it_step < it_end) issue(it + it_step);
-
-        passes_from<LOGN, 0>(v, j, a.tw, mybuf);
+        StageIssue nxt{stage, nullptr, 0u, bar, it + it_step < it_end, lt == 0};
+        if (nxt.go) chunk(it + it_step, &nxt.src, &nxt.bytes);
+        if constexpr (PL::NP == 1) {  // no exchange barrier to piggy-back on
+            group_sync(bar_id, PL::NT);
+            nxt();
+        }
+        passes_from<LOGN, 0, KS::TW_SMEM>(v, j, tw, mybuf, bar_id, nxt);
 
         // epilogue: outputs of the last pass, index q = b + r*NS_last
-        constexpr int RL = PL::radix(PL::NP - 1);
-        constexpr int NSL = PL::ns(PL::NP - 1);
-        constexpr int UL = PL::P / RL;
         float m[PL::P];
-#ifndef SSB_EXP_NO_MAG
         mags<PL::P>(v, m);
-#else
-#pragma unroll
-        for (int i = 0; i < PL::P; ++i) m[i] = static_cast<float>(v[i].re);
-#endif
         if constexpr (G == 1) {
             float* out = a.tf ? a.tf + row * N : nullptr;
 #pragma unroll
@@ -388,7 +466,8 @@ fft_mag_kernel(FftArgs a) {
                     if constexpr (PSD) {
                         if (valid) {
                             const double md = static_cast<double>(m[u * RL + r]);
-                            acc[u * RL + r] = __fma_rn(md, md, acc[u * RL + r]);
+                            if constexpr (KS::ACC_SMEM) sacc[k] = __fma_rn(md, md, sacc[k]);  // column k is this thread's
+                            else acc[u * RL + r] = __fma_rn(md, md, acc[u * RL + r]);
                         }
                     }
                 }
@@ -405,18 +484,18 @@ fft_mag_kernel(FftArgs a) {
                     mrow[k] = m[u * RL + r];
                 }
             }
-            __syncthreads();
+            group_sync(bar_id, PL::NT);
             long long nvalid = row_limit - r0;
             if (nvalid > G) nvalid = G;
             if (a.tf) {
                 float* out = a.tf + r0 * N;
                 const int total = static_cast<int>(nvalid) * N;
-                for (int e = tid; e < total; e += PL::NT) out[e] = magbuf[e];
+                for (int e = lt; e < total; e += PL::NT) out[e] = magbuf[e];
             }
             if constexpr (PSD) {
 #pragma unroll
                 for (int i = 0; i < NACC; ++i) {
-                    const int c = tid + PL::NT * i;
+                    const int c = lt + PL::NT * i;
                     if (c < N) {
                         for (int gg = 0; gg < nvalid; ++gg) {
                             const double md = static_cast<double>(magbuf[gg * N + c]);
@@ -425,30 +504,30 @@ fft_mag_kernel(FftArgs a) {
                     }
                 }
             }
-            __syncthreads();
+            group_sync(bar_id, PL::NT);
         }
     }
 
     if constexpr (PSD) {
-        const double inv_rows = __ddiv_rn(1.0, static_cast<double>(a.rows_per_plot));
-        float* psd = a.psd + static_cast<long long>(blockIdx.x) * N;
-        if constexpr (G == 1) {
-            constexpr int RL = PL::radix(PL::NP - 1);
-            constexpr int NSL = PL::ns(PL::NP - 1);
-            constexpr int UL = PL::P / RL;
+        const long long plot = static_cast<long long>(blockIdx.x) * KS::GROUPS + gi;
+        if (plot < a.n_plots) {
+            const double inv_rows = __ddiv_rn(1.0, static_cast<double>(a.rows_per_plot));
+            float* psd = a.psd + plot * N;
+            if constexpr (G == 1) {
 #pragma unroll
-            for (int u = 0; u < UL; ++u)
+                for (int u = 0; u < UL; ++u)
 #pragma unroll
-                for (int r = 0; r < RL; ++r) {
-                    const int q = j + PL::TPR * u + r * NSL;
-                    const int k = (q + N / 2) & (N - 1);
-                    psd[k] = __double2float_rn(__dmul_rn(acc[u * RL + r], inv_rows));
+                    for (int r = 0; r < RL; ++r) {
+                        const int q = j + PL::TPR * u + r * NSL;
+                        const int k = (q + N / 2) & (N - 1);
+                        psd[k] = __double2float_rn(__dmul_rn(KS::ACC_SMEM ? sacc[k] : acc[u * RL + r], inv_rows));
+                    }
+            } else {
+#pragma unroll
+                for (int i = 0; i < NACC; ++i) {
+                    const int c = lt + PL::NT * i;
+                    if (c < N) psd[c] = __double2float_rn(__dmul_rn(acc[i], inv_rows));
                 }
-        } else {
-#pragma unroll
-            for (int i = 0; i < NACC; ++i) {
-                const int c = tid + PL::NT * i;
-                if (c < N) psd[c] = __double2float_rn(__dmul_rn(acc[i], inv_rows));
             }
         }
     }
@@ -457,6 +536,7 @@ fft_mag_kernel(FftArgs a) {
 } // namespace ssb
 
 // ------------------------------------------------------------------ host side
+
 
 namespace ssb {
 
@@ -483,30 +563,16 @@ static void build_tw(std::vector<double2>& out) {
     }
 }
 
-template <int LOGN>
-static size_t smem_bytes(int fmt) {
-    using PL = FftPlan<LOGN>;
-    const size_t sb = fmt == 0 ? 8 : 4;
-    size_t bytes = sizeof(double) * PL::G * PL::SROW + sb * PL::G * PL::N;
-    if (PL::G > 1) bytes += sizeof(float) * PL::G * PL::N;
-    return bytes;
-}
-
 template <int LOGN, int FMT, bool PSD>
 static cudaError_t launch_one(const FftLaunch& L, cudaStream_t st) {
     using PL = FftPlan<LOGN>;
+    using KS = K1Shape<LOGN>;
     auto kern = fft_mag_kernel<LOGN, FMT, PSD>;
-    const size_t smem = smem_bytes<LOGN>(FMT);
+    const size_t smem = KS::smem(FMT == 0 ? 8 : 4);
     static bool attr_done = false;  // per instantiation
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        // carve out only what the resident CTAs need; the rest stays L1 for the
-        // pass-major twiddle tables (~65 KB at N = 4096)
-        const int per_sm = static_cast<int>((smem + 1024) * (LOGN >= 13 ? 1 : 2));
-        const int pct = (per_sm * 100 + 228 * 1024 - 1) / (228 * 1024);
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
@@ -517,16 +583,17 @@ static cudaError_t launch_one(const FftLaunch& L, cudaStream_t st) {
     a.tw = L.tw;
     a.total_rows = L.total_rows;
     a.rows_per_plot = L.rows_per_plot;
+    a.n_plots = L.n_plots;
     long long grid;
     if (PSD) {
-        grid = L.n_plots;
+        grid = (L.n_plots + KS::GROUPS - 1) / KS::GROUPS;
     } else {
         const long long iters = (L.total_rows + PL::G - 1) / PL::G;
-        const long long cap = static_cast<long long>(L.num_sms) * (LOGN >= 13 ? 1 : 2);
-        grid = iters < cap ? iters : cap;
+        const long long groups = (iters + KS::GROUPS - 1) / KS::GROUPS;
+        grid = groups < L.num_sms ? groups : L.num_sms;
     }
     if (grid <= 0) return cudaSuccess;
-    kern<<<static_cast<unsigned>(grid), PL::NT, smem, st>>>(a);
+    kern<<<static_cast<unsigned>(grid), KS::THREADS, smem, st>>>(a);
     return cudaGetLastError();
 }
 
