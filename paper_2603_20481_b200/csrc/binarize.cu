@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(kBinThreads) binarize_kernel(BinarizeLaunch a)
         const uint32_t* h = hist + c * kHistStride;
         unsigned long long cnt[8], wsum[8];
         unsigned long long lc = 0, ls = 0;
+        uint32_t nz = 0;  // bins whose count is non-zero (or bin 0)
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const int bin = lane * 8 + q;
@@ -142,6 +143,7 @@ __global__ void __launch_bounds__(kBinThreads) binarize_kernel(BinarizeLaunch a)
             ls += static_cast<unsigned long long>(bin) * h[bin];
             cnt[q] = lc;
             wsum[q] = ls;
+            nz |= (h[bin] != 0u || bin == 0) ? (1u << q) : 0u;
         }
         // exclusive prefix over lanes of (lc, ls)
         unsigned long long pc = lc, ps = ls;
@@ -165,8 +167,10 @@ __global__ void __launch_bounds__(kBinThreads) binarize_kernel(BinarizeLaunch a)
             const unsigned long long w0 = pc + cnt[q];
             const unsigned long long w1 = total - w0;
             const double sum0 = static_cast<double>(ps + wsum[q]);
-            double var = 0.0;
-            if (w0 > 0 && w1 > 0) {
+            // an empty bin i > 0 repeats bin i-1's (w0, sum0), hence its
+            // variance: it can never be the first maximum, so skip its divides
+            double var = ((nz >> q) & 1u) ? 0.0 : -1.0;
+            if (((nz >> q) & 1u) && w0 > 0 && w1 > 0) {
                 const double mu0 = __ddiv_rn(sum0, static_cast<double>(w0));
                 const double mu1 = __ddiv_rn(__dsub_rn(sum_all, sum0), static_cast<double>(w1));
                 const double d = __dsub_rn(mu0, mu1);
@@ -294,31 +298,42 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     cp_async_wait_all();
     __syncthreads();
 
-    // ---- sweep A: column c = tid & 7 over rows tid>>3, +32 ...
+    // ---- sweep A: two threads per row, one float4 (4 columns) each; fminf /
+    // fmaxf equal std::min / std::max here (NaN is never taken by either, and
+    // the sign of a zero extreme never reaches an output)
     const int c = tid & 7;
-    float lo = INFINITY, hi = -INFINITY;
-    for (int r = tid >> 3; r < rows; r += kBinThreads / kTileCols) {
-        const float x = bt_vals[r * kTileCols + c];
-        lo = (x < lo) ? x : lo;
-        hi = (hi < x) ? x : hi;
-    }
-    // reduce the 4 lanes of a warp sharing column c (lane, lane^8, lane^16, lane^24)
+    {
+        const int hh = tid & 1;
+        float lo4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+        float hi4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        for (int r = tid >> 1; r < rows; r += kBinThreads / 2) {
+            const float4 x = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols + 4 * hh);
+            lo4[0] = fminf(lo4[0], x.x); hi4[0] = fmaxf(hi4[0], x.x);
+            lo4[1] = fminf(lo4[1], x.y); hi4[1] = fmaxf(hi4[1], x.y);
+            lo4[2] = fminf(lo4[2], x.z); hi4[2] = fmaxf(hi4[2], x.z);
+            lo4[3] = fminf(lo4[3], x.w); hi4[3] = fmaxf(hi4[3], x.w);
+        }
 #pragma unroll
-    for (int o = 8; o < 32; o <<= 1) {
-        const float ol = __shfl_xor_sync(0xffffffffu, lo, o), oh = __shfl_xor_sync(0xffffffffu, hi, o);
-        lo = (ol < lo) ? ol : lo;
-        hi = (hi < oh) ? oh : hi;
-    }
-    if (lane < kTileCols) {
-        s_lo[warp][lane] = lo;
-        s_hi[warp][lane] = hi;
+        for (int o = 2; o < 32; o <<= 1)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                lo4[q] = fminf(lo4[q], __shfl_xor_sync(0xffffffffu, lo4[q], o));
+                hi4[q] = fmaxf(hi4[q], __shfl_xor_sync(0xffffffffu, hi4[q], o));
+            }
+        if (lane < 2) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                s_lo[warp][4 * lane + q] = lo4[q];
+                s_hi[warp][4 * lane + q] = hi4[q];
+            }
+        }
     }
     __syncthreads();
     if (tid < kTileCols) {
         float l = s_lo[0][tid], h = s_hi[0][tid];
         for (int q = 1; q < kBinWarps; ++q) {
-            l = (s_lo[q][tid] < l) ? s_lo[q][tid] : l;
-            h = (h < s_hi[q][tid]) ? s_hi[q][tid] : h;
+            l = fminf(l, s_lo[q][tid]);
+            h = fmaxf(h, s_hi[q][tid]);
         }
         const float scale = __fdiv_rn(256.0f, __fsub_rn(h, l));
         const bool valid = h > l && isfinite(scale);
@@ -346,16 +361,20 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     // ---- Otsu: warp w handles column w
     if (warp < kTileCols && c_use[warp]) {
         const int cc = warp;
-        const uint32_t* h = hist + cc * kHistStride;
+        uint32_t hq[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) hq[q] = hist[cc * kHistStride + lane * 8 + q];
         unsigned long long cnt[8], wsum[8];
         unsigned long long lc = 0, ls = 0;
+        uint32_t nz = 0;  // bins whose count is non-zero (or bin 0)
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const int bin = lane * 8 + q;
-            lc += h[bin];
-            ls += static_cast<unsigned long long>(bin) * h[bin];
+            lc += hq[q];
+            ls += static_cast<unsigned long long>(bin) * hq[q];
             cnt[q] = lc;
             wsum[q] = ls;
+            nz |= (hq[q] != 0u || bin == 0) ? (1u << q) : 0u;
         }
         unsigned long long pc = lc, ps = ls;
 #pragma unroll
@@ -378,8 +397,10 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
             const unsigned long long w0 = pc + cnt[q];
             const unsigned long long w1 = total - w0;
             const double sum0 = static_cast<double>(ps + wsum[q]);
-            double var = 0.0;
-            if (w0 > 0 && w1 > 0) {
+            // an empty bin i > 0 repeats bin i-1's (w0, sum0), hence its
+            // variance: it can never be the first maximum, so skip its divides
+            double var = ((nz >> q) & 1u) ? 0.0 : -1.0;
+            if (((nz >> q) & 1u) && w0 > 0 && w1 > 0) {
                 const double mu0 = __ddiv_rn(sum0, static_cast<double>(w0));
                 const double mu1 = __ddiv_rn(__dsub_rn(sum_all, sum0), static_cast<double>(w1));
                 const double d = __dsub_rn(mu0, mu1);
