@@ -48,6 +48,10 @@ typedef enum { SS_FMT_F32 = 0, SS_FMT_I16 = 1 } ss_fmt; /* frontend.hpp:134 Samp
 
 typedef enum { SS_ERODE = 0, SS_DILATE = 1, SS_OPEN = 2, SS_CLOSE = 3 } ss_morph_op; /* detector.hpp:54 */
 
+/* STFT extension windows (BASELINE config 5 as written; no reference oracle):
+   rectangular, or periodic Hann w[n] = 0.5*(1 - cos(2*pi*n/N)). */
+typedef enum { SS_WIN_RECT = 0, SS_WIN_HANN = 1 } ss_window;
+
 typedef struct ss_ctx ss_ctx;
 
 /* DetectorConfig (proj/include/specsense/detector.hpp:11-23), same defaults. */
@@ -124,6 +128,14 @@ ss_status ss_stage_times(const ss_ctx* ctx, double* ms8);
 ss_status ss_tf_plots(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int rows, int n_plots,
                       float* tf);
 
+/* STFT extension of ss_tf_plots (the reference is
+   rectangular with hop = n_fft): frame f covers samples
+   [f*hop, f*hop + n_fft), each sample multiplied by the window in double
+   before the same SSFFT-2 transform.  iq holds (n_plots*rows - 1)*hop +
+   n_fft samples.  hop = n_fft with SS_WIN_RECT reproduces ss_tf_plots. */
+ss_status ss_stft_plots(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int hop, int window, int rows,
+                        int n_plots, float* tf);
+
 /* ---- detector stages (one plot unless noted) --------------------------- */
 /* estimate_psd_into (detector.cpp:170-184): out[k - c0] for k in [c0, c1). */
 ss_status ss_psd_cols(ss_ctx* ctx, const float* tf, int rows, int cols, int c0, int c1, float* out);
@@ -175,6 +187,12 @@ ss_status ss_detect_batch(ss_ctx* ctx, const float* tf, int n_plots, int rows, i
 ss_status ss_sense_batch(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int rows, int n_plots,
                          uint64_t first_seq, double sample_rate_hz, const ss_detector_cfg* cfg,
                          float* tf_out, const ss_batch_out* out);
+
+/* STFT-extension form of ss_sense_batch: frames as in ss_stft_plots, plot p's
+   first frame = first_frame + p*rows, box times use the frame step hop/fs. */
+ss_status ss_stft_sense_batch(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int hop, int window, int rows,
+                              int n_plots, uint64_t first_frame, double sample_rate_hz,
+                              const ss_detector_cfg* cfg, float* tf_out, const ss_batch_out* out);
 
 /* ---- test hooks -------------------------------------------------------- */
 /* Device ports of glibc log10f (which=0) / powf(10, x) (which=1) over n

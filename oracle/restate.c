@@ -58,6 +58,49 @@ int oracle_tf_plot(const void* iq, int fmt, int n_fft, int rows, float* out) {
     return 0;
 }
 
+/* STFT extension (no reference oracle): frontend.cpp:127-171
+   with a window multiply (double) before the transform and frames every `hop`
+   samples.  window 0 = rectangular, 1 = periodic Hann 0.5*(1 - cos(2 pi n / N)). */
+int oracle_stft_plot(const void* iq, int fmt, int n_fft, int hop, int window, int rows, float* out) {
+    if (n_fft < 8 || !is_pow2(n_fft) || rows < 0 || hop < 1) return ORACLE_EVALIDATION;
+    double* w = (double*)malloc(sizeof(double) * (size_t)n_fft);
+    const double two_pi = 2.0 * 3.14159265358979323846;
+    for (int n = 0; n < n_fft; ++n)
+        w[n] = window == 1 ? 0.5 * (1.0 - cos((two_pi * (double)n) / (double)n_fft)) : 1.0;
+    fftw_complex* in = fftw_alloc_complex((size_t)n_fft);
+    fftw_complex* spec = fftw_alloc_complex((size_t)n_fft);
+    fftw_plan plan = fftw_plan_dft_1d(n_fft, in, in, FFTW_FORWARD, FFTW_ESTIMATE);
+    const int half = n_fft / 2;
+    for (int r = 0; r < rows; ++r) {
+        const size_t base = (size_t)r * (size_t)hop;
+        for (int i = 0; i < n_fft; ++i) {
+            double re, im;
+            if (fmt == 0) {
+                const float* f = (const float*)iq + 2 * (base + (size_t)i);
+                re = (double)f[0];
+                im = (double)f[1];
+            } else {
+                const int16_t* q = (const int16_t*)iq + 2 * (base + (size_t)i);
+                re = (double)((float)q[0] * (1.0f / 32768.0f));
+                im = (double)((float)q[1] * (1.0f / 32768.0f));
+            }
+            in[i][0] = re * w[i];
+            in[i][1] = im * w[i];
+        }
+        fftw_execute_dft(plan, in, spec);
+        float* o = out + (size_t)r * (size_t)n_fft;
+        for (int k = 0; k < n_fft; ++k) {
+            const int src = k < half ? k + half : k - half;
+            o[k] = (float)sqrt(fma(spec[src][0], spec[src][0], spec[src][1] * spec[src][1]));
+        }
+    }
+    fftw_destroy_plan(plan);
+    fftw_free(in);
+    fftw_free(spec);
+    free(w);
+    return 0;
+}
+
 /* detector.cpp:170-184 */
 int oracle_psd(const float* tf, int rows, int cols, int c0, int c1, float* out) {
     if (rows < 1 || cols < 1) return ORACLE_EVALIDATION;

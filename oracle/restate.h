@@ -17,6 +17,9 @@ extern "C" {
 /* frontend::fft_row / make_plot (frontend.cpp:127-171). fmt 0 = f32 IQ, 1 = i16. */
 int oracle_tf_plot(const void* iq, int fmt, int n_fft, int rows, float* out);
 
+/* STFT extension: window (0 rect, 1 periodic Hann) and frame step `hop`. */
+int oracle_stft_plot(const void* iq, int fmt, int n_fft, int hop, int window, int rows, float* out);
+
 /* detector::estimate_psd_into (detector.cpp:170-184). */
 int oracle_psd(const float* tf, int rows, int cols, int c0, int c1, float* out);
 

@@ -54,6 +54,9 @@ SIGNATURES = {
     "ss_enable_stage_timing": (_I, [_P, _I]),
     "ss_stage_times": (_I, [_P, C.POINTER(C.c_double)]),
     "ss_tf_plots": (_I, [_P, _P, _I, _I, _I, _I, _P]),
+    "ss_stft_plots": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _P]),
+    "ss_stft_sense_batch": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, C.c_uint64, C.c_double, C.POINTER(DetectorCfg), _P,
+                                 C.POINTER(BatchOut)]),
     "ss_psd_cols": (_I, [_P, _P, _I, _I, _I, _I, _P]),
     "ss_savgol_smooth": (_I, [_P, _P, _I, _I, _I, _P]),
     "ss_floor": (_I, [_P, _P, _I, C.POINTER(DetectorCfg), _P, _P, _P, C.POINTER(C.c_int32)]),

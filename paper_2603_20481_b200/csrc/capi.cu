@@ -36,6 +36,7 @@ struct ss_ctx {
     std::string err;
     std::map<int, double2*> tw;                       // per log2(n_fft)
     std::map<std::pair<int, int>, double*> sg;        // per (window, order)
+    std::map<std::pair<int, int>, double*> win;       // STFT window per (n_fft, kind)
     std::map<std::string, DevBuf> ws;                 // grow-only workspace
     int64_t launches = 0;
     // optional per-stage timing (CUDA events on the context stream)
@@ -128,6 +129,31 @@ ss_status twiddles(ss_ctx* ctx, int n_fft, const double2** out) {
     return SS_OK;
 }
 
+ss_status window_table(ss_ctx* ctx, int n_fft, int kind, const double** out) {
+    auto key = std::make_pair(n_fft, kind);
+    auto it = ctx->win.find(key);
+    if (it == ctx->win.end()) {
+        std::vector<double> w;
+        ssb::fft_window(n_fft, kind, w);
+        double* d = nullptr;
+        SS_CK(ctx, cudaMalloc(&d, sizeof(double) * w.size()));
+        SS_CK(ctx, cudaMemcpy(d, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice));
+        it = ctx->win.emplace(key, d).first;
+    }
+    *out = it->second;
+    return SS_OK;
+}
+
+// frame geometry of the STFT extension: hop in [1, n_fft], 16-byte aligned
+// frame starts for the TMA stage loads
+ss_status check_stft(ss_ctx* ctx, int n_fft, int hop, int window, ss_fmt fmt) {
+    if (window != SS_WIN_RECT && window != SS_WIN_HANN) return fail(ctx, SS_EVALIDATION, "unknown window");
+    if (hop < 1 || hop > n_fft) return fail(ctx, SS_EVALIDATION, "hop must be in [1, n_fft]");
+    const int align = fmt == SS_FMT_F32 ? 2 : 4;
+    if (hop % align != 0) return fail(ctx, SS_EUNSUPPORTED, "hop must keep frames 16-byte aligned (multiple of 2 f32 / 4 i16 samples)");
+    return SS_OK;
+}
+
 ss_status check_savgol(ss_ctx* ctx, int window, int order) {
     // detector.cpp:144-149
     if (window < 5 || window % 2 == 0) return fail(ctx, SS_EVALIDATION, "savgol window must be odd and >= 5");
@@ -179,8 +205,9 @@ bool is_device_ptr(const void* p) {
 ss_status run_ccl(ss_ctx* ctx, const uint32_t* bits, int n_plots, int rows, int cols, int min_area,
                   long long pool_cap, int* n_comp, long long cap, long long* extents, int* bin_boxes,
                   double* boxes, const unsigned long long* start_seq, double fs, int32_t* labels,
-                  int* overflow_host) {
+                  int* overflow_host, int time_bins = 0) {
     ssb::CclLaunch L;
+    L.time_bins = time_bins;
     L.bits = bits;
     L.n_plots = n_plots;
     L.rows = rows;
@@ -241,7 +268,7 @@ long long worst_pool(int rows, int cols) { return static_cast<long long>(rows) *
 // already in psd (fused into K1); else computed here.
 ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int cols,
                         const unsigned long long* seq_dev, double fs, const ss_detector_cfg& cfg,
-                        float* psd, bool psd_ready, const ss_batch_out& out_dev) {
+                        float* psd, bool psd_ready, const ss_batch_out& out_dev, int time_bins = 0) {
     const int W = (cols + 31) / 32;
     const double* wts = nullptr;
     ss_status s = weights(ctx, cfg.savgol_window, cfg.savgol_order, &wts);
@@ -300,7 +327,7 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
     s = run_ccl(ctx, m1, n_plots, rows, cols, cfg.min_component_area, default_pool(n_plots, rows, cols),
                 out_dev.n_boxes ? out_dev.n_boxes : ncomp, cap, nullptr,
                 reinterpret_cast<int*>(out_dev.bin_boxes), reinterpret_cast<double*>(out_dev.boxes), seq_dev, fs,
-                nullptr, overflow_h);
+                nullptr, overflow_h, time_bins);
     if (s != SS_OK) {
         cudaFreeHost(overflow_h);
         return s;
@@ -319,7 +346,7 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
             s = run_ccl(ctx, m1 + mo, 1, rows, cols, cfg.min_component_area, worst_pool(rows, cols), nb + p, cap,
                         nullptr, out_dev.bin_boxes ? reinterpret_cast<int*>(out_dev.bin_boxes) + 4 * cap * p : nullptr,
                         out_dev.boxes ? reinterpret_cast<double*>(out_dev.boxes) + 4 * cap * p : nullptr,
-                        seq_dev ? seq_dev + p : nullptr, fs, nullptr, nullptr);
+                        seq_dev ? seq_dev + p : nullptr, fs, nullptr, nullptr, time_bins);
             if (s != SS_OK) return s;
         }
         SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
@@ -372,6 +399,7 @@ void ss_close(ss_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (auto& kv : ctx->tw) cudaFree(kv.second);
     for (auto& kv : ctx->sg) cudaFree(kv.second);
+    for (auto& kv : ctx->win) cudaFree(kv.second);
     for (auto& kv : ctx->ws) cudaFree(kv.second.p);
     for (cudaEvent_t e : ctx->ev)
         if (e) cudaEventDestroy(e);
@@ -431,6 +459,40 @@ ss_status ss_tf_plots(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int ro
     L.rows_per_plot = rows;
     L.n_plots = n_plots;
     L.num_sms = ctx->num_sms;
+    SS_CK(ctx, ssb::fft_mag_launch(L, ctx->stream));
+    ctx->launches += 1;
+    return SS_OK;
+}
+
+ss_status ss_stft_plots(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int hop, int window, int rows,
+                        int n_plots, float* tf) {
+    if (!ctx) return SS_EVALIDATION;
+    if (n_fft < 8 || !is_pow2(n_fft))
+        return fail(ctx, SS_EVALIDATION, "FFT size must be a power of two >= 8, got " + std::to_string(n_fft));
+    if (n_fft > 8192) return fail(ctx, SS_EUNSUPPORTED, "device FFT supports n_fft <= 8192");
+    if (rows < 0 || n_plots < 0) return fail(ctx, SS_EVALIDATION, "negative plot geometry");
+    ss_status s = check_stft(ctx, n_fft, hop, window, fmt);
+    if (s != SS_OK) return s;
+    if (static_cast<long long>(rows) * n_plots == 0) return SS_OK;
+    if (reinterpret_cast<uintptr_t>(iq) % 16 != 0) return fail(ctx, SS_EVALIDATION, "IQ buffer must be 16-byte aligned");
+    const double2* tw = nullptr;
+    s = twiddles(ctx, n_fft, &tw);
+    if (s != SS_OK) return s;
+    const double* w = nullptr;
+    s = window_table(ctx, n_fft, window, &w);
+    if (s != SS_OK) return s;
+    ssb::FftLaunch L;
+    L.logn = ilog2(n_fft);
+    L.fmt = fmt;
+    L.iq = iq;
+    L.tf = tf;
+    L.tw = tw;
+    L.total_rows = static_cast<long long>(rows) * n_plots;
+    L.rows_per_plot = rows;
+    L.n_plots = n_plots;
+    L.num_sms = ctx->num_sms;
+    L.hop = hop;
+    L.win = w;
     SS_CK(ctx, ssb::fft_mag_launch(L, ctx->stream));
     ctx->launches += 1;
     return SS_OK;
@@ -650,8 +712,25 @@ ss_status ss_detect_batch(ss_ctx* ctx, const float* tf, int n_plots, int rows, i
     return SS_OK;
 }
 
+static ss_status sense_impl(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int hop, int window, int rows,
+                            int n_plots, uint64_t first_seq, double sample_rate_hz, const ss_detector_cfg* cfg,
+                            float* tf_out, const ss_batch_out* out);
+
 ss_status ss_sense_batch(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int rows, int n_plots, uint64_t first_seq,
                          double sample_rate_hz, const ss_detector_cfg* cfg, float* tf_out, const ss_batch_out* out) {
+    return sense_impl(ctx, iq, fmt, n_fft, n_fft, SS_WIN_RECT, rows, n_plots, first_seq, sample_rate_hz, cfg, tf_out,
+                      out);
+}
+
+ss_status ss_stft_sense_batch(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int hop, int window, int rows,
+                              int n_plots, uint64_t first_frame, double sample_rate_hz, const ss_detector_cfg* cfg,
+                              float* tf_out, const ss_batch_out* out) {
+    return sense_impl(ctx, iq, fmt, n_fft, hop, window, rows, n_plots, first_frame, sample_rate_hz, cfg, tf_out, out);
+}
+
+static ss_status sense_impl(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int hop, int window, int rows,
+                            int n_plots, uint64_t first_seq, double sample_rate_hz, const ss_detector_cfg* cfg,
+                            float* tf_out, const ss_batch_out* out) {
     if (!ctx || !cfg || !out) return SS_EVALIDATION;
     if (n_fft < 8 || !is_pow2(n_fft))
         return fail(ctx, SS_EVALIDATION, "FFT size must be a power of two >= 8, got " + std::to_string(n_fft));
@@ -661,8 +740,13 @@ ss_status ss_sense_batch(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int
     if (fmt != SS_FMT_F32 && fmt != SS_FMT_I16) return fail(ctx, SS_EVALIDATION, "unknown sample format");
     ss_status s = check_cfg(ctx, *cfg, n_fft);
     if (s != SS_OK) return s;
+    s = check_stft(ctx, n_fft, hop, window, fmt);
+    if (s != SS_OK) return s;
     if (n_plots <= 0) return SS_OK;
-    const size_t nsamp = static_cast<size_t>(n_plots) * rows * n_fft;
+    const bool stft = hop != n_fft || window != SS_WIN_RECT;
+    const size_t frames = static_cast<size_t>(n_plots) * rows;
+    const size_t nsamp = (frames - 1) * static_cast<size_t>(hop) + static_cast<size_t>(n_fft);  // input span
+    const size_t ntf = frames * static_cast<size_t>(n_fft);
     const size_t sbytes = fmt == SS_FMT_F32 ? 8 : 4;
     const void* diq = iq;
     if (!is_device_ptr(iq) || reinterpret_cast<uintptr_t>(iq) % 16 != 0) {
@@ -675,7 +759,7 @@ ss_status ss_sense_batch(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int
     const int cols = n_fft;
     float* tf = tf_out;
     if (!tf) {
-        SS_WS(t, float, "sense.tf", nsamp);
+        SS_WS(t, float, "sense.tf", ntf);
         tf = t;
     }
     // outputs: device pointers used directly, host pointers staged
@@ -723,6 +807,13 @@ ss_status ss_sense_batch(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int
     L.rows_per_plot = rows;
     L.n_plots = n_plots;
     L.num_sms = ctx->num_sms;
+    if (stft) {
+        const double* w = nullptr;
+        s = window_table(ctx, n_fft, window, &w);
+        if (s != SS_OK) return s;
+        L.hop = hop;
+        L.win = w;
+    }
     tmark(ctx, 0, 0);
     SS_CK(ctx, ssb::fft_mag_launch(L, ctx->stream));
     tmark(ctx, 0, 1);
@@ -732,7 +823,7 @@ ss_status ss_sense_batch(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int
     for (int p = 0; p < n_plots; ++p) hseq[p] = first_seq + static_cast<unsigned long long>(p) * rows;
     SS_CK(ctx, cudaMemcpyAsync(seq, hseq.data(), sizeof(unsigned long long) * n_plots, cudaMemcpyHostToDevice,
                                ctx->stream));
-    s = detect_device(ctx, tf, n_plots, rows, cols, seq, sample_rate_hz, *cfg, praw, true, dev);
+    s = detect_device(ctx, tf, n_plots, rows, cols, seq, sample_rate_hz, *cfg, praw, true, dev, hop);
     if (s != SS_OK) return s;
     if (host_out) {
         tmark(ctx, 7, 0);

@@ -220,7 +220,8 @@ __global__ void compact_kernel(int rows, int cols, const int* row_off, const lon
     const long long base = plot_base[p];
     const long long n = row_off[static_cast<long long>(p) * (rows + 1) + rows];
     const double fs = L.fs;
-    const double dt = __ddiv_rn(static_cast<double>(cols), fs);
+    // TFPlotView::dt_s = cols / fs (frontend.hpp:61); STFT extension: hop / fs
+    const double dt = __ddiv_rn(static_cast<double>(L.time_bins > 0 ? L.time_bins : cols), fs);
     const double df = __ddiv_rn(fs, static_cast<double>(cols));
     const double seq = L.start_seq ? static_cast<double>(L.start_seq[p]) : 0.0;
     if (threadIdx.x == 0) carry_s = 0;

@@ -310,6 +310,8 @@ struct FftArgs {
     long long total_rows;
     int rows_per_plot;   // PSD mode: T
     int n_plots;
+    int hop;             // samples between consecutive rows (N: rectangular, no overlap)
+    const double* win;   // N window weights (WIN mode), x_w = double(x) * w[n]
 };
 
 // CTA = GROUPS independent row groups of NT threads.  Each group owns one plot
@@ -334,7 +336,7 @@ struct K1Shape {
     __host__ __device__ static constexpr size_t smem(int sample_bytes) { return tw_bytes() + GROUPS * group_bytes(sample_bytes); }
 };
 
-template <int LOGN, int FMT, bool PSD>
+template <int LOGN, int FMT, bool PSD, bool WIN>
 __global__ void __launch_bounds__(K1Shape<LOGN>::THREADS, 1)
 fft_mag_kernel(FftArgs a) {
     using PL = FftPlan<LOGN>;
@@ -385,8 +387,10 @@ fft_mag_kernel(FftArgs a) {
         const long long r0 = row_base + it * G;
         long long nr = row_limit - r0;
         if (nr > G) nr = G;
-        *src = static_cast<const unsigned char*>(a.iq) + r0 * N * SAMPLE_BYTES;
-        *bytes = static_cast<uint32_t>(nr * N * SAMPLE_BYTES);
+        // rows (frames) start every `hop` samples; rectangular mode: hop == N
+        const int hop = WIN ? a.hop : N;
+        *src = static_cast<const unsigned char*>(a.iq) + r0 * hop * SAMPLE_BYTES;
+        *bytes = static_cast<uint32_t>(((nr - 1) * hop + N) * SAMPLE_BYTES);
     };
 
     if (lt == 0) {
@@ -430,7 +434,8 @@ fft_mag_kernel(FftArgs a) {
                 const int b = j + PL::TPR * u;
 #pragma unroll
                 for (int r = 0; r < R0; ++r) {
-                    const int s = g * N + b + r * (N / R0);
+                    const int n = b + r * (N / R0);  // sample position within the frame
+                    const int s = (WIN ? g * a.hop : g * N) + n;
                     if constexpr (FMT == 0) {
                         const float2 x = valid ? reinterpret_cast<const float2*>(stage)[s] : make_float2(0.f, 0.f);
                         v[u * R0 + r] = {static_cast<double>(x.x), static_cast<double>(x.y)};
@@ -439,6 +444,10 @@ fft_mag_kernel(FftArgs a) {
                         // frontend.cpp:383: raw * (1.0f/32768) is exact, so (double)raw * 2^-15
                         v[u * R0 + r] = {__dmul_rn(static_cast<double>(x.x), 0x1p-15),
                                          __dmul_rn(static_cast<double>(x.y), 0x1p-15)};
+                    }
+                    if constexpr (WIN) {  // STFT extension: one rounded product per component
+                        const double w = __ldg(a.win + n);
+                        v[u * R0 + r] = {__dmul_rn(v[u * R0 + r].re, w), __dmul_rn(v[u * R0 + r].im, w)};
                     }
                 }
             }
@@ -563,11 +572,11 @@ static void build_tw(std::vector<double2>& out) {
     }
 }
 
-template <int LOGN, int FMT, bool PSD>
+template <int LOGN, int FMT, bool PSD, bool WIN>
 static cudaError_t launch_one(const FftLaunch& L, cudaStream_t st) {
     using PL = FftPlan<LOGN>;
     using KS = K1Shape<LOGN>;
-    auto kern = fft_mag_kernel<LOGN, FMT, PSD>;
+    auto kern = fft_mag_kernel<LOGN, FMT, PSD, WIN>;
     const size_t smem = KS::smem(FMT == 0 ? 8 : 4);
     static bool attr_done = false;  // per instantiation
     if (!attr_done) {
@@ -584,6 +593,8 @@ static cudaError_t launch_one(const FftLaunch& L, cudaStream_t st) {
     a.total_rows = L.total_rows;
     a.rows_per_plot = L.rows_per_plot;
     a.n_plots = L.n_plots;
+    a.hop = L.hop > 0 ? L.hop : PL::N;
+    a.win = L.win;
     long long grid;
     if (PSD) {
         grid = (L.n_plots + KS::GROUPS - 1) / KS::GROUPS;
@@ -599,8 +610,25 @@ static cudaError_t launch_one(const FftLaunch& L, cudaStream_t st) {
 
 template <int LOGN>
 static cudaError_t dispatch_fmt(const FftLaunch& L, cudaStream_t st) {
-    if (L.fmt == 0) return L.psd ? launch_one<LOGN, 0, true>(L, st) : launch_one<LOGN, 0, false>(L, st);
-    return L.psd ? launch_one<LOGN, 1, true>(L, st) : launch_one<LOGN, 1, false>(L, st);
+    if (L.win) {
+        if (L.fmt == 0) return L.psd ? launch_one<LOGN, 0, true, true>(L, st) : launch_one<LOGN, 0, false, true>(L, st);
+        return L.psd ? launch_one<LOGN, 1, true, true>(L, st) : launch_one<LOGN, 1, false, true>(L, st);
+    }
+    if (L.fmt == 0) return L.psd ? launch_one<LOGN, 0, true, false>(L, st) : launch_one<LOGN, 0, false, false>(L, st);
+    return L.psd ? launch_one<LOGN, 1, true, false>(L, st) : launch_one<LOGN, 1, false, false>(L, st);
+}
+
+// STFT extension window (BASELINE config 5: "4096-pt Hann STFT with 50%
+// overlap"; no reference oracle -- SURVEY.md §8(f) F2): periodic Hann,
+// w[n] = 0.5 * (1 - cos(t)), t = (2 pi n) / N, glibc cos in double.
+void fft_window(int n_fft, int kind, std::vector<double>& out) {
+    out.assign(static_cast<size_t>(n_fft), 1.0);
+    if (kind != 1) return;
+    const double two_pi = 2.0 * 3.14159265358979323846;
+    for (int n = 0; n < n_fft; ++n) {
+        const double t = (two_pi * static_cast<double>(n)) / static_cast<double>(n_fft);
+        out[static_cast<size_t>(n)] = 0.5 * (1.0 - std::cos(t));
+    }
 }
 
 cudaError_t fft_mag_launch(const FftLaunch& L, cudaStream_t st) {

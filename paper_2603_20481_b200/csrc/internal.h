@@ -21,8 +21,11 @@ struct FftLaunch {
     int rows_per_plot = 0;
     int n_plots = 0;
     int num_sms = 148;
+    int hop = 0;                 // STFT extension: frame step (0 = n_fft, the reference's rectangular hop)
+    const double* win = nullptr; // STFT extension: device window weights (null = rectangular)
 };
 cudaError_t fft_mag_launch(const FftLaunch& L, cudaStream_t st);
+void fft_window(int n_fft, int kind, std::vector<double>& out);  // kind 0 rect, 1 periodic Hann
 void fft_twiddles(int logn, std::vector<double2>& out);
 
 // ---- K2/K3 floor.cu
@@ -121,6 +124,7 @@ struct CclLaunch {
     double* boxes = nullptr;          // n_plots x cap x 4 (f0,f1,t0,t1) or null
     const unsigned long long* start_seq = nullptr;  // n_plots (boxes)
     double fs = 0.0;
+    int time_bins = 0;                // samples per row step for t: cols (reference) or the STFT hop
     int32_t* labels = nullptr;        // rows x cols label raster (single plot) or null
 };
 cudaError_t ccl_launch(const CclLaunch& L, cudaStream_t st);

@@ -199,6 +199,30 @@ def make_plots(samples: np.ndarray, sample_rate_hz: float, n_fft: int, plot_rows
     return _host(make_plots_device(_dev(raw), n_fft, plot_rows, n_plots, fmt))
 
 
+def stft_plots(samples: np.ndarray, sample_rate_hz: float, n_fft: int, hop: int, window: int, plot_rows: int,
+               fmt: int = N.SS_FMT_F32) -> np.ndarray:
+    """STFT extension of make_plots (BASELINE config 5 as written): frames every
+    `hop` samples, window 0 = rectangular / 1 = periodic Hann; consecutive plots
+    of `plot_rows` frames."""
+    if fmt == N.SS_FMT_I16:
+        raw = np.ascontiguousarray(samples, np.int16)
+        n = len(raw) // 2
+    else:
+        raw = np.ascontiguousarray(samples.astype(np.complex64)).view(np.float32)
+        n = len(samples)
+    frames = (n - n_fft) // hop + 1 if n >= n_fft else 0
+    n_plots = frames // plot_rows
+    if n_plots == 0:
+        return np.zeros((0, plot_rows, n_fft), np.float32)
+    torch = _torch()
+    ctx = _ctx()
+    span = (n_plots * plot_rows - 1) * hop + n_fft
+    d = _dev(raw[: 2 * span])
+    tf = torch.empty((n_plots, plot_rows, n_fft), dtype=torch.float32, device="cuda")
+    ctx.check(ctx.lib.ss_stft_plots(ctx.h, _ptr(d), fmt, n_fft, hop, window, plot_rows, n_plots, _ptr(tf)))
+    return _host(tf)
+
+
 def fft_row(chunk: np.ndarray) -> np.ndarray:
     """frontend::fft_row (frontend.cpp:127-149)."""
     n = len(chunk)
@@ -390,8 +414,9 @@ def detect(tf: np.ndarray, config: DetectorConfig | None = None, sample_rate_hz:
 
 def sense(samples: np.ndarray, sample_rate_hz: float, n_fft: int, plot_rows: int,
           config: DetectorConfig | None = None, fmt: int = N.SS_FMT_F32, first_seq: int = 0,
-          box_capacity: int = 1024, return_tf: bool = False):
-    """IQ -> Detections per full window (make_plots + detect, the runtime's per-plot work)."""
+          box_capacity: int = 1024, return_tf: bool = False, hop: int | None = None, window: int = 0):
+    """IQ -> Detections per full window (make_plots + detect, the runtime's per-plot work).
+    hop / window select the STFT extension (default: the reference's rect, hop = n_fft)."""
     config = config or DetectorConfig()
     ctx = _ctx()
     torch = _torch()
@@ -401,16 +426,24 @@ def sense(samples: np.ndarray, sample_rate_hz: float, n_fft: int, plot_rows: int
     else:
         raw = np.ascontiguousarray(samples.astype(np.complex64)).view(np.float32)
         n = len(samples)
-    P = n // (plot_rows * n_fft)
+    hop = n_fft if hop is None else hop
+    frames = (n - n_fft) // hop + 1 if n >= n_fft else 0
+    P = frames // plot_rows
     if P == 0:
         return ([], None) if return_tf else []
-    raw = raw[: P * plot_rows * n_fft * 2]
+    span = (P * plot_rows - 1) * hop + n_fft
+    raw = raw[: 2 * span]
     d = _dev(raw)
     tf = torch.empty((P, plot_rows, n_fft), dtype=torch.float32, device="cuda") if return_tf else None
     t, out = _batch_out(torch, P, n_fft, box_capacity)
     cfg = config.c()
-    ctx.check(ctx.lib.ss_sense_batch(ctx.h, _ptr(d), fmt, n_fft, plot_rows, P, first_seq, float(sample_rate_hz),
-                                     C.byref(cfg), _ptr(tf) if tf is not None else None, C.byref(out)))
+    if hop == n_fft and window == 0:
+        ctx.check(ctx.lib.ss_sense_batch(ctx.h, _ptr(d), fmt, n_fft, plot_rows, P, first_seq, float(sample_rate_hz),
+                                         C.byref(cfg), _ptr(tf) if tf is not None else None, C.byref(out)))
+    else:
+        ctx.check(ctx.lib.ss_stft_sense_batch(ctx.h, _ptr(d), fmt, n_fft, hop, window, plot_rows, P, first_seq,
+                                              float(sample_rate_hz), C.byref(cfg),
+                                              _ptr(tf) if tf is not None else None, C.byref(out)))
     dets = _unpack_batch(t, P)
     return (dets, _host(tf)) if return_tf else dets
 

@@ -223,6 +223,7 @@ class _Ora:
         sig = {
             "oracle_tf_plot": ([C.c_void_p, C.c_int, C.c_int, C.c_int, _f32p], C.c_int),
             "oracle_psd": ([_f32p, C.c_int, C.c_int, C.c_int, C.c_int, _f32p], C.c_int),
+            "oracle_stft_plot": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _f32p], C.c_int),
             "oracle_savgol_weights": ([C.c_int, C.c_int, _f64p], C.c_int),
             "oracle_savgol_smooth": ([_f32p, C.c_int, C.c_int, C.c_int, _f32p], C.c_int),
             "oracle_floor_prune": ([_f32p, C.c_int, C.c_int, C.c_int, C.c_double, _f32p, _f32p,
@@ -262,6 +263,16 @@ class _Ora:
         out = np.empty((rows, n_fft), np.float32)
         self._chk(self.L.oracle_tf_plot(iq.ctypes.data_as(C.c_void_p), fmt, n_fft, rows,
                                         out.reshape(-1)))
+        return out
+
+    def stft_plot(self, iq: np.ndarray, n_fft: int, hop: int, window: int, rows: int) -> np.ndarray:
+        iq = np.ascontiguousarray(iq)
+        fmt = 1 if iq.dtype == np.int16 else 0
+        if fmt == 0:
+            iq = iq.astype(np.complex64, copy=False)
+        out = np.empty((rows, n_fft), np.float32)
+        self._chk(self.L.oracle_stft_plot(iq.ctypes.data_as(C.c_void_p), fmt, n_fft, hop, window, rows,
+                                          out.reshape(-1)))
         return out
 
     def psd(self, tf, c0=0, c1=None):

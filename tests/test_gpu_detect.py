@@ -134,3 +134,25 @@ def test_config_validation(ss):
         ss.detect_batch(np.ones((1, 10, 64), np.float32), 1e6, ss.DetectorConfig(savgol_window=30))
     with pytest.raises(ss.ValidationError):
         ss.detect_batch(np.ones((1, 10, 64), np.float32), 1e6, ss.DetectorConfig(min_component_area=0))
+
+
+def test_stft_hann_detect(ss, ref, ora):
+    """Config 5 as written (4096-pt Hann, 50 % overlap) end to end on the device
+    vs the oracle restatement: TF plot, PSD, active set, bin boxes bit-exact;
+    box times on the hop/fs frame grid."""
+    sc = signals.c5_scenario(7, duration_s=0.025)
+    iq, _ = ref.synthesize(signals.scenario_json(sc))
+    fs, n_fft, hop, rows = 100e6, 4096, 2048, 600
+    dets, tf = ss.sense(iq, fs, n_fft, rows, hop=hop, window=1, return_tf=True, first_seq=0)
+    assert len(dets) == 2
+    exp_tf = ora.stft_plot(iq, n_fft, hop, 1, 2 * rows).reshape(2, rows, n_fft)
+    for p, det in enumerate(dets):
+        assert np.array_equal(tf[p].view(np.uint32), exp_tf[p].view(np.uint32))
+        exp = ora.detect(exp_tf[p], start_seq=p * rows, fs=fs)
+        assert np.array_equal(det.psd.raw, exp["raw"]) and np.array_equal(det.active_columns, exp["active"])
+        assert np.array_equal(det.bin_boxes, exp["bin_boxes"])
+        bb = exp["bin_boxes"].astype(np.float64)
+        dt, df = hop / fs, fs / n_fft
+        assert np.array_equal(det.boxes[:, 0], (bb[:, 2] - n_fft // 2) * df)
+        assert np.array_equal(det.boxes[:, 2], (p * rows + bb[:, 0]) * dt)
+        assert np.array_equal(det.boxes[:, 3], (p * rows + bb[:, 1]) * dt)

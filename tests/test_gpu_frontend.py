@@ -89,3 +89,32 @@ def test_validation(ss):
         ss.make_plots(np.zeros(100, np.complex64), 0.0, 16, 5)
     with pytest.raises(ss.ValidationError):
         ss.make_plots(np.zeros(100, np.complex64), 1e6, 16, 0)
+
+
+@pytest.mark.parametrize("n_fft,hop,window", [(1024, 512, 1), (4096, 2048, 1), (256, 64, 1), (1024, 1024, 1),
+                                              (512, 256, 0), (8192, 4096, 1)])
+def test_stft_extension_bit_exact(ss, ora, n_fft, hop, window):
+    """STFT extension (config 5 as written: Hann, 50 % overlap) vs the oracle's
+    restatement (frontend path + window multiply + hop); no reference oracle."""
+    rng = np.random.default_rng(n_fft + hop)
+    rows = max(3, min(90, (1 << 18) // n_fft))
+    n = (2 * rows - 1) * hop + n_fft + 7
+    x = _rand_iq(rng, n)
+    got = ss.stft_plots(x, 1e6, n_fft, hop, window, rows)
+    assert got.shape == (2, rows, n_fft)
+    exp = ora.stft_plot(x, n_fft, hop, window, 2 * rows).reshape(2, rows, n_fft)
+    assert np.array_equal(got.view(np.uint32), exp.view(np.uint32))
+
+
+def test_stft_rect_equals_make_plots(ss, ref):
+    rng = np.random.default_rng(9)
+    x = _rand_iq(rng, 40 * 1024)
+    assert np.array_equal(ss.stft_plots(x, 1e6, 1024, 1024, 0, 20), ref.make_plots(x, 1e6, 1024, 20))
+
+
+def test_stft_int16(ss, ora):
+    rng = np.random.default_rng(10)
+    raw = rng.integers(-32768, 32768, size=2 * (39 * 512 + 1024), dtype=np.int16)
+    got = ss.stft_plots(raw, 1e6, 1024, 512, 1, 20, fmt=1)
+    exp = ora.stft_plot(raw, 1024, 512, 1, 40).reshape(2, 20, 1024)
+    assert np.array_equal(got.view(np.uint32), exp.view(np.uint32))

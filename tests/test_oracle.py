@@ -257,3 +257,11 @@ def test_single_burst_iou_reference(ref):
     assert len(c["plots"][0]["bin_boxes"]) == 1
     box = np.array(c["plots"][0]["boxes_bits"], np.uint64).view(np.float64)[0]
     assert ref.iou(box, np.array(c["truth"][0][:4])) >= 0.6
+
+
+def test_stft_restatement_rect_is_tf_plot(ora):
+    rng = np.random.default_rng(12)
+    x = (rng.normal(size=30 * 512) + 1j * rng.normal(size=30 * 512)).astype(np.complex64)
+    assert np.array_equal(ora.stft_plot(x, 512, 512, 0, 30), ora.tf_plot(x, 512, 30))
+    h = ora.stft_plot(x, 512, 256, 1, 50)
+    assert h.shape == (50, 512) and np.all(np.isfinite(h))
