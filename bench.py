@@ -8,7 +8,11 @@ proj/src/frontend.cpp:177) -> PSD / SG floor / prune -> per-column Otsu ->
 close3x3/open3x3/open1x3 -> 4-connected components -> boxes.  A step is one
 batch of `--batch` captures through ss_sense_batch (the fused C-ABI call).
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--mode c5r|hann]
+
+--mode hann runs config 5 as BASELINE.json writes it (periodic Hann, hop 2048,
+T = 4881 frames per 100 ms plot of a continuous stream) through the STFT
+extension entry point ss_stft_sense_batch; its CPU arm is the oracle port.
 
 Under torchrun each rank processes its own captures (weak scaling); boxes
 are gathered to every rank with one NCCL all_gather per step (the path's only
@@ -31,11 +35,34 @@ sys.path.insert(0, str(ROOT))
 FS = 100e6
 N_FFT = 4096
 CAPTURE_S = 0.1
-ROWS = int(CAPTURE_S * FS) // N_FFT            # 2441
-SAMPLES = ROWS * N_FFT                         # processed samples per capture
-ALG_BYTES = SAMPLES * 8 + ROWS * N_FFT * 4     # K1 algorithmic bytes per capture (read IQ, write TF)
-ALG_FLOP64 = ROWS * 5 * N_FFT * 12             # conventional 5 N log2 N per row
 FP64_PEAK_TFLOPS = 33.9                        # measured DFMA peak, tools/fp64_peak.cu (profiles/fp64_peak.txt)
+
+
+class Workload:
+    """One plot = `rows` frames of `n_fft` samples every `hop` samples of a
+    continuous 100 MS/s stream.  c5r: hop = n_fft, rect (the reference's own
+    frontend, frontend.cpp:127-183) -> plots are back-to-back 100 ms captures.
+    hann: config 5 as written (periodic Hann, 50 % overlap, STFT extension)."""
+
+    def __init__(self, name, hop, window, desc):
+        self.name, self.hop, self.window, self.desc = name, hop, window, desc
+        self.rows = (int(CAPTURE_S * FS) - N_FFT) // hop + 1          # 2441 | 4881
+        self.stride = self.rows * hop                                  # new samples per plot
+        self.tail = N_FFT - hop                                        # extra samples after the last plot
+        # K1 algorithmic bytes per plot: read its new IQ once + write the TF plot
+        self.alg_bytes = self.stride * 8 + self.rows * N_FFT * 4
+        self.alg_flop64 = self.rows * 5 * N_FFT * 12                   # conventional 5 N log2 N per row
+
+    def samples(self, plots):
+        return plots * self.stride + self.tail
+
+
+WORKLOADS = {
+    "c5r": Workload("c5r", N_FFT, 0, "C5r: 100 ms fp32 IQ @ 100 MS/s, F=4096 rect hop 4096 (T=2441), "
+                                      "default DetectorConfig"),
+    "hann": Workload("hann", N_FFT // 2, 1, "C5h: 100 ms fp32 IQ @ 100 MS/s, F=4096 periodic Hann hop 2048 "
+                                            "(T=4881, STFT extension), default DetectorConfig"),
+}
 METRIC = "spectrum-occupancy frames/s (config 5: 100 ms fp32 IQ capture @ 100 MS/s -> 2441x4096 TF plot -> boxes)"
 
 
@@ -102,60 +129,95 @@ def _dist():
     return ws, rank, local
 
 
-def cpu_reference(n_captures_total: int, threads: int, seconds_budget: float, seed: int = 2603):
-    """The reference's CPU path (oracle/_ref: the unmodified reference sources +
-    the FFTW-API shim) on host cores: make_plot + detect per capture, one
-    capture per std::thread at a time, all `threads` threads."""
-    sys.path.insert(0, str(ROOT / "tests"))
-    import numpy as np
+def _cpu_caps(wl, k=4):
     import torch
 
     from paper_2603_20481_b200 import signals
-    from _oracle import ref
-
-    R = ref()
-    # a few distinct captures, cycled (MemorySource-style)
     dev = "cuda" if torch.cuda.is_available() else "cpu"
-    caps = [signals.synthesize_torch(signals.c5_scenario(i), device=dev)[:SAMPLES].cpu().numpy()
-            for i in range(4)]
-    iq = np.concatenate(caps)
-    # calibrate: one capture per thread
-    t0 = time.perf_counter()
-    R.bench_detect(iq, FS, N_FFT, ROWS, threads, threads)
-    one_round = time.perf_counter() - t0
-    rounds = max(1, int(seconds_budget / max(one_round, 1e-3)))
-    n = min(n_captures_total, rounds * threads) if n_captures_total else rounds * threads
-    boxes, secs = R.bench_detect(iq, FS, N_FFT, ROWS, n, threads)
-    return n / secs, n, secs, boxes
+    return [signals.synthesize_torch(signals.c5_scenario(i), device=dev)[:wl.samples(1)].cpu().numpy()
+            for i in range(k)]
+
+
+def cpu_reference(wl, threads: int, seconds_budget: float):
+    """The reference's CPU path on host cores, `threads` threads.
+
+    c5r: oracle/_ref (the unmodified reference sources + the FFTW-API shim):
+    make_plot + detect per capture, one capture per std::thread at a time
+    (kind "reference").  hann: the reference has no windowed/overlapped
+    frontend, so the oracle restatement (oracle_stft_plot + oracle_detect,
+    ctypes calls release the GIL) runs one plot per thread (kind "port")."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import numpy as np
+
+    from _oracle import ora, ref
+
+    caps = _cpu_caps(wl)
+    if wl.name == "c5r":
+        R = ref()
+        iq = np.concatenate(caps)
+        t0 = time.perf_counter()
+        R.bench_detect(iq, FS, N_FFT, wl.rows, threads, threads)       # calibrate: one capture per thread
+        one_round = time.perf_counter() - t0
+        n = max(1, int(seconds_budget / max(one_round, 1e-3))) * threads
+        _, secs = R.bench_detect(iq, FS, N_FFT, wl.rows, n, threads)
+        return n / secs, n, secs, "reference"
+    from concurrent.futures import ThreadPoolExecutor
+    O = ora()
+
+    def one(i):
+        tf = O.stft_plot(caps[i % len(caps)], N_FFT, wl.hop, wl.window, wl.rows)
+        O.detect(tf, start_seq=0, fs=FS)
+
+    with ThreadPoolExecutor(threads) as pool:
+        t0 = time.perf_counter()
+        list(pool.map(one, range(threads)))
+        one_round = time.perf_counter() - t0
+        n = max(1, int(seconds_budget / max(one_round, 1e-3))) * threads
+        t0 = time.perf_counter()
+        list(pool.map(one, range(n)))
+        secs = time.perf_counter() - t0
+    return n / secs, n, secs, "port"
+
+
+def _cpu_sample(wl, n, secs):
+    if wl.name == "c5r":
+        return (f"{n} C5r captures (make_plot + detect each, one capture per thread) in {secs:.1f} s; "
+                "reference sources + builder FFTW-API shim (FFTW absent)")
+    return (f"{n} C5h plots (oracle_stft_plot + oracle_detect each, one plot per thread) in {secs:.1f} s; "
+            "oracle restatement (the reference has no Hann/overlap frontend)")
 
 
 def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return
+    wl = WORKLOADS[args.mode]
     threads = os.cpu_count() or 1
-    vals = []
-    total_caps, total_s = 0, 0.0
+    total_caps, total_s, kind = 0, 0.0, "reference"
     for i in range(args.warmup + args.steps):
-        v, n, secs, _ = cpu_reference(0, threads, args.ref_step_seconds)
+        v, n, secs, kind = cpu_reference(wl, threads, args.ref_step_seconds)
         if i >= args.warmup:
-            vals.append(v)
             total_caps += n
             total_s += secs
     value = total_caps / total_s
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": _metric(wl), "value": value, "unit": "frames/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded config-5 bursts)",
-        "config": {"workload": "C5r: 100 ms fp32 IQ @ 100 MS/s, F=4096 rect hop 4096, T=2441",
-                   "captures_per_step": total_caps // max(args.steps, 1)},
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "reference",
-                         "sample": f"{total_caps} captures over {args.steps} steps, make_plot+detect per capture "
-                                   f"(reference sources + FFTW-API shim; FFTW absent)"},
+        "config": {"workload": wl.desc, "captures_per_step": total_caps // max(args.steps, 1)},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": kind,
+                         "sample": f"over {args.steps} steps: " + _cpu_sample(wl, total_caps, total_s)},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
+
+
+def _metric(wl):
+    if wl.name == "c5r":
+        return METRIC
+    return ("spectrum-occupancy frames/s (config 5 as written: 100 ms fp32 IQ @ 100 MS/s -> "
+            "4881x4096 Hann/50% TF plot -> boxes)")
 
 
 def run_ours(args):
@@ -173,18 +235,19 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     lib = ctx.lib
+    wl = WORKLOADS[args.mode]
     B = args.batch
     K = args.box_capacity
 
     # ---- inputs: D distinct seeded captures, tiled to B captures, resident in HBM
     D = min(args.distinct, B)
-    caps = [signals.synthesize_torch(signals.c5_scenario(1000 * rank + i), device="cuda")[:SAMPLES]
+    caps = [signals.synthesize_torch(signals.c5_scenario(1000 * rank + i), device="cuda")[:wl.stride]
             for i in range(D)]
-    iq = torch.empty(B * SAMPLES, dtype=torch.complex64, device="cuda")
+    iq = torch.zeros(wl.samples(B), dtype=torch.complex64, device="cuda")
     for b in range(B):
-        iq[b * SAMPLES:(b + 1) * SAMPLES] = caps[b % D]
+        iq[b * wl.stride:(b + 1) * wl.stride] = caps[b % D]
     del caps
-    tf = torch.empty(B * SAMPLES, dtype=torch.float32, device="cuda")
+    tf = torch.empty(B * wl.rows * N_FFT, dtype=torch.float32, device="cuda")
     outs = dict(
         psd_raw=torch.empty((B, N_FFT), dtype=torch.float32, device="cuda"),
         psd_smoothed=torch.empty((B, N_FFT), dtype=torch.float32, device="cuda"),
@@ -202,10 +265,16 @@ def run_ours(args):
         gathered = torch.empty((ws, B, K, 4), dtype=torch.float64, device="cuda")
         gathered_n = torch.empty((ws, B), dtype=torch.int32, device="cuda")
 
+    def sense(src_ptr, nb, tf_ptr, out):
+        if wl.name == "c5r":    # the reference-parity entry point
+            return lib.ss_sense_batch(ctx.h, C.c_void_p(src_ptr), NAT.SS_FMT_F32, N_FFT, wl.rows, nb,
+                                      C.c_uint64(0), C.c_double(FS), C.byref(cfg), tf_ptr, C.byref(out))
+        return lib.ss_stft_sense_batch(ctx.h, C.c_void_p(src_ptr), NAT.SS_FMT_F32, N_FFT, wl.hop, wl.window,
+                                       wl.rows, nb, C.c_uint64(0), C.c_double(FS), C.byref(cfg), tf_ptr,
+                                       C.byref(out))
+
     def step(src_ptr, out):
-        ctx.check(lib.ss_sense_batch(ctx.h, C.c_void_p(src_ptr), NAT.SS_FMT_F32, N_FFT, ROWS, B,
-                                     C.c_uint64(0), C.c_double(FS), C.byref(cfg), C.c_void_p(tf.data_ptr()),
-                                     C.byref(out)))
+        ctx.check(sense(src_ptr, B, C.c_void_p(tf.data_ptr()), out))
         if ws > 1:
             dist.all_gather_into_tensor(gathered_n, outs["n_boxes"])
             dist.all_gather_into_tensor(gathered, outs["boxes"])
@@ -244,17 +313,17 @@ def run_ours(args):
     stage_ms = {n: st[i] / args.steps for i, n in enumerate(stage_names) if st[i] > 0}
     k1_ms = stage_ms.get("k1_fft_mag_psd", float("nan"))
     hbm_peak, peak_kind = _peaks()
-    achieved = B * ALG_BYTES / (k1_ms / 1e3) / 1e9
+    achieved = B * wl.alg_bytes / (k1_ms / 1e3) / 1e9
     traffic = None
     tp = ROOT / "profiles" / "k1_traffic.json"
     if tp.exists():
-        traffic = json.loads(tp.read_text()).get("bytes_per_capture")
+        traffic = json.loads(tp.read_text()).get(wl.name, {}).get("bytes_per_capture")
         traffic = traffic * B if traffic else None
 
     # ---- e2e: host (pinned) IQ in, host boxes out, through the same C-ABI call
     Be = max(1, min(B, args.e2e_batch))
-    host_iq = torch.empty(Be * SAMPLES, dtype=torch.complex64, pin_memory=True)
-    host_iq.copy_(iq[: Be * SAMPLES])
+    host_iq = torch.empty(wl.samples(Be), dtype=torch.complex64, pin_memory=True)
+    host_iq.copy_(iq[: wl.samples(Be)])
     host_out = {k: torch.empty((Be,) + tuple(v.shape[1:]), dtype=v.dtype, pin_memory=True) for k, v in outs.items()}
     hout = NAT.BatchOut(*(C.c_void_p(v.data_ptr()) for v in host_out.values()), K)
 
@@ -262,8 +331,7 @@ def run_ours(args):
         Be = 0
 
     def e2e_step():
-        ctx.check(lib.ss_sense_batch(ctx.h, C.c_void_p(host_iq.data_ptr()), NAT.SS_FMT_F32, N_FFT, ROWS, Be,
-                                     C.c_uint64(0), C.c_double(FS), C.byref(cfg), None, C.byref(hout)))
+        ctx.check(sense(host_iq.data_ptr(), Be, None, hout))
 
     for _ in range(max(1, args.warmup // 2) if Be else 0):
         e2e_step()
@@ -293,29 +361,27 @@ def run_ours(args):
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        v, n, secs, _ = cpu_reference(0, threads, args.cpu_seconds)
-        cpu = {"value": v, "unit": "frames/s", "cores": threads, "kind": "reference",
-               "sample": f"{n} C5r captures (make_plot + detect each, one capture per thread) in {secs:.1f} s; "
-                         "reference sources + builder FFTW-API shim (FFTW absent)"}
+        v, n, secs, kind = cpu_reference(wl, threads, args.cpu_seconds)
+        cpu = {"value": v, "unit": "frames/s", "cores": threads, "kind": kind, "sample": _cpu_sample(wl, n, secs)}
 
     if rank == 0:
         clocks = clk.summary()
         line = {
-            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
+            "metric": _metric(wl), "value": value, "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * sec_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: seeded config-5 captures (16 rectangular bursts, 5-40 MHz, 0.1-5 ms, 0-20 dB) on unit AWGN",
-            "config": {"workload": "C5r: 100 ms fp32 IQ @ 100 MS/s, F=4096 rect hop 4096 (T=2441), default DetectorConfig",
+            "config": {"workload": wl.desc,
                        "captures_per_step_per_gpu": B, "distinct_captures": D,
-                       "l2": f"inputs > L2 ({B * SAMPLES * 8 / 1e9:.1f} GB IQ per step, no flush needed)",
+                       "l2": f"inputs > L2 ({wl.samples(B) * 8 / 1e9:.1f} GB IQ per step, no flush needed)",
                        "parallelism": f"capture-sharded x{ws}"},
-            "iq_gbps": value * SAMPLES * 32 / 1e9,
+            "iq_gbps": value * wl.stride * 32 / 1e9,
             "stage_ms_per_step": stage_ms,
             "roofline": {"bound": "hbm", "kernel": "k1_fft_mag_psd", "achieved": achieved, "peak": hbm_peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
-                         "alg_bytes_per_capture": ALG_BYTES,
-                         "fp64_tflops": B * ALG_FLOP64 / (k1_ms / 1e3) / 1e12, "fp64_peak_tflops": FP64_PEAK_TFLOPS},
-            "e2e": {"value": e2e_val, "unit": "frames/s", "h2d_bytes_per_step": Be * SAMPLES * 8,
+                         "alg_bytes_per_capture": wl.alg_bytes,
+                         "fp64_tflops": B * wl.alg_flop64 / (k1_ms / 1e3) / 1e12, "fp64_peak_tflops": FP64_PEAK_TFLOPS},
+            "e2e": {"value": e2e_val, "unit": "frames/s", "h2d_bytes_per_step": wl.samples(Be) * 8 if Be else 0,
                     "d2h_bytes_per_step": d2h, "captures_per_step": Be},
             "gpu_launches": launches,
             "clocks": clocks,
@@ -329,6 +395,8 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--mode", default="c5r", choices=sorted(WORKLOADS),
+                    help="c5r: reference-parity rect/hop-N frontend (default); hann: config 5 as written")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -4,6 +4,7 @@
 #include "../../include/specsense_b200.h"
 #include "internal.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -38,6 +39,11 @@ struct ss_ctx {
     std::map<std::pair<int, int>, double*> sg;        // per (window, order)
     std::map<std::pair<int, int>, double*> win;       // STFT window per (n_fft, kind)
     std::map<std::string, DevBuf> ws;                 // grow-only workspace
+    // host-input pipeline: copy stream + per-staging-buffer events
+    cudaStream_t copy = nullptr;
+    cudaEvent_t in_ready[2] = {};
+    cudaEvent_t buf_free[2] = {};
+    int* pinned = nullptr;                             // pinned host word: CCL pool-overflow flag
     int64_t launches = 0;
     // optional per-stage timing (CUDA events on the context stream)
     bool timing = false;
@@ -47,6 +53,12 @@ struct ss_ctx {
 };
 
 namespace {
+
+// host-input staging chunk (two buffers): large enough that per-chunk launch
+// overhead is noise next to the PCIe copy, small enough that pipeline fill is short
+constexpr size_t kStageChunkBytes = size_t(256) << 20;
+// fused-PSD K1 needs this fraction of its last wave of plot slots filled
+constexpr double kFusedPsdMinFill = 0.85;
 
 ss_status fail(ss_ctx* c, ss_status s, const std::string& msg) {
     if (c) c->err = msg;
@@ -321,22 +333,17 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
     ctx->launches += 3;
     const long long cap = out_dev.box_capacity > 0 ? out_dev.box_capacity : 0;
     SS_WS(ncomp, int, "det.n_comp", n_plots);
-    int* overflow_h = nullptr;
-    SS_CK(ctx, cudaMallocHost(&overflow_h, sizeof(int)));
+    int* overflow_h = ctx->pinned;
     tmark(ctx, 5, 0);
     s = run_ccl(ctx, m1, n_plots, rows, cols, cfg.min_component_area, default_pool(n_plots, rows, cols),
                 out_dev.n_boxes ? out_dev.n_boxes : ncomp, cap, nullptr,
                 reinterpret_cast<int*>(out_dev.bin_boxes), reinterpret_cast<double*>(out_dev.boxes), seq_dev, fs,
                 nullptr, overflow_h, time_bins);
-    if (s != SS_OK) {
-        cudaFreeHost(overflow_h);
-        return s;
-    }
+    if (s != SS_OK) return s;
     tmark(ctx, 5, 1);
     SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
     tcollect(ctx);
     const int overflow = *overflow_h;
-    cudaFreeHost(overflow_h);
     if (overflow) {
         // rare: some plot had more runs than the shared pool; redo every plot
         // alone with its exact worst-case pool
@@ -389,6 +396,11 @@ ss_status ss_open(int device, ss_ctx** out) {
         return SS_ECUDA;
     }
     c->stream = c->own;
+    if (cudaMallocHost(&c->pinned, 16 * sizeof(int)) != cudaSuccess) {
+        cudaStreamDestroy(c->own);
+        delete c;
+        return SS_ECUDA;
+    }
     *out = c;
     return SS_OK;
 }
@@ -403,7 +415,16 @@ void ss_close(ss_ctx* ctx) {
     for (auto& kv : ctx->ws) cudaFree(kv.second.p);
     for (cudaEvent_t e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->in_ready[b]) cudaEventDestroy(ctx->in_ready[b]);
+        if (ctx->buf_free[b]) cudaEventDestroy(ctx->buf_free[b]);
+    }
+    if (ctx->copy) {
+        cudaStreamSynchronize(ctx->copy);
+        cudaStreamDestroy(ctx->copy);
+    }
     cudaStreamDestroy(ctx->own);
+    cudaFreeHost(ctx->pinned);
     delete ctx;
 }
 
@@ -728,6 +749,96 @@ ss_status ss_stft_sense_batch(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft
     return sense_impl(ctx, iq, fmt, n_fft, hop, window, rows, n_plots, first_frame, sample_rate_hz, cfg, tf_out, out);
 }
 
+__global__ void seq_fill_kernel(unsigned long long* seq, int n, unsigned long long first, int rows) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) seq[p] = first + static_cast<unsigned long long>(p) * rows;
+}
+
+// K1 (+PSD) and the detector chain on device-resident IQ; `tf` and every
+// non-null pointer in `dev` are device memory.  No host synchronisation.
+static ss_status sense_device(ss_ctx* ctx, const void* diq, ss_fmt fmt, int n_fft, int hop, int window, int rows,
+                              int n_plots, uint64_t first_seq, double sample_rate_hz, const ss_detector_cfg& cfg,
+                              float* tf, const ss_batch_out& dev) {
+    const bool stft = hop != n_fft || window != SS_WIN_RECT;
+    const int cols = n_fft;
+    SS_WS(psd, float, "det.psd", static_cast<size_t>(n_plots) * cols);
+    float* praw = dev.psd_raw ? dev.psd_raw : psd;
+    const double2* tw = nullptr;
+    ss_status s = twiddles(ctx, n_fft, &tw);
+    if (s != SS_OK) return s;
+    // Fused PSD (K1 accumulates each plot's column sums in row order, one plot
+    // per row group) only when the batch fills whole waves of plot slots;
+    // otherwise K1 spreads all rows over every SM and K2 sums the columns.
+    const int slots = ssb::fft_psd_slots_per_sm(ilog2(n_fft), fmt, stft) * ctx->num_sms;
+    bool fused = false;
+    if (slots > 0) {
+        const long long waves = (n_plots + slots - 1) / slots;
+        fused = static_cast<double>(n_plots) >= kFusedPsdMinFill * static_cast<double>(waves * slots);
+    }
+    ssb::FftLaunch L;
+    L.logn = ilog2(n_fft);
+    L.fmt = fmt;
+    L.psd = fused;
+    L.iq = diq;
+    L.tf = tf;
+    L.psd_out = praw;
+    L.tw = tw;
+    L.total_rows = static_cast<long long>(rows) * n_plots;
+    L.rows_per_plot = rows;
+    L.n_plots = n_plots;
+    L.num_sms = ctx->num_sms;
+    if (stft) {
+        const double* w = nullptr;
+        s = window_table(ctx, n_fft, window, &w);
+        if (s != SS_OK) return s;
+        L.hop = hop;
+        L.win = w;
+    }
+    tmark(ctx, 0, 0);
+    SS_CK(ctx, ssb::fft_mag_launch(L, ctx->stream));
+    tmark(ctx, 0, 1);
+    ctx->launches += 1;
+    if (!fused) {
+        tmark(ctx, 1, 0);
+        SS_CK(ctx, ssb::psd_cols_launch(tf, n_plots, rows, cols, 0, cols, praw, ctx->stream));
+        tmark(ctx, 1, 1);
+        ctx->launches += 1;
+    }
+    SS_WS(seq, unsigned long long, "det.seq", n_plots);
+    seq_fill_kernel<<<(n_plots + 255) / 256, 256, 0, ctx->stream>>>(seq, n_plots, first_seq, rows);
+    SS_CK(ctx, cudaGetLastError());
+    ctx->launches += 1;
+    return detect_device(ctx, tf, n_plots, rows, cols, seq, sample_rate_hz, cfg, praw, true, dev, hop);
+}
+
+// outputs of plots [p0, p0 + n) inside a batch-out block of box capacity K
+static ss_batch_out out_slice(const ss_batch_out& o, int p0, int cols, long long K) {
+    ss_batch_out r = o;
+    const size_t p = static_cast<size_t>(p0);
+    if (r.psd_raw) r.psd_raw += p * cols;
+    if (r.psd_smoothed) r.psd_smoothed += p * cols;
+    if (r.floor_thr) r.floor_thr += p * 2;
+    if (r.active) r.active += p * cols;
+    if (r.n_active) r.n_active += p;
+    if (r.boxes) r.boxes += p * static_cast<size_t>(K);
+    if (r.bin_boxes) r.bin_boxes += p * static_cast<size_t>(K);
+    if (r.n_boxes) r.n_boxes += p;
+    return r;
+}
+
+// Host (or unaligned) IQ: chunks of plots are copied into two staging buffers
+// on a private copy stream while the previous chunk computes on ctx->stream,
+// so the PCIe transfer (the e2e bound) overlaps K1..K6.
+static ss_status ensure_copy_stream(ss_ctx* ctx) {
+    if (ctx->copy) return SS_OK;
+    SS_CK(ctx, cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+        SS_CK(ctx, cudaEventCreateWithFlags(&ctx->in_ready[b], cudaEventDisableTiming));
+        SS_CK(ctx, cudaEventCreateWithFlags(&ctx->buf_free[b], cudaEventDisableTiming));
+    }
+    return SS_OK;
+}
+
 static ss_status sense_impl(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int hop, int window, int rows,
                             int n_plots, uint64_t first_seq, double sample_rate_hz, const ss_detector_cfg* cfg,
                             float* tf_out, const ss_batch_out* out) {
@@ -743,20 +854,10 @@ static ss_status sense_impl(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, 
     s = check_stft(ctx, n_fft, hop, window, fmt);
     if (s != SS_OK) return s;
     if (n_plots <= 0) return SS_OK;
-    const bool stft = hop != n_fft || window != SS_WIN_RECT;
-    const size_t frames = static_cast<size_t>(n_plots) * rows;
-    const size_t nsamp = (frames - 1) * static_cast<size_t>(hop) + static_cast<size_t>(n_fft);  // input span
-    const size_t ntf = frames * static_cast<size_t>(n_fft);
-    const size_t sbytes = fmt == SS_FMT_F32 ? 8 : 4;
-    const void* diq = iq;
-    if (!is_device_ptr(iq) || reinterpret_cast<uintptr_t>(iq) % 16 != 0) {
-        SS_WS(stage, unsigned char, "sense.iq", nsamp * sbytes);
-        tmark(ctx, 6, 0);
-        SS_CK(ctx, cudaMemcpyAsync(stage, iq, nsamp * sbytes, cudaMemcpyDefault, ctx->stream));
-        tmark(ctx, 6, 1);
-        diq = stage;
-    }
     const int cols = n_fft;
+    const size_t sbytes = fmt == SS_FMT_F32 ? 8 : 4;
+    const size_t plot_stride = static_cast<size_t>(rows) * hop;      // samples between plot starts
+    const size_t ntf = static_cast<size_t>(n_plots) * rows * cols;
     float* tf = tf_out;
     if (!tf) {
         SS_WS(t, float, "sense.tf", ntf);
@@ -790,41 +891,59 @@ static ss_status sense_impl(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, 
         dev.bin_boxes = a7;
         dev.n_boxes = a8;
     }
-    SS_WS(psd, float, "det.psd", static_cast<size_t>(n_plots) * cols);
-    float* praw = dev.psd_raw ? dev.psd_raw : psd;
-    const double2* tw = nullptr;
-    s = twiddles(ctx, n_fft, &tw);
-    if (s != SS_OK) return s;
-    ssb::FftLaunch L;
-    L.logn = ilog2(n_fft);
-    L.fmt = fmt;
-    L.psd = true;
-    L.iq = diq;
-    L.tf = tf;
-    L.psd_out = praw;
-    L.tw = tw;
-    L.total_rows = static_cast<long long>(rows) * n_plots;
-    L.rows_per_plot = rows;
-    L.n_plots = n_plots;
-    L.num_sms = ctx->num_sms;
-    if (stft) {
-        const double* w = nullptr;
-        s = window_table(ctx, n_fft, window, &w);
+    if (is_device_ptr(iq) && reinterpret_cast<uintptr_t>(iq) % 16 == 0) {
+        s = sense_device(ctx, iq, fmt, n_fft, hop, window, rows, n_plots, first_seq, sample_rate_hz, *cfg, tf, dev);
         if (s != SS_OK) return s;
-        L.hop = hop;
-        L.win = w;
+    } else {
+        s = ensure_copy_stream(ctx);
+        if (s != SS_OK) return s;
+        const size_t plot_bytes = plot_stride * sbytes;
+        const int cp = static_cast<int>(std::max<size_t>(1, std::min<size_t>(n_plots, kStageChunkBytes / plot_bytes)));
+        const size_t chunk_span = (static_cast<size_t>(cp) * rows - 1) * hop + n_fft;
+        unsigned char* stage[2];
+        {
+            SS_WS(s0, unsigned char, "sense.iq0", chunk_span * sbytes);
+            stage[0] = s0;
+        }
+        if (cp < n_plots) {
+            SS_WS(s1, unsigned char, "sense.iq1", chunk_span * sbytes);
+            stage[1] = s1;
+        } else {
+            stage[1] = stage[0];
+        }
+        const int nchunks = (n_plots + cp - 1) / cp;
+        // chunk c -> staging buffer c & 1; the copy of chunk c + 1 is queued
+        // before chunk c computes, so the copy engine never idles on the
+        // host's per-chunk synchronisation inside detect_device
+        auto issue_copy = [&](int c) -> ss_status {
+            const int b = c & 1;
+            const int p0 = c * cp;
+            const int np = std::min(cp, n_plots - p0);
+            const size_t span = (static_cast<size_t>(np) * rows - 1) * hop + n_fft;
+            const unsigned char* src = static_cast<const unsigned char*>(iq) + p0 * plot_stride * sbytes;
+            SS_CK(ctx, cudaStreamWaitEvent(ctx->copy, ctx->buf_free[b], 0));
+            SS_CK(ctx, cudaMemcpyAsync(stage[b], src, span * sbytes, cudaMemcpyDefault, ctx->copy));
+            SS_CK(ctx, cudaEventRecord(ctx->in_ready[b], ctx->copy));
+            return SS_OK;
+        };
+        s = issue_copy(0);
+        if (s != SS_OK) return s;
+        for (int c = 0; c < nchunks; ++c) {
+            const int b = c & 1;
+            const int p0 = c * cp;
+            const int np = std::min(cp, n_plots - p0);
+            if (c + 1 < nchunks) {
+                s = issue_copy(c + 1);
+                if (s != SS_OK) return s;
+            }
+            SS_CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->in_ready[b], 0));
+            s = sense_device(ctx, stage[b], fmt, n_fft, hop, window, rows, np, first_seq + p0 * static_cast<uint64_t>(rows),
+                             sample_rate_hz, *cfg, tf + static_cast<size_t>(p0) * rows * cols,
+                             out_slice(dev, p0, cols, K));
+            if (s != SS_OK) return s;
+            SS_CK(ctx, cudaEventRecord(ctx->buf_free[b], ctx->stream));
+        }
     }
-    tmark(ctx, 0, 0);
-    SS_CK(ctx, ssb::fft_mag_launch(L, ctx->stream));
-    tmark(ctx, 0, 1);
-    ctx->launches += 1;
-    SS_WS(seq, unsigned long long, "det.seq", n_plots);
-    std::vector<unsigned long long> hseq(static_cast<size_t>(n_plots));
-    for (int p = 0; p < n_plots; ++p) hseq[p] = first_seq + static_cast<unsigned long long>(p) * rows;
-    SS_CK(ctx, cudaMemcpyAsync(seq, hseq.data(), sizeof(unsigned long long) * n_plots, cudaMemcpyHostToDevice,
-                               ctx->stream));
-    s = detect_device(ctx, tf, n_plots, rows, cols, seq, sample_rate_hz, *cfg, praw, true, dev, hop);
-    if (s != SS_OK) return s;
     if (host_out) {
         tmark(ctx, 7, 0);
         auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
@@ -840,14 +959,17 @@ static ss_status sense_impl(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, 
         SS_CK(ctx, cp(out->bin_boxes, dev.bin_boxes, sizeof(ss_bin_box) * n_plots * K));
         SS_CK(ctx, cp(out->n_boxes, dev.n_boxes, sizeof(int32_t) * n_plots));
         tmark(ctx, 7, 1);
-        SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
-        tcollect(ctx);
     }
     if (out->n_boxes) {
         std::vector<int> nb(static_cast<size_t>(n_plots));
-        SS_CK(ctx, cudaMemcpy(nb.data(), out->n_boxes, sizeof(int) * n_plots, cudaMemcpyDefault));
+        SS_CK(ctx, cudaMemcpyAsync(nb.data(), dev.n_boxes, sizeof(int) * n_plots, cudaMemcpyDeviceToHost, ctx->stream));
+        SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
+        tcollect(ctx);
         for (int v : nb)
             if (v > K) return fail(ctx, SS_ECAPACITY, "box capacity too small: " + std::to_string(v));
+    } else if (host_out) {
+        SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
+        tcollect(ctx);
     }
     return SS_OK;
 }

@@ -573,18 +573,38 @@ static void build_tw(std::vector<double2>& out) {
 }
 
 template <int LOGN, int FMT, bool PSD, bool WIN>
+static cudaError_t ensure_smem_attr() {
+    static bool attr_done = false;  // per instantiation
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(fft_mag_kernel<LOGN, FMT, PSD, WIN>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(K1Shape<LOGN>::smem(FMT == 0 ? 8 : 4)));
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    return cudaSuccess;
+}
+
+// plots the fused-PSD grid processes concurrently per SM (one plot per row group)
+template <int LOGN, int FMT, bool WIN>
+static int psd_slots_one() {
+    if (ensure_smem_attr<LOGN, FMT, true, WIN>() != cudaSuccess) return 0;
+    int blocks = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fft_mag_kernel<LOGN, FMT, true, WIN>,
+                                                      K1Shape<LOGN>::THREADS,
+                                                      K1Shape<LOGN>::smem(FMT == 0 ? 8 : 4)) != cudaSuccess)
+        return 0;
+    return blocks * K1Shape<LOGN>::GROUPS;
+}
+
+template <int LOGN, int FMT, bool PSD, bool WIN>
 static cudaError_t launch_one(const FftLaunch& L, cudaStream_t st) {
     using PL = FftPlan<LOGN>;
     using KS = K1Shape<LOGN>;
     auto kern = fft_mag_kernel<LOGN, FMT, PSD, WIN>;
     const size_t smem = KS::smem(FMT == 0 ? 8 : 4);
-    static bool attr_done = false;  // per instantiation
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        attr_done = true;
-    }
+    cudaError_t e = ensure_smem_attr<LOGN, FMT, PSD, WIN>();
+    if (e != cudaSuccess) return e;
     FftArgs a;
     a.iq = L.iq;
     a.tf = L.tf;
@@ -645,6 +665,29 @@ cudaError_t fft_mag_launch(const FftLaunch& L, cudaStream_t st) {
     case 12: return dispatch_fmt<12>(L, st);
     case 13: return dispatch_fmt<13>(L, st);
     default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int LOGN>
+static int psd_slots_fmt(int fmt, bool win) {
+    if (win) return fmt == 0 ? psd_slots_one<LOGN, 0, true>() : psd_slots_one<LOGN, 1, true>();
+    return fmt == 0 ? psd_slots_one<LOGN, 0, false>() : psd_slots_one<LOGN, 1, false>();
+}
+
+int fft_psd_slots_per_sm(int logn, int fmt, bool win) {
+    switch (logn) {
+    case 3: return psd_slots_fmt<3>(fmt, win);
+    case 4: return psd_slots_fmt<4>(fmt, win);
+    case 5: return psd_slots_fmt<5>(fmt, win);
+    case 6: return psd_slots_fmt<6>(fmt, win);
+    case 7: return psd_slots_fmt<7>(fmt, win);
+    case 8: return psd_slots_fmt<8>(fmt, win);
+    case 9: return psd_slots_fmt<9>(fmt, win);
+    case 10: return psd_slots_fmt<10>(fmt, win);
+    case 11: return psd_slots_fmt<11>(fmt, win);
+    case 12: return psd_slots_fmt<12>(fmt, win);
+    case 13: return psd_slots_fmt<13>(fmt, win);
+    default: return 0;
     }
 }
 

@@ -25,6 +25,8 @@ struct FftLaunch {
     const double* win = nullptr; // STFT extension: device window weights (null = rectangular)
 };
 cudaError_t fft_mag_launch(const FftLaunch& L, cudaStream_t st);
+// plots per SM the fused-PSD K1 grid runs concurrently (one plot per row group)
+int fft_psd_slots_per_sm(int logn, int fmt, bool win);
 void fft_window(int n_fft, int kind, std::vector<double>& out);  // kind 0 rect, 1 periodic Hann
 void fft_twiddles(int logn, std::vector<double2>& out);
 

@@ -156,3 +156,42 @@ def test_stft_hann_detect(ss, ref, ora):
         assert np.array_equal(det.boxes[:, 0], (bb[:, 2] - n_fft // 2) * df)
         assert np.array_equal(det.boxes[:, 2], (p * rows + bb[:, 0]) * dt)
         assert np.array_equal(det.boxes[:, 3], (p * rows + bb[:, 1]) * dt)
+
+
+def _host_sense(ss, src, n_fft, hop, window, rows, P, fs, K=2048):
+    """ss_(stft_)sense_batch with HOST input and HOST outputs: the chunked
+    copy-stream pipeline (capi.cu sense_impl) instead of the device-resident path."""
+    import ctypes as C
+    from paper_2603_20481_b200 import _native as NAT
+    ctx = ss.Context.get(0)
+    o = dict(raw=np.empty((P, n_fft), np.float32), sm=np.empty((P, n_fft), np.float32),
+             ft=np.empty((P, 2), np.float32), act=np.empty((P, n_fft), np.int32), nact=np.empty(P, np.int32),
+             boxes=np.empty((P, K, 4), np.float64), bins=np.empty((P, K, 4), np.int32), nb=np.empty(P, np.int32))
+    bout = NAT.BatchOut(*(C.c_void_p(v.ctypes.data) for v in o.values()), K)
+    cfg = ss.DetectorConfig().c()
+    src = np.ascontiguousarray(src)
+    ctx.check(ctx.lib.ss_stft_sense_batch(ctx.h, C.c_void_p(src.ctypes.data), NAT.SS_FMT_F32, n_fft, hop, window,
+                                          rows, P, C.c_uint64(0), C.c_double(fs), C.byref(cfg), None, C.byref(bout)))
+    return o
+
+
+@pytest.mark.parametrize("hop,window,rows", [(4096, 0, 2441), (2048, 1, 4881)])
+def test_host_input_pipeline_matches_device(ss, hop, window, rows):
+    """4 x 80 MB plots from host memory -> 2 staging chunks (3 + 1 plots, the STFT
+    chunks overlapping by n_fft - hop samples) == the device-resident result."""
+    import torch
+    n_fft, P, fs = 4096, 4, 100e6
+    n = P * rows * hop + n_fft - hop
+    iq = np.concatenate([signals.synthesize_torch(signals.c5_scenario(40 + i), device="cuda").cpu().numpy()
+                         for i in range((n + 9_999_999) // 10_000_000)])[:n]
+    got = _host_sense(ss, iq, n_fft, hop, window, rows, P, fs)
+    dets = ss.sense(iq, fs, n_fft, rows, hop=hop, window=window, box_capacity=2048)
+    assert len(dets) == P
+    for p, d in enumerate(dets):
+        k = int(got["nb"][p])
+        assert k == len(d.boxes)
+        assert np.array_equal(got["raw"][p], d.psd.raw) and np.array_equal(got["sm"][p], d.psd.smoothed)
+        assert np.array_equal(got["act"][p][: got["nact"][p]], d.active_columns)
+        assert np.array_equal(got["bins"][p][:k], d.bin_boxes)
+        assert np.array_equal(got["boxes"][p][:k], d.boxes)
+    torch.cuda.synchronize()
