@@ -194,6 +194,70 @@ ss_status ss_stft_sense_batch(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft
                               int n_plots, uint64_t first_frame, double sample_rate_hz,
                               const ss_detector_cfg* cfg, float* tf_out, const ss_batch_out* out);
 
+/* ---- streaming engine ---------------------------------------------------
+   GPU form of the reference's real-time engine (runtime::run,
+   proj/src/runtime.cpp:221-487, with frontend::PingPongBuffer,
+   proj/include/specsense/frontend.hpp:86-135): F-sample chunks with a
+   sequence number stream into HBM banks; window w = seq / T fills bank
+   w % n_banks; when its T rows are in, the whole window runs K1..K6 on the
+   engine's stream and its boxes land in pinned host memory.  A bank stays
+   held until its record is polled (the reference releases after the
+   detection handler).  Rows for a window whose bank is still held are
+   dropped and the window is counted as one overrun (paced) or the push
+   blocks until the bank is released (unpaced: back-pressure, no loss).
+   Latency = host time from the push that delivered the window's last row
+   to the moment its boxes are in host memory (the reference: bank complete
+   -> boxes emitted, runtime.cpp:441).  Thread model: one pushing thread,
+   one polling thread. */
+typedef struct ss_engine ss_engine;
+
+typedef struct {
+    int n_fft;             /* F: power of two, 8..8192 */
+    int plot_rows;         /* T */
+    ss_fmt fmt;            /* chunk sample format */
+    double sample_rate_hz;
+    int n_banks;           /* >= 2; 2 = the reference's ping-pong */
+    int paced;             /* 1: shed windows (overruns); 0: push blocks */
+    double deadline_s;     /* <= 0: the plot span T*F/fs */
+    int box_capacity;      /* boxes kept per plot */
+} ss_engine_cfg;
+
+/* runtime::PlotRecord (proj/include/specsense/runtime.hpp:62-69) + extras */
+typedef struct {
+    uint64_t plot_index;   /* window id */
+    uint64_t start_seq;
+    double latency_s;      /* bank complete -> boxes on the host */
+    double deadline_s;
+    int32_t met;           /* latency_s <= deadline_s */
+    int32_t n_boxes;       /* true count (> capacity: only the first capacity returned) */
+    int32_t n_active;
+    float noise_floor;
+    float threshold;
+    double complete_s;     /* engine clock: window complete */
+    double done_s;         /* engine clock: boxes on the host */
+} ss_plot_record;
+
+ss_status ss_engine_open(int device, const ss_engine_cfg* cfg, const ss_detector_cfg* det, ss_engine** out);
+void ss_engine_close(ss_engine* eng);
+const char* ss_engine_last_error(const ss_engine* eng);
+/* n_chunks chunks of n_fft samples (host or device memory, contiguous),
+   sequence numbers first_seq, first_seq + 1, ... */
+ss_status ss_engine_push(ss_engine* eng, const void* samples, int64_t n_chunks, uint64_t first_seq);
+/* Chunks [first_seq, last_seq) were lost upstream: their windows drop
+   (frontend::PingPongBuffer::mark_lost_range). */
+ss_status ss_engine_mark_lost(ss_engine* eng, uint64_t first_seq, uint64_t last_seq);
+/* End of stream: an incomplete last window is discarded. */
+ss_status ss_engine_finish(ss_engine* eng);
+/* Next completed window in completion (= window) order.  wait_ms < 0 waits
+   until a record is ready or the stream is finished and drained; *got = 1
+   when rec/boxes/bin_boxes (each may be NULL, capacity cap) were filled. */
+ss_status ss_engine_poll(ss_engine* eng, int wait_ms, ss_plot_record* rec, ss_box* boxes, ss_bin_box* bin_boxes,
+                         int cap, int* got);
+/* windows completed (handed to the GPU), windows dropped (overruns), rows
+   retired (used + dropped + lost), windows in flight or awaiting poll */
+ss_status ss_engine_stats(ss_engine* eng, uint64_t* completed, uint64_t* overruns, uint64_t* rows_retired,
+                          uint64_t* pending);
+
 /* ---- test hooks -------------------------------------------------------- */
 /* Device ports of glibc log10f (which=0) / powf(10, x) (which=1) over n
    DEVICE floats; variant: 1 FMA build, 0 SSE2 build, -1 host-matched. */

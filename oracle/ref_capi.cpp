@@ -375,4 +375,79 @@ long long ref_run_engine(const float* iq, long long n_samples, double fs, int n_
     });
 }
 
+
+// runtime::summarize (runtime.cpp:166-199) on scripted records: stats =
+// {plots, overruns, deadline, fraction_met, realtime_met, p50, p90, p99, max,
+// percentiles_valid}; ccdf points (latency, fraction) into ccdf[2*i..]
+// (capacity cap points).  Returns the ccdf point count.
+long long ref_summarize(long long n, const unsigned long long* plot_index, const double* latency, const int* met,
+                        unsigned long long overruns, double deadline, double* stats, double* ccdf, long long cap) {
+    return guard([&]() -> long long {
+        std::vector<runtime::PlotRecord> recs(static_cast<std::size_t>(n));
+        for (long long i = 0; i < n; ++i) {
+            recs[i].plot_index = plot_index[i];
+            recs[i].latency_s = latency[i];
+            recs[i].met = met[i] != 0;
+            recs[i].deadline_s = deadline;
+        }
+        const auto rep = runtime::summarize(std::move(recs), overruns, deadline);
+        stats[0] = static_cast<double>(rep.plots);
+        stats[1] = static_cast<double>(rep.overruns);
+        stats[2] = rep.deadline_s;
+        stats[3] = rep.fraction_met;
+        stats[4] = rep.realtime_met ? 1.0 : 0.0;
+        stats[5] = rep.p50_s;
+        stats[6] = rep.p90_s;
+        stats[7] = rep.p99_s;
+        stats[8] = rep.max_s;
+        stats[9] = rep.percentiles_valid ? 1.0 : 0.0;
+        const auto pts = rep.ccdf();
+        if (static_cast<long long>(pts.size()) > cap) return -7;
+        for (std::size_t i = 0; i < pts.size(); ++i) {
+            ccdf[2 * i] = pts[i].first;
+            ccdf[2 * i + 1] = pts[i].second;
+        }
+        return static_cast<long long>(pts.size());
+    });
+}
+
+// runtime::run over an unpaced MemorySource of n_plots windows (cycling the
+// samples), collecting every window's boxes: out_plot[i] = plot_index of box
+// i, out_boxes[4*i..] = (f0, f1, t0, t1).  Returns the box count.
+long long ref_run_engine_boxes(const float* iq, long long n_samples, double fs, int n_fft, int rows, long long n_plots,
+                               int n_compute, int n_sensing, unsigned long long* out_plot, double* out_boxes,
+                               long long cap, unsigned long long* plots_seen) {
+    return guard([&]() -> long long {
+        frontend::FrontendConfig fc;
+        fc.sample_rate_hz = fs;
+        fc.n_fft = n_fft;
+        fc.plot_rows = rows;
+        runtime::RuntimeConfig rc;
+        rc.n_compute_workers = n_compute;
+        rc.n_sensing_workers = n_sensing;
+        std::vector<cfloat> samples(reinterpret_cast<const cfloat*>(iq),
+                                    reinterpret_cast<const cfloat*>(iq) + n_samples);
+        frontend::MemorySource src(std::move(samples), n_fft, static_cast<std::uint64_t>(n_plots) * rows);
+        long long nb = 0;
+        bool overflow = false;
+        const auto rep = runtime::run(src, fc, detector::DetectorConfig{}, rc,
+                                      [&](const runtime::PlotRecord& r, std::span<const BoundingBox> b) {
+                                          for (const BoundingBox& x : b) {
+                                              if (nb >= cap) {
+                                                  overflow = true;
+                                                  return;
+                                              }
+                                              out_plot[nb] = r.plot_index;
+                                              out_boxes[4 * nb] = x.f0_hz;
+                                              out_boxes[4 * nb + 1] = x.f1_hz;
+                                              out_boxes[4 * nb + 2] = x.t0_s;
+                                              out_boxes[4 * nb + 3] = x.t1_s;
+                                              ++nb;
+                                          }
+                                      });
+        *plots_seen = rep.plots;
+        return overflow ? -7 : nb;
+    });
+}
+
 } // extern "C"

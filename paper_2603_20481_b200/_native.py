@@ -39,6 +39,18 @@ class BatchOut(C.Structure):
                 ("bin_boxes", C.c_void_p), ("n_boxes", C.c_void_p), ("box_capacity", C.c_int32)]
 
 
+class EngineCfg(C.Structure):
+    _fields_ = [("n_fft", C.c_int), ("plot_rows", C.c_int), ("fmt", C.c_int), ("sample_rate_hz", C.c_double),
+                ("n_banks", C.c_int), ("paced", C.c_int), ("deadline_s", C.c_double), ("box_capacity", C.c_int)]
+
+
+class PlotRecord(C.Structure):
+    _fields_ = [("plot_index", C.c_uint64), ("start_seq", C.c_uint64), ("latency_s", C.c_double),
+                ("deadline_s", C.c_double), ("met", C.c_int32), ("n_boxes", C.c_int32), ("n_active", C.c_int32),
+                ("noise_floor", C.c_float), ("threshold", C.c_float), ("complete_s", C.c_double),
+                ("done_s", C.c_double)]
+
+
 # name -> (restype, argtypes); every symbol include/specsense_b200.h declares
 _P = C.c_void_p
 _I = C.c_int
@@ -72,6 +84,15 @@ SIGNATURES = {
     "ss_test_libm": (_I, [_P, _P, C.c_int64, _I, _I, _P]),
     "ss_fft_twiddle_count": (C.c_int64, [_I]),
     "ss_fft_twiddles": (_I, [_I, _P]),
+    "ss_engine_open": (_I, [_I, C.POINTER(EngineCfg), C.POINTER(DetectorCfg), C.POINTER(_P)]),
+    "ss_engine_close": (None, [_P]),
+    "ss_engine_last_error": (C.c_char_p, [_P]),
+    "ss_engine_push": (_I, [_P, _P, C.c_int64, C.c_uint64]),
+    "ss_engine_mark_lost": (_I, [_P, C.c_uint64, C.c_uint64]),
+    "ss_engine_finish": (_I, [_P]),
+    "ss_engine_poll": (_I, [_P, _I, C.POINTER(PlotRecord), _P, _P, _I, C.POINTER(_I)]),
+    "ss_engine_stats": (_I, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                             C.POINTER(C.c_uint64)]),
 }
 
 _lib = None

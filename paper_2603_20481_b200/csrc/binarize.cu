@@ -22,6 +22,81 @@ constexpr int kBinThreads = 256;
 constexpr int kBinWarps = kBinThreads / 32;
 constexpr int kHistStride = 257;  // padded so column l, bin b hits bank (l + b) % 32
 
+// bin_of (detector.cpp:36-39): trunc(fl(fl(v - lo) * scale)) clamped to 255.
+// y >= 0 here, so trunc = floor, taken as the low mantissa bits of
+// fl_rd(y + 2^23) -- an FP32 add instead of an F2I on the XU pipe.  NaN (only
+// from infinite input, undefined behaviour in the reference) goes to bin 0.
+__device__ __forceinline__ int bin_index(float v, float lo, float scale) {
+    const float y = __fmul_rn(__fsub_rn(v, lo), scale);
+    const int b = __float_as_int(__fadd_rd(y, 8388608.0f)) - 0x4B000000;
+    return y == y ? (b > 255 ? 255 : b) : 0;
+}
+
+// otsu_split (detector.cpp:43-67) for one column, one warp: lane owns bins
+// 8*lane .. 8*lane+7 (hq).  Integer prefix sums, exact double variances,
+// first maximum.  Returns the split index.
+__device__ __forceinline__ int otsu_split_warp(const uint32_t* hq, int lane) {
+    unsigned long long cnt[8], wsum[8];
+    unsigned long long lc = 0, ls = 0;
+    uint32_t nz = 0;  // bins whose count is non-zero (or bin 0)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int bin = lane * 8 + q;
+        lc += hq[q];
+        ls += static_cast<unsigned long long>(bin) * hq[q];
+        cnt[q] = lc;
+        wsum[q] = ls;
+        nz |= (hq[q] != 0u || bin == 0) ? (1u << q) : 0u;
+    }
+    // exclusive prefix over lanes of (lc, ls)
+    unsigned long long pc = lc, ps = ls;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long tc = __shfl_up_sync(0xffffffffu, pc, o);
+        const unsigned long long ts = __shfl_up_sync(0xffffffffu, ps, o);
+        if (lane >= o) {
+            pc += tc;
+            ps += ts;
+        }
+    }
+    const unsigned long long total = __shfl_sync(0xffffffffu, pc, 31);
+    const double sum_all = static_cast<double>(__shfl_sync(0xffffffffu, ps, 31));
+    pc -= lc;
+    ps -= ls;
+    double best_v = -1.0;
+    int best_i = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const unsigned long long w0 = pc + cnt[q];
+        const unsigned long long w1 = total - w0;
+        // an empty bin i > 0 repeats bin i-1's (w0, sum0), hence its variance:
+        // it can never be the first maximum, so skip its divides
+        double var = ((nz >> q) & 1u) ? 0.0 : -1.0;
+        if (((nz >> q) & 1u) && w0 > 0 && w1 > 0) {
+            const double sum0 = static_cast<double>(ps + wsum[q]);
+            const double mu0 = __ddiv_rn(sum0, static_cast<double>(w0));
+            const double mu1 = __ddiv_rn(__dsub_rn(sum_all, sum0), static_cast<double>(w1));
+            const double d = __dsub_rn(mu0, mu1);
+            var = __dmul_rn(__dmul_rn(__dmul_rn(static_cast<double>(w0), static_cast<double>(w1)), d), d);
+        }
+        if (var > best_v) {
+            best_v = var;
+            best_i = lane * 8 + q;
+        }
+    }
+    // first maximum across lanes (ties -> lowest split index)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best_v, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+        if (ov > best_v || (ov == best_v && oi < best_i)) {
+            best_v = ov;
+            best_i = oi;
+        }
+    }
+    return best_i;
+}
+
 __global__ void __launch_bounds__(kBinThreads) binarize_kernel(BinarizeLaunch a) {
     __shared__ uint32_t hist[32 * kHistStride];
     __shared__ float s_lo[kBinWarps][32], s_hi[kBinWarps][32];
@@ -112,18 +187,13 @@ __global__ void __launch_bounds__(kBinThreads) binarize_kernel(BinarizeLaunch a)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 if (use) {
-                    int b = __float2int_rz(__fmul_rn(__fsub_rn(x[q], clo), csc));
-                    b = b > 255 ? 255 : b;
-                    atomicAdd(h + b, 1u);
+                    atomicAdd(h + bin_index(x[q], clo, csc), 1u);
                 }
             }
         }
         for (; r < rows; r += kBinWarps) {
             if (use) {
-                const float x = __ldg(tf + static_cast<long long>(r) * a.cols + col);
-                int b = __float2int_rz(__fmul_rn(__fsub_rn(x, clo), csc));
-                b = b > 255 ? 255 : b;
-                atomicAdd(h + b, 1u);
+                atomicAdd(h + bin_index(__ldg(tf + static_cast<long long>(r) * a.cols + col), clo, csc), 1u);
             }
         }
     }
@@ -132,65 +202,10 @@ __global__ void __launch_bounds__(kBinThreads) binarize_kernel(BinarizeLaunch a)
     // ---- Otsu split: one warp per column, lane owns bins 8*lane .. 8*lane+7
     for (int c = warp; c < 32; c += kBinWarps) {
         if (!c_use[c]) continue;
-        const uint32_t* h = hist + c * kHistStride;
-        unsigned long long cnt[8], wsum[8];
-        unsigned long long lc = 0, ls = 0;
-        uint32_t nz = 0;  // bins whose count is non-zero (or bin 0)
+        uint32_t hq[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int bin = lane * 8 + q;
-            lc += h[bin];
-            ls += static_cast<unsigned long long>(bin) * h[bin];
-            cnt[q] = lc;
-            wsum[q] = ls;
-            nz |= (h[bin] != 0u || bin == 0) ? (1u << q) : 0u;
-        }
-        // exclusive prefix over lanes of (lc, ls)
-        unsigned long long pc = lc, ps = ls;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long tc = __shfl_up_sync(0xffffffffu, pc, o);
-            const unsigned long long ts = __shfl_up_sync(0xffffffffu, ps, o);
-            if (lane >= o) {
-                pc += tc;
-                ps += ts;
-            }
-        }
-        const unsigned long long total = __shfl_sync(0xffffffffu, pc, 31);
-        const double sum_all = static_cast<double>(__shfl_sync(0xffffffffu, ps, 31));
-        pc -= lc;
-        ps -= ls;
-        double best_v = -1.0;
-        int best_i = 0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const unsigned long long w0 = pc + cnt[q];
-            const unsigned long long w1 = total - w0;
-            const double sum0 = static_cast<double>(ps + wsum[q]);
-            // an empty bin i > 0 repeats bin i-1's (w0, sum0), hence its
-            // variance: it can never be the first maximum, so skip its divides
-            double var = ((nz >> q) & 1u) ? 0.0 : -1.0;
-            if (((nz >> q) & 1u) && w0 > 0 && w1 > 0) {
-                const double mu0 = __ddiv_rn(sum0, static_cast<double>(w0));
-                const double mu1 = __ddiv_rn(__dsub_rn(sum_all, sum0), static_cast<double>(w1));
-                const double d = __dsub_rn(mu0, mu1);
-                var = __dmul_rn(__dmul_rn(__dmul_rn(static_cast<double>(w0), static_cast<double>(w1)), d), d);
-            }
-            if (var > best_v) {
-                best_v = var;
-                best_i = lane * 8 + q;
-            }
-        }
-        // first maximum across lanes (ties -> lowest split index)
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, best_v, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
-            if (ov > best_v || (ov == best_v && oi < best_i)) {
-                best_v = ov;
-                best_i = oi;
-            }
-        }
+        for (int q = 0; q < 8; ++q) hq[q] = hist[c * kHistStride + lane * 8 + q];
+        const int best_i = otsu_split_warp(hq, lane);
         if (lane == 0) {
             const double lod = static_cast<double>(c_lo[c]);
             const double e = __ddiv_rn(__dmul_rn(static_cast<double>(best_i) + 1.0, c_span[c]), 256.0);
@@ -351,9 +366,7 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
         const float clo = c_lo[c], csc = c_scale[c];
         uint32_t* h = hist + c * kHistStride;
         for (int r = tid >> 3; r < rows; r += kBinThreads / kTileCols) {
-            int b = __float2int_rz(__fmul_rn(__fsub_rn(bt_vals[r * kTileCols + c], clo), csc));
-            b = b > 255 ? 255 : b;
-            atomicAdd(h + b, 1u);
+            atomicAdd(h + bin_index(bt_vals[r * kTileCols + c], clo, csc), 1u);
         }
     }
     __syncthreads();
@@ -364,62 +377,7 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
         uint32_t hq[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) hq[q] = hist[cc * kHistStride + lane * 8 + q];
-        unsigned long long cnt[8], wsum[8];
-        unsigned long long lc = 0, ls = 0;
-        uint32_t nz = 0;  // bins whose count is non-zero (or bin 0)
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int bin = lane * 8 + q;
-            lc += hq[q];
-            ls += static_cast<unsigned long long>(bin) * hq[q];
-            cnt[q] = lc;
-            wsum[q] = ls;
-            nz |= (hq[q] != 0u || bin == 0) ? (1u << q) : 0u;
-        }
-        unsigned long long pc = lc, ps = ls;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long tc = __shfl_up_sync(0xffffffffu, pc, o);
-            const unsigned long long ts = __shfl_up_sync(0xffffffffu, ps, o);
-            if (lane >= o) {
-                pc += tc;
-                ps += ts;
-            }
-        }
-        const unsigned long long total = __shfl_sync(0xffffffffu, pc, 31);
-        const double sum_all = static_cast<double>(__shfl_sync(0xffffffffu, ps, 31));
-        pc -= lc;
-        ps -= ls;
-        double best_v = -1.0;
-        int best_i = 0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const unsigned long long w0 = pc + cnt[q];
-            const unsigned long long w1 = total - w0;
-            const double sum0 = static_cast<double>(ps + wsum[q]);
-            // an empty bin i > 0 repeats bin i-1's (w0, sum0), hence its
-            // variance: it can never be the first maximum, so skip its divides
-            double var = ((nz >> q) & 1u) ? 0.0 : -1.0;
-            if (((nz >> q) & 1u) && w0 > 0 && w1 > 0) {
-                const double mu0 = __ddiv_rn(sum0, static_cast<double>(w0));
-                const double mu1 = __ddiv_rn(__dsub_rn(sum_all, sum0), static_cast<double>(w1));
-                const double d = __dsub_rn(mu0, mu1);
-                var = __dmul_rn(__dmul_rn(__dmul_rn(static_cast<double>(w0), static_cast<double>(w1)), d), d);
-            }
-            if (var > best_v) {
-                best_v = var;
-                best_i = lane * 8 + q;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, best_v, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
-            if (ov > best_v || (ov == best_v && oi < best_i)) {
-                best_v = ov;
-                best_i = oi;
-            }
-        }
+        const int best_i = otsu_split_warp(hq, lane);
         if (lane == 0) {
             const double lod = static_cast<double>(c_lo[cc]);
             const double e = __ddiv_rn(__dmul_rn(static_cast<double>(best_i) + 1.0, c_span[cc]), 256.0);

@@ -44,6 +44,9 @@ struct ss_ctx {
     cudaEvent_t in_ready[2] = {};
     cudaEvent_t buf_free[2] = {};
     int* pinned = nullptr;                             // pinned host word: CCL pool-overflow flag
+    // streaming engine contexts: size the CCL run pool for the worst case so
+    // detect never synchronises the host to check for a pool overflow
+    bool exact_pool = false;
     int64_t launches = 0;
     // optional per-stage timing (CUDA events on the context stream)
     bool timing = false;
@@ -333,6 +336,14 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
     ctx->launches += 3;
     const long long cap = out_dev.box_capacity > 0 ? out_dev.box_capacity : 0;
     SS_WS(ncomp, int, "det.n_comp", n_plots);
+    if (ctx->exact_pool) {
+        tmark(ctx, 5, 0);
+        s = run_ccl(ctx, m1, n_plots, rows, cols, cfg.min_component_area, worst_pool(rows, cols) * n_plots,
+                    out_dev.n_boxes ? out_dev.n_boxes : ncomp, cap, nullptr, reinterpret_cast<int*>(out_dev.bin_boxes),
+                    reinterpret_cast<double*>(out_dev.boxes), seq_dev, fs, nullptr, nullptr, time_bins);
+        tmark(ctx, 5, 1);
+        return s;
+    }
     int* overflow_h = ctx->pinned;
     tmark(ctx, 5, 0);
     s = run_ccl(ctx, m1, n_plots, rows, cols, cfg.min_component_area, default_pool(n_plots, rows, cols),
@@ -998,3 +1009,32 @@ ss_status ss_fft_twiddles(int n_fft, double* out_re_im) {
 }
 
 } // extern "C"
+
+// ---- hooks for the streaming engine (engine.cpp), not part of the C ABI
+namespace ssb {
+
+ss_status engine_ctx_open(int device, ss_ctx** out) {
+    const ss_status s = ss_open(device, out);
+    if (s == SS_OK) (*out)->exact_pool = true;
+    return s;
+}
+
+cudaStream_t engine_ctx_stream(ss_ctx* ctx) { return ctx->stream; }
+
+ss_status engine_check(ss_ctx* ctx, int n_fft, int rows, ss_fmt fmt, double fs, const ss_detector_cfg& cfg) {
+    if (n_fft < 8 || !is_pow2(n_fft))
+        return fail(ctx, SS_EVALIDATION, "FFT size must be a power of two >= 8, got " + std::to_string(n_fft));
+    if (n_fft > 8192) return fail(ctx, SS_EUNSUPPORTED, "device FFT supports n_fft <= 8192");
+    if (rows < 1) return fail(ctx, SS_EVALIDATION, "plot_rows must be >= 1");
+    if (!(fs > 0.0)) return fail(ctx, SS_EVALIDATION, "sample_rate_hz must be positive");
+    if (fmt != SS_FMT_F32 && fmt != SS_FMT_I16) return fail(ctx, SS_EVALIDATION, "unknown sample format");
+    return check_cfg(ctx, cfg, n_fft);
+}
+
+// one window, device-resident IQ -> device outputs, on the context stream, no host sync
+ss_status engine_sense(ss_ctx* ctx, const void* diq, ss_fmt fmt, int n_fft, int rows, uint64_t start_seq, double fs,
+                       const ss_detector_cfg& cfg, float* tf, const ss_batch_out& dev) {
+    return sense_device(ctx, diq, fmt, n_fft, n_fft, SS_WIN_RECT, rows, 1, start_seq, fs, cfg, tf, dev);
+}
+
+} // namespace ssb

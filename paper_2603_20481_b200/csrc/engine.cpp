@@ -1,0 +1,409 @@
+// engine.cpp -- the streaming engine behind ss_engine_* (include/specsense_b200.h).
+//
+// GPU form of runtime::run's data plane (proj/src/runtime.cpp:221-487) and
+// frontend::PingPongBuffer (proj/include/specsense/frontend.hpp:86-135):
+//
+//   push()  : F-sample chunks -> the HBM bank of their window (w % n_banks),
+//             one async H2D per run of consecutive rows on the copy stream.
+//             The reference FFTs rows as they arrive; here the rows wait in
+//             HBM and the whole window is transformed at once (K1 over T rows
+//             is ~10-100 us), so a window's latency covers its FFT as well.
+//   window complete: an event on the copy stream gates K1..K6 for that window
+//             on the compute stream (its own ss_ctx, exact-pool CCL: no host
+//             synchronisation anywhere on this path), then a D2H of the
+//             boxes into the bank's pinned record and a host callback that
+//             stamps the completion time and queues the bank for poll().
+//   poll()  : hands records out in completion order and releases the bank.
+//
+// Bank rules follow PingPongBuffer: rows of a window whose bank is still held
+// are dropped and the window counts as one overrun (paced sources) or the
+// writer waits for release (unpaced); rows of stale windows are ignored;
+// lost ranges drop their windows.
+#include "specsense_b200.h"
+
+#include <algorithm>
+#include <chrono>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+namespace ssb {
+ss_status engine_ctx_open(int device, ss_ctx** out);
+cudaStream_t engine_ctx_stream(ss_ctx* ctx);
+ss_status engine_check(ss_ctx* ctx, int n_fft, int rows, ss_fmt fmt, double fs, const ss_detector_cfg& cfg);
+ss_status engine_sense(ss_ctx* ctx, const void* diq, ss_fmt fmt, int n_fft, int rows, uint64_t start_seq, double fs,
+                       const ss_detector_cfg& cfg, float* tf, const ss_batch_out& dev);
+} // namespace ssb
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+enum class BankState { Free, Filling, Busy };
+
+struct Bank {
+    BankState state = BankState::Free;
+    uint64_t window = 0;
+    int rows_in = 0;
+    // device
+    unsigned char* iq = nullptr;
+    float* tf = nullptr;
+    float* psd_raw = nullptr;
+    float* psd_smoothed = nullptr;
+    float* floor_thr = nullptr;
+    int32_t* active = nullptr;
+    int32_t* n_active = nullptr;
+    ss_box* boxes = nullptr;
+    ss_bin_box* bin_boxes = nullptr;
+    int32_t* n_boxes = nullptr;
+    // pinned host record
+    struct Host {
+        int32_t n_boxes;
+        int32_t n_active;
+        float floor_thr[2];
+    }* host = nullptr;
+    ss_box* h_boxes = nullptr;
+    ss_bin_box* h_bin_boxes = nullptr;
+    cudaEvent_t rows_ready = nullptr;
+    Clock::time_point complete_at{};
+    Clock::time_point done_at{};
+};
+
+} // namespace
+
+struct ss_engine {
+    ss_engine_cfg cfg{};
+    ss_detector_cfg det{};
+    ss_ctx* ctx = nullptr;
+    cudaStream_t compute = nullptr;
+    cudaStream_t copy = nullptr;
+    int device = 0;
+    size_t sbytes = 8;
+    double deadline_s = 0.0;
+    Clock::time_point t0{};
+    std::vector<Bank> banks;
+
+    std::mutex mu;
+    std::condition_variable released;  // a bank went Free (writers waiting)
+    std::condition_variable ready;     // a record is ready (poller waiting)
+    std::deque<int> done;              // banks with records, completion order
+    uint64_t completed = 0, overruns = 0, rows_retired = 0, launched = 0, polled = 0;
+    bool have_dropped = false;
+    uint64_t dropped_window = 0;       // most recent window shed (its later rows are ignored)
+    uint64_t newest_window = 0;        // highest window seen (rows of older, recycled windows are stale)
+    bool finished = false;
+    std::string err;
+
+    double secs(Clock::time_point t) const { return std::chrono::duration<double>(t - t0).count(); }
+};
+
+namespace {
+
+ss_status efail(ss_engine* e, ss_status s, const std::string& msg) {
+    e->err = msg;
+    return s;
+}
+
+#define EN_CK(e, expr)                                                                                  \
+    do {                                                                                                \
+        cudaError_t c_ = (expr);                                                                        \
+        if (c_ != cudaSuccess) return efail((e), SS_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(c_)); \
+    } while (0)
+
+struct DoneArg {
+    ss_engine* e;
+    int bank;
+};
+
+void CUDART_CB on_done(void* p) {
+    // driver thread: no CUDA calls here
+    const Clock::time_point now = Clock::now();  // before the lock: a pusher may hold it
+    DoneArg* a = static_cast<DoneArg*>(p);
+    ss_engine* e = a->e;
+    {
+        std::lock_guard<std::mutex> lk(e->mu);
+        e->banks[static_cast<size_t>(a->bank)].done_at = now;
+        e->done.push_back(a->bank);
+    }
+    e->ready.notify_all();
+    delete a;
+}
+
+ss_batch_out dev_out(const Bank& b, int cap) {
+    ss_batch_out o{};
+    o.psd_raw = b.psd_raw;
+    o.psd_smoothed = b.psd_smoothed;
+    o.floor_thr = b.floor_thr;
+    o.active = b.active;
+    o.n_active = b.n_active;
+    o.boxes = b.boxes;
+    o.bin_boxes = b.bin_boxes;
+    o.n_boxes = b.n_boxes;
+    o.box_capacity = cap;
+    return o;
+}
+
+// Window of bank b is complete: launch its sensing.  Called with mu held.
+ss_status launch_window(ss_engine* e, int bi) {
+    Bank& b = e->banks[static_cast<size_t>(bi)];
+    const int F = e->cfg.n_fft, T = e->cfg.plot_rows, K = e->cfg.box_capacity;
+    b.complete_at = Clock::now();
+    EN_CK(e, cudaEventRecord(b.rows_ready, e->copy));
+    EN_CK(e, cudaStreamWaitEvent(e->compute, b.rows_ready, 0));
+    const ss_status s = ssb::engine_sense(e->ctx, b.iq, e->cfg.fmt, F, T, b.window * static_cast<uint64_t>(T),
+                                          e->cfg.sample_rate_hz, e->det, b.tf, dev_out(b, K));
+    if (s != SS_OK) return efail(e, s, ss_last_error(e->ctx));
+    EN_CK(e, cudaMemcpyAsync(&b.host->n_boxes, b.n_boxes, sizeof(int32_t), cudaMemcpyDeviceToHost, e->compute));
+    EN_CK(e, cudaMemcpyAsync(&b.host->n_active, b.n_active, sizeof(int32_t), cudaMemcpyDeviceToHost, e->compute));
+    EN_CK(e, cudaMemcpyAsync(b.host->floor_thr, b.floor_thr, 2 * sizeof(float), cudaMemcpyDeviceToHost, e->compute));
+    EN_CK(e, cudaMemcpyAsync(b.h_boxes, b.boxes, sizeof(ss_box) * K, cudaMemcpyDeviceToHost, e->compute));
+    EN_CK(e, cudaMemcpyAsync(b.h_bin_boxes, b.bin_boxes, sizeof(ss_bin_box) * K, cudaMemcpyDeviceToHost, e->compute));
+    EN_CK(e, cudaLaunchHostFunc(e->compute, on_done, new DoneArg{e, bi}));
+    b.state = BankState::Busy;
+    ++e->completed;
+    ++e->launched;
+    return SS_OK;
+}
+
+// Bank for window w, or -1 when its rows must be dropped.  Called with lk held.
+int claim_bank(ss_engine* e, uint64_t w, std::unique_lock<std::mutex>& lk) {
+    if (e->have_dropped && w == e->dropped_window) return -1;
+    if (w + static_cast<uint64_t>(e->cfg.n_banks) <= e->newest_window) return -1;  // stale row
+    const int bi = static_cast<int>(w % static_cast<uint64_t>(e->cfg.n_banks));
+    for (;;) {
+        Bank& b = e->banks[static_cast<size_t>(bi)];
+        if (b.state == BankState::Filling && b.window == w) return bi;
+        if (b.state == BankState::Filling && b.window < w) {
+            // an older window never completed (rows lost upstream): shed it
+            ++e->overruns;
+            b.state = BankState::Free;
+        }
+        if (b.state == BankState::Free) {
+            b.state = BankState::Filling;
+            b.window = w;
+            b.rows_in = 0;
+            e->newest_window = std::max(e->newest_window, w);
+            return bi;
+        }
+        // Busy: held by the reader (or a newer window is filling it)
+        if (b.state == BankState::Filling && b.window > w) return -1;
+        if (e->cfg.paced) {
+            ++e->overruns;
+            e->have_dropped = true;
+            e->dropped_window = w;
+            e->newest_window = std::max(e->newest_window, w);
+            return -1;
+        }
+        e->released.wait(lk);
+    }
+}
+
+} // namespace
+
+extern "C" {
+
+ss_status ss_engine_open(int device, const ss_engine_cfg* cfg, const ss_detector_cfg* det, ss_engine** out) {
+    if (!cfg || !det || !out) return SS_EVALIDATION;
+    *out = nullptr;
+    ss_engine* e = new ss_engine();
+    e->cfg = *cfg;
+    e->det = *det;
+    e->device = device;
+    if (e->cfg.n_banks == 0) e->cfg.n_banks = 2;
+    if (e->cfg.box_capacity <= 0) e->cfg.box_capacity = 1024;
+    ss_status s = ssb::engine_ctx_open(device, &e->ctx);
+    if (s != SS_OK) {
+        delete e;
+        return s;
+    }
+    auto bad = [&](ss_status st, const std::string& m) {
+        // keep the message reachable through the half-built engine
+        e->err = m;
+        *out = e;
+        return st;
+    };
+    s = ssb::engine_check(e->ctx, cfg->n_fft, cfg->plot_rows, cfg->fmt, cfg->sample_rate_hz, *det);
+    if (s != SS_OK) return bad(s, ss_last_error(e->ctx));
+    if (e->cfg.n_banks < 2) return bad(SS_EVALIDATION, "n_banks must be >= 2");
+    if (cfg->deadline_s < 0.0) return bad(SS_EVALIDATION, "deadline_s must be >= 0");
+    const int F = cfg->n_fft, T = cfg->plot_rows, K = e->cfg.box_capacity;
+    e->sbytes = cfg->fmt == SS_FMT_F32 ? 8 : 4;
+    e->deadline_s = cfg->deadline_s > 0.0 ? cfg->deadline_s : static_cast<double>(T) * F / cfg->sample_rate_hz;
+    e->compute = ssb::engine_ctx_stream(e->ctx);
+    if (cudaStreamCreateWithFlags(&e->copy, cudaStreamNonBlocking) != cudaSuccess) return bad(SS_ECUDA, "copy stream");
+    e->banks.resize(static_cast<size_t>(e->cfg.n_banks));
+    const size_t cells = static_cast<size_t>(T) * F;
+    for (Bank& b : e->banks) {
+        bool ok = cudaMalloc(&b.iq, cells * e->sbytes) == cudaSuccess && cudaMalloc(&b.tf, cells * sizeof(float)) == cudaSuccess &&
+                  cudaMalloc(&b.psd_raw, sizeof(float) * F) == cudaSuccess &&
+                  cudaMalloc(&b.psd_smoothed, sizeof(float) * F) == cudaSuccess &&
+                  cudaMalloc(&b.floor_thr, sizeof(float) * 2) == cudaSuccess &&
+                  cudaMalloc(&b.active, sizeof(int32_t) * F) == cudaSuccess &&
+                  cudaMalloc(&b.n_active, sizeof(int32_t)) == cudaSuccess &&
+                  cudaMalloc(&b.boxes, sizeof(ss_box) * K) == cudaSuccess &&
+                  cudaMalloc(&b.bin_boxes, sizeof(ss_bin_box) * K) == cudaSuccess &&
+                  cudaMalloc(&b.n_boxes, sizeof(int32_t)) == cudaSuccess &&
+                  cudaMallocHost(&b.host, sizeof(Bank::Host)) == cudaSuccess &&
+                  cudaMallocHost(&b.h_boxes, sizeof(ss_box) * K) == cudaSuccess &&
+                  cudaMallocHost(&b.h_bin_boxes, sizeof(ss_bin_box) * K) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&b.rows_ready, cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) return bad(SS_ECUDA, "engine bank allocation failed");
+    }
+    // warm-up: one window of zeros through the whole chain, so workspace,
+    // twiddles and weights exist before the first real window is timed
+    Bank& b0 = e->banks[0];
+    if (cudaMemsetAsync(b0.iq, 0, cells * e->sbytes, e->compute) != cudaSuccess) return bad(SS_ECUDA, "memset");
+    s = ssb::engine_sense(e->ctx, b0.iq, cfg->fmt, F, T, 0, cfg->sample_rate_hz, *det, b0.tf, dev_out(b0, K));
+    if (s != SS_OK) return bad(s, ss_last_error(e->ctx));
+    if (cudaStreamSynchronize(e->compute) != cudaSuccess) return bad(SS_ECUDA, "warm-up failed");
+    e->t0 = Clock::now();
+    *out = e;
+    return SS_OK;
+}
+
+void ss_engine_close(ss_engine* e) {
+    if (!e) return;
+    if (e->compute) cudaStreamSynchronize(e->compute);
+    if (e->copy) {
+        cudaStreamSynchronize(e->copy);
+        cudaStreamDestroy(e->copy);
+    }
+    for (Bank& b : e->banks) {
+        cudaFree(b.iq);
+        cudaFree(b.tf);
+        cudaFree(b.psd_raw);
+        cudaFree(b.psd_smoothed);
+        cudaFree(b.floor_thr);
+        cudaFree(b.active);
+        cudaFree(b.n_active);
+        cudaFree(b.boxes);
+        cudaFree(b.bin_boxes);
+        cudaFree(b.n_boxes);
+        cudaFreeHost(b.host);
+        cudaFreeHost(b.h_boxes);
+        cudaFreeHost(b.h_bin_boxes);
+        if (b.rows_ready) cudaEventDestroy(b.rows_ready);
+    }
+    if (e->ctx) ss_close(e->ctx);
+    delete e;
+}
+
+const char* ss_engine_last_error(const ss_engine* e) { return e ? e->err.c_str() : "no engine"; }
+
+ss_status ss_engine_push(ss_engine* e, const void* samples, int64_t n_chunks, uint64_t first_seq) {
+    if (!e || (!samples && n_chunks > 0) || n_chunks < 0) return SS_EVALIDATION;
+    const int F = e->cfg.n_fft, T = e->cfg.plot_rows;
+    const size_t row_bytes = static_cast<size_t>(F) * e->sbytes;
+    const unsigned char* src = static_cast<const unsigned char*>(samples);
+    std::unique_lock<std::mutex> lk(e->mu);
+    if (e->finished) return efail(e, SS_EVALIDATION, "push after finish");
+    int64_t i = 0;
+    while (i < n_chunks) {
+        const uint64_t seq = first_seq + static_cast<uint64_t>(i);
+        const uint64_t w = seq / static_cast<uint64_t>(T);
+        const int r0 = static_cast<int>(seq % static_cast<uint64_t>(T));
+        // rows of this window in this push
+        const int64_t run = std::min<int64_t>(n_chunks - i, T - r0);
+        const int bi = claim_bank(e, w, lk);
+        e->rows_retired += static_cast<uint64_t>(run);
+        if (bi >= 0) {
+            Bank& b = e->banks[static_cast<size_t>(bi)];
+            EN_CK(e, cudaMemcpyAsync(b.iq + static_cast<size_t>(r0) * row_bytes, src + static_cast<size_t>(i) * row_bytes,
+                                     static_cast<size_t>(run) * row_bytes, cudaMemcpyDefault, e->copy));
+            b.rows_in += static_cast<int>(run);
+            if (b.rows_in >= T) {
+                const ss_status s = launch_window(e, bi);
+                if (s != SS_OK) return s;
+            }
+        }
+        i += run;
+    }
+    return SS_OK;
+}
+
+ss_status ss_engine_mark_lost(ss_engine* e, uint64_t first, uint64_t last) {
+    if (!e) return SS_EVALIDATION;
+    if (last <= first) return SS_OK;
+    const uint64_t T = static_cast<uint64_t>(e->cfg.plot_rows);
+    std::lock_guard<std::mutex> lk(e->mu);
+    e->rows_retired += last - first;
+    for (uint64_t w = first / T; w <= (last - 1) / T; ++w) {
+        const int bi = static_cast<int>(w % static_cast<uint64_t>(e->cfg.n_banks));
+        Bank& b = e->banks[static_cast<size_t>(bi)];
+        if (b.state == BankState::Filling && b.window == w) b.state = BankState::Free;
+        if (!(e->have_dropped && e->dropped_window == w)) ++e->overruns;
+        e->have_dropped = true;
+        e->dropped_window = w;
+        e->newest_window = std::max(e->newest_window, w);
+    }
+    return SS_OK;
+}
+
+ss_status ss_engine_finish(ss_engine* e) {
+    if (!e) return SS_EVALIDATION;
+    {
+        std::lock_guard<std::mutex> lk(e->mu);
+        e->finished = true;
+        for (Bank& b : e->banks)
+            if (b.state == BankState::Filling) b.state = BankState::Free;  // partial tail window
+    }
+    e->ready.notify_all();
+    return SS_OK;
+}
+
+ss_status ss_engine_poll(ss_engine* e, int wait_ms, ss_plot_record* rec, ss_box* boxes, ss_bin_box* bin_boxes, int cap,
+                         int* got) {
+    if (!e || !got) return SS_EVALIDATION;
+    *got = 0;
+    std::unique_lock<std::mutex> lk(e->mu);
+    auto has = [&] { return !e->done.empty() || (e->finished && e->polled == e->launched); };
+    if (wait_ms < 0) e->ready.wait(lk, has);
+    else if (wait_ms > 0) e->ready.wait_for(lk, std::chrono::milliseconds(wait_ms), has);
+    if (e->done.empty()) return SS_OK;
+    const int bi = e->done.front();
+    e->done.pop_front();
+    Bank& b = e->banks[static_cast<size_t>(bi)];
+    const int K = e->cfg.box_capacity;
+    const int nb = b.host->n_boxes;
+    const int keep = std::min({nb, K, std::max(cap, 0)});
+    if (rec) {
+        rec->plot_index = b.window;
+        rec->start_seq = b.window * static_cast<uint64_t>(e->cfg.plot_rows);
+        rec->latency_s = std::chrono::duration<double>(b.done_at - b.complete_at).count();
+        rec->deadline_s = e->deadline_s;
+        rec->met = rec->latency_s <= e->deadline_s ? 1 : 0;
+        rec->n_boxes = nb;
+        rec->n_active = b.host->n_active;
+        rec->noise_floor = b.host->floor_thr[0];
+        rec->threshold = b.host->floor_thr[1];
+        rec->complete_s = e->secs(b.complete_at);
+        rec->done_s = e->secs(b.done_at);
+    }
+    if (boxes && keep > 0) std::memcpy(boxes, b.h_boxes, sizeof(ss_box) * static_cast<size_t>(keep));
+    if (bin_boxes && keep > 0) std::memcpy(bin_boxes, b.h_bin_boxes, sizeof(ss_bin_box) * static_cast<size_t>(keep));
+    b.state = BankState::Free;
+    ++e->polled;
+    *got = 1;
+    lk.unlock();
+    e->released.notify_all();
+    if (nb > K) return efail(e, SS_ECAPACITY, "box capacity too small: " + std::to_string(nb));
+    return SS_OK;
+}
+
+ss_status ss_engine_stats(ss_engine* e, uint64_t* completed, uint64_t* overruns, uint64_t* rows_retired,
+                          uint64_t* pending) {
+    if (!e) return SS_EVALIDATION;
+    std::lock_guard<std::mutex> lk(e->mu);
+    if (completed) *completed = e->completed;
+    if (overruns) *overruns = e->overruns;
+    if (rows_retired) *rows_retired = e->rows_retired;
+    if (pending) *pending = e->launched - e->polled;
+    return SS_OK;
+}
+
+} // extern "C"

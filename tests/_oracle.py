@@ -66,6 +66,10 @@ class _Ref:
                                  C.POINTER(C.c_double)],
             "ref_run_engine": [_f32p, _ll, C.c_double, C.c_int, C.c_int, _ll, C.c_int, C.c_int,
                                _f64p],
+            "ref_summarize": [_ll, C.POINTER(C.c_ulonglong), _f64p, _i32p, C.c_ulonglong, C.c_double, _f64p,
+                              _f64p, _ll],
+            "ref_run_engine_boxes": [_f32p, _ll, C.c_double, C.c_int, C.c_int, _ll, C.c_int, C.c_int,
+                                     C.POINTER(C.c_ulonglong), _f64p, _ll, C.POINTER(C.c_ulonglong)],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -214,6 +218,35 @@ class _Ref:
                                                 n_compute, n_sensing, stats))
         keys = ["plots", "overruns", "wall_s", "p50_s", "p99_s", "fraction_met", "fft_time_s"]
         return boxes, dict(zip(keys, stats.tolist()))
+
+    def summarize(self, plot_index, latency, met, overruns, deadline):
+        """runtime::summarize + RunReport::ccdf on scripted records."""
+        n = len(latency)
+        pi = np.ascontiguousarray(plot_index, np.uint64)
+        lat = np.ascontiguousarray(latency, np.float64)
+        m = np.ascontiguousarray(met, np.int32)
+        stats = np.zeros(10, np.float64)
+        cc = np.zeros(2 * max(n, 1), np.float64)
+        k = self._chk(self.L.ref_summarize(n, pi.ctypes.data_as(C.POINTER(C.c_ulonglong)), lat, m, overruns,
+                                           deadline, stats, cc, max(n, 1)))
+        keys = ["plots", "overruns", "deadline_s", "fraction_met", "realtime_met", "p50_s", "p90_s", "p99_s",
+                "max_s", "percentiles_valid"]
+        return dict(zip(keys, stats.tolist())), [tuple(x) for x in cc[: 2 * k].reshape(-1, 2).tolist()]
+
+    def run_engine_boxes(self, samples, fs, n_fft, rows, n_plots, n_compute=2, n_sensing=4, cap=1 << 16):
+        """The reference engine (runtime::run, unpaced MemorySource) -> {plot_index: boxes (n,4)}."""
+        iq = np.ascontiguousarray(samples.astype(np.complex64)).view(np.float32)
+        plots = np.zeros(cap, np.uint64)
+        boxes = np.zeros(4 * cap, np.float64)
+        seen = C.c_ulonglong(0)
+        n = self._chk(self.L.ref_run_engine_boxes(iq, len(samples), fs, n_fft, rows, n_plots, n_compute, n_sensing,
+                                                  plots.ctypes.data_as(C.POINTER(C.c_ulonglong)), boxes, cap,
+                                                  C.byref(seen)))
+        out = {}
+        b = boxes[: 4 * n].reshape(-1, 4)
+        for i in range(n):
+            out.setdefault(int(plots[i]), []).append(b[i])
+        return {k: np.array(v) for k, v in out.items()}, int(seen.value)
 
 
 class _Ora:
