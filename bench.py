@@ -392,11 +392,120 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------- stream mode
+# the real-time engine at the paper's configuration P
+# (fs = 100 MS/s, F = 1024, T = 2000: one window per 20.48 ms), fed from
+# pinned host memory through ss_engine_* (ingest thread -> HBM banks -> GPU).
+P_F, P_T = 1024, 2000
+
+
+def _p_samples(n_windows=5):
+    sys.path.insert(0, str(ROOT / "tests"))
+    from paper_2603_20481_b200 import signals
+    from _oracle import ref
+
+    sc = signals.paper_scenario(rows=n_windows * P_T)
+    iq, _ = ref().synthesize(signals.scenario_json(sc))
+    return iq[: n_windows * P_T * P_F]
+
+
+def run_stream(args):
+    import numpy as np  # noqa: F401
+    import torch
+
+    from paper_2603_20481_b200 import runtime as rt
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    iq = _p_samples()
+    fc = rt.FrontendConfig(FS, P_F, P_T)
+    windows = max(args.steps, 1) * args.stream_windows
+    # warm-up pass (allocations, pinned copies, clocks)
+    rt.run(rt.MemorySource(iq, P_F, total_chunks=args.warmup * P_T, block=256), fc)
+    with Clocks(local) as clk:
+        t0 = time.perf_counter()
+        rep = rt.run(rt.MemorySource(iq, P_F, total_chunks=windows * P_T, block=256), fc)
+        wall = time.perf_counter() - t0
+    # paced at the real sample rate: latency against the 20.48 ms deadline
+    paced_windows = max(20, int(args.stream_paced_s / fc.plot_span_s()))
+    prep = rt.run(rt.MemorySource(iq, P_F, total_chunks=paced_windows * P_T, pace=True, sample_rate_hz=FS,
+                                  block=64), fc)
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = _stream_reference(iq, args.cpu_seconds)
+    if rank == 0:
+        line = {
+            "metric": "streaming-engine plots/s (config P: 100 MS/s fp32, F=1024, T=2000 windows, host-fed)",
+            "value": rep.plots / wall, "unit": "plots/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic: the acceptance-style paper scenario, cycled",
+            "config": {"workload": "P stream: MemorySource (pinned) -> ss_engine (2 HBM banks) -> boxes",
+                       "windows_per_step": args.stream_windows, "parallelism": "replicas" if ws > 1 else "single"},
+            "stream": {"unpaced": {"plots": rep.plots, "overruns": rep.overruns, "wall_s": wall,
+                                   "p50_ms": 1e3 * rep.p50_s, "p99_ms": 1e3 * rep.p99_s,
+                                   "iq_gbps": rep.plots * P_T * P_F * 32 / wall / 1e9,
+                                   "h2d_gbps": rep.plots * P_T * P_F * 8 / wall / 1e9},
+                       "paced": {"plots": prep.plots, "overruns": prep.overruns, "p50_ms": 1e3 * prep.p50_s,
+                                 "p90_ms": 1e3 * prep.p90_s, "p99_ms": 1e3 * prep.p99_s, "max_ms": 1e3 * prep.max_s,
+                                 "deadline_ms": 1e3 * prep.deadline_s, "fraction_met": prep.fraction_met,
+                                 "realtime_met": prep.realtime_met, "percentiles_valid": prep.percentiles_valid}},
+            "e2e": {"value": rep.plots / wall, "unit": "plots/s", "h2d_bytes_per_step": args.stream_windows * P_T * P_F * 8,
+                    "d2h_bytes_per_step": args.stream_windows * 1024 * 64},
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+
+
+def _stream_reference(iq, seconds):
+    """The reference engine (runtime::run over an unpaced MemorySource, the
+    acceptance split: 16 sensing + 4 compute workers on >= 16 cores, else 4 + 2)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from _oracle import ref
+
+    R = ref()
+    cores = os.cpu_count() or 1
+    n_sense, n_comp = (16, 4) if cores >= 16 else (4, 2)
+    _, st = R.run_engine(iq, FS, P_F, P_T, 4, n_comp, n_sense)
+    per = st["wall_s"] / max(st["plots"], 1)
+    n = max(8, int(seconds / max(per, 1e-3)))
+    _, st = R.run_engine(iq, FS, P_F, P_T, n, n_comp, n_sense)
+    return {"value": st["plots"] / st["wall_s"], "unit": "plots/s", "cores": n_sense + n_comp, "kind": "reference",
+            "sample": f"{int(st['plots'])} P windows through runtime::run ({n_comp} compute + {n_sense} sensing "
+                      f"workers, unpaced MemorySource) in {st['wall_s']:.1f} s",
+            "p50_ms": 1e3 * st["p50_s"], "p99_ms": 1e3 * st["p99_s"], "fraction_met": st["fraction_met"]}
+
+
+def run_stream_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    iq = _p_samples()
+    vals = []
+    for i in range(args.warmup + args.steps):
+        c = _stream_reference(iq, args.ref_step_seconds)
+        if i >= args.warmup:
+            vals.append(c)
+    v = sum(c["value"] for c in vals) / len(vals)
+    line = {"impl": "reference",
+            "metric": "streaming-engine plots/s (config P: 100 MS/s fp32, F=1024, T=2000 windows, host-fed)",
+            "value": v, "unit": "plots/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: the acceptance-style paper scenario, cycled",
+            "config": {"workload": "P stream: MemorySource -> runtime::run (CPU)"},
+            "cpu_baseline": dict(vals[-1], value=v),
+            "e2e": {"value": v, "unit": "plots/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--mode", default="c5r", choices=sorted(WORKLOADS),
-                    help="c5r: reference-parity rect/hop-N frontend (default); hann: config 5 as written")
+    ap.add_argument("--mode", default="c5r", choices=sorted(WORKLOADS) + ["stream"],
+                    help="c5r: reference-parity rect/hop-N frontend (default); hann: config 5 as written; "
+                         "stream: the real-time engine at config P (latency + plots/s)")
+    ap.add_argument("--stream-windows", type=int, default=200, help="stream mode: windows per timed step")
+    ap.add_argument("--stream-paced-s", type=float, default=3.0, help="stream mode: seconds of paced real-time input")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -409,7 +518,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (kernel experiments only)")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.mode == "stream":
+        (run_stream_reference if args.impl == "reference" else run_stream)(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -234,10 +234,84 @@ __global__ void psd_cols_kernel(const float* __restrict__ tf, int rows, int cols
     out[static_cast<long long>(p) * (c1 - c0) + (c - c0)] = __double2float_rn(__dmul_rn(acc, inv));
 }
 
+// Tiled form for 8-column groups (16-byte aligned rows): one CTA per (plot,
+// 8 columns).  All 256 threads stream row chunks (256 rows x 32 B) into a
+// 4-deep shared ring with cp.async; the 8 owning threads then run each
+// column's sum in row order out of shared memory.  Keeps ~24 KB per CTA in
+// flight, so even one plot (F/8 CTAs) streams its TF plot at a useful rate
+// where the thread-per-column form is bound by 8 loads in flight per column.
+constexpr int kPsdTileCols = 8;
+constexpr int kPsdTileRows = 256;
+constexpr int kPsdStages = 4;
+
+__device__ __forceinline__ void psd_cp16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem)
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(kPsdTileRows) psd_tile_kernel(const float* __restrict__ tf, int rows, int cols,
+                                                               int c0, int c1, float* __restrict__ out) {
+    __shared__ __align__(16) float ring[kPsdStages][kPsdTileRows * kPsdTileCols];
+    const int g = blockIdx.x, p = blockIdx.y, t = threadIdx.x;
+    const float* base = tf + static_cast<long long>(p) * rows * cols + c0 + g * kPsdTileCols;
+    const int nchunks = (rows + kPsdTileRows - 1) / kPsdTileRows;
+    auto load = [&](int chunk) {
+        if (chunk < nchunks) {
+            const int r = chunk * kPsdTileRows + t;
+            if (r < rows) {
+                float* dst = &ring[chunk % kPsdStages][t * kPsdTileCols];
+                const float* src = base + static_cast<long long>(r) * cols;
+                psd_cp16(dst, src);
+                psd_cp16(dst + 4, src + 4);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll
+    for (int c = 0; c < kPsdStages - 1; ++c) load(c);
+    double acc = 0.0;
+    for (int c = 0; c < nchunks; ++c) {
+        load(c + kPsdStages - 1);
+        asm volatile("cp.async.wait_group %0;" ::"n"(kPsdStages - 1) : "memory");
+        __syncthreads();
+        if (t < kPsdTileCols) {
+            const float* v = &ring[c % kPsdStages][t];
+            const int nr = min(kPsdTileRows, rows - c * kPsdTileRows);
+            int r = 0;
+            for (; r + 8 <= nr; r += 8) {
+                float x[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) x[q] = v[(r + q) * kPsdTileCols];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const double d = static_cast<double>(x[q]);
+                    acc = __fma_rn(d, d, acc);
+                }
+            }
+            for (; r < nr; ++r) {
+                const double d = static_cast<double>(v[r * kPsdTileCols]);
+                acc = __fma_rn(d, d, acc);
+            }
+        }
+        __syncthreads();  // slot c % stages is refilled by the load at c + 1
+    }
+    if (t < kPsdTileCols) {
+        const double inv = __ddiv_rn(1.0, static_cast<double>(rows));
+        out[static_cast<long long>(p) * (c1 - c0) + g * kPsdTileCols + t] = __double2float_rn(__dmul_rn(acc, inv));
+    }
+}
+
 cudaError_t psd_cols_launch(const float* tf, int n_plots, int rows, int cols, int c0, int c1,
                             float* out, cudaStream_t st) {
     const int w = c1 - c0;
     if (w <= 0 || n_plots <= 0) return cudaSuccess;
+    const bool aligned = reinterpret_cast<uintptr_t>(tf) % 16 == 0 && cols % 4 == 0 && c0 % 4 == 0;
+    if (aligned && w % kPsdTileCols == 0) {
+        dim3 grid(w / kPsdTileCols, n_plots);
+        psd_tile_kernel<<<grid, kPsdTileRows, 0, st>>>(tf, rows, cols, c0, c1, out);
+        return cudaGetLastError();
+    }
     dim3 grid((w + 127) / 128, n_plots);
     psd_cols_kernel<<<grid, 128, 0, st>>>(tf, rows, cols, c0, c1, out);
     return cudaGetLastError();
