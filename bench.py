@@ -448,7 +448,9 @@ def run_stream(args):
                        "paced": {"plots": prep.plots, "overruns": prep.overruns, "p50_ms": 1e3 * prep.p50_s,
                                  "p90_ms": 1e3 * prep.p90_s, "p99_ms": 1e3 * prep.p99_s, "max_ms": 1e3 * prep.max_s,
                                  "deadline_ms": 1e3 * prep.deadline_s, "fraction_met": prep.fraction_met,
-                                 "realtime_met": prep.realtime_met, "percentiles_valid": prep.percentiles_valid}},
+                                 "realtime_met": prep.realtime_met, "percentiles_valid": prep.percentiles_valid,
+                                 "slowest": [[r.plot_index, round(1e3 * r.latency_s, 3), round(1e3 * r.gpu_s, 3), round(r.complete_s, 4)]
+                                             for r in sorted(prep.records, key=lambda r: -r.latency_s)[:6]]}},
             "e2e": {"value": rep.plots / wall, "unit": "plots/s", "h2d_bytes_per_step": args.stream_windows * P_T * P_F * 8,
                     "d2h_bytes_per_step": args.stream_windows * 1024 * 64},
             "clocks": clk.summary(),

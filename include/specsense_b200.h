@@ -235,6 +235,7 @@ typedef struct {
     float threshold;
     double complete_s;     /* engine clock: window complete */
     double done_s;         /* engine clock: boxes on the host */
+    double gpu_s;          /* device time from the window's first kernel to its boxes' D2H end */
 } ss_plot_record;
 
 ss_status ss_engine_open(int device, const ss_engine_cfg* cfg, const ss_detector_cfg* det, ss_engine** out);

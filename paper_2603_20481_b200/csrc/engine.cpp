@@ -11,8 +11,12 @@
 //   window complete: an event on the copy stream gates K1..K6 for that window
 //             on the compute stream (its own ss_ctx, exact-pool CCL: no host
 //             synchronisation anywhere on this path), then a D2H of the
-//             boxes into the bank's pinned record and a host callback that
-//             stamps the completion time and queues the bank for poll().
+//             boxes into the bank's pinned record and a `done` event.  A
+//             completion thread spin-polls the done events in launch order,
+//             stamps the completion time and queues the bank for poll()
+//             (a cudaLaunchHostFunc callback showed 10-40 ms delivery
+//             outliers at P rates; the spinning waiter is busy only while a
+//             window is in flight).
 //   poll()  : hands records out in completion order and releases the bank.
 //
 // Bank rules follow PingPongBuffer: rows of a window whose bank is still held
@@ -28,6 +32,7 @@
 #include <deque>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -70,6 +75,9 @@ struct Bank {
     ss_box* h_boxes = nullptr;
     ss_bin_box* h_bin_boxes = nullptr;
     cudaEvent_t rows_ready = nullptr;
+    cudaEvent_t start_ev = nullptr;  // compute stream, before the window's first kernel
+    cudaEvent_t done_ev = nullptr;   // compute stream, after the boxes' D2H
+    double gpu_s = 0.0;
     Clock::time_point complete_at{};
     Clock::time_point done_at{};
 };
@@ -92,6 +100,10 @@ struct ss_engine {
     std::condition_variable released;  // a bank went Free (writers waiting)
     std::condition_variable ready;     // a record is ready (poller waiting)
     std::deque<int> done;              // banks with records, completion order
+    std::deque<int> inflight;          // banks launched, not yet complete (launch order)
+    std::condition_variable launched_cv;
+    std::thread waiter;
+    bool stop = false;
     uint64_t completed = 0, overruns = 0, rows_retired = 0, launched = 0, polled = 0;
     bool have_dropped = false;
     uint64_t dropped_window = 0;       // most recent window shed (its later rows are ignored)
@@ -115,23 +127,33 @@ ss_status efail(ss_engine* e, ss_status s, const std::string& msg) {
         if (c_ != cudaSuccess) return efail((e), SS_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(c_)); \
     } while (0)
 
-struct DoneArg {
-    ss_engine* e;
-    int bank;
-};
-
-void CUDART_CB on_done(void* p) {
-    // driver thread: no CUDA calls here
-    const Clock::time_point now = Clock::now();  // before the lock: a pusher may hold it
-    DoneArg* a = static_cast<DoneArg*>(p);
-    ss_engine* e = a->e;
-    {
-        std::lock_guard<std::mutex> lk(e->mu);
-        e->banks[static_cast<size_t>(a->bank)].done_at = now;
-        e->done.push_back(a->bank);
+// Completion thread: waits for each launched window's done event in launch
+// order (spin on cudaEventQuery, yield between polls), then publishes it.
+void waiter_main(ss_engine* e) {
+    cudaSetDevice(e->device);
+    for (;;) {
+        int bi;
+        {
+            std::unique_lock<std::mutex> lk(e->mu);
+            e->launched_cv.wait(lk, [&] { return e->stop || !e->inflight.empty(); });
+            if (e->inflight.empty()) return;  // stop requested and nothing in flight
+            bi = e->inflight.front();
+        }
+        Bank& b = e->banks[static_cast<size_t>(bi)];
+        cudaError_t st;
+        while ((st = cudaEventQuery(b.done_ev)) == cudaErrorNotReady) std::this_thread::yield();
+        const Clock::time_point now = Clock::now();
+        float ms = 0.f;
+        if (st == cudaSuccess) cudaEventElapsedTime(&ms, b.start_ev, b.done_ev);
+        {
+            std::lock_guard<std::mutex> lk(e->mu);
+            e->inflight.pop_front();
+            b.done_at = now;
+            b.gpu_s = 1e-3 * ms;
+            e->done.push_back(bi);
+        }
+        e->ready.notify_all();
     }
-    e->ready.notify_all();
-    delete a;
 }
 
 ss_batch_out dev_out(const Bank& b, int cap) {
@@ -155,6 +177,7 @@ ss_status launch_window(ss_engine* e, int bi) {
     b.complete_at = Clock::now();
     EN_CK(e, cudaEventRecord(b.rows_ready, e->copy));
     EN_CK(e, cudaStreamWaitEvent(e->compute, b.rows_ready, 0));
+    EN_CK(e, cudaEventRecord(b.start_ev, e->compute));
     const ss_status s = ssb::engine_sense(e->ctx, b.iq, e->cfg.fmt, F, T, b.window * static_cast<uint64_t>(T),
                                           e->cfg.sample_rate_hz, e->det, b.tf, dev_out(b, K));
     if (s != SS_OK) return efail(e, s, ss_last_error(e->ctx));
@@ -163,8 +186,10 @@ ss_status launch_window(ss_engine* e, int bi) {
     EN_CK(e, cudaMemcpyAsync(b.host->floor_thr, b.floor_thr, 2 * sizeof(float), cudaMemcpyDeviceToHost, e->compute));
     EN_CK(e, cudaMemcpyAsync(b.h_boxes, b.boxes, sizeof(ss_box) * K, cudaMemcpyDeviceToHost, e->compute));
     EN_CK(e, cudaMemcpyAsync(b.h_bin_boxes, b.bin_boxes, sizeof(ss_bin_box) * K, cudaMemcpyDeviceToHost, e->compute));
-    EN_CK(e, cudaLaunchHostFunc(e->compute, on_done, new DoneArg{e, bi}));
+    EN_CK(e, cudaEventRecord(b.done_ev, e->compute));
     b.state = BankState::Busy;
+    e->inflight.push_back(bi);
+    e->launched_cv.notify_one();
     ++e->completed;
     ++e->launched;
     return SS_OK;
@@ -251,7 +276,8 @@ ss_status ss_engine_open(int device, const ss_engine_cfg* cfg, const ss_detector
                   cudaMallocHost(&b.host, sizeof(Bank::Host)) == cudaSuccess &&
                   cudaMallocHost(&b.h_boxes, sizeof(ss_box) * K) == cudaSuccess &&
                   cudaMallocHost(&b.h_bin_boxes, sizeof(ss_bin_box) * K) == cudaSuccess &&
-                  cudaEventCreateWithFlags(&b.rows_ready, cudaEventDisableTiming) == cudaSuccess;
+                  cudaEventCreateWithFlags(&b.rows_ready, cudaEventDisableTiming) == cudaSuccess &&
+                  cudaEventCreate(&b.start_ev) == cudaSuccess && cudaEventCreate(&b.done_ev) == cudaSuccess;
         if (!ok) return bad(SS_ECUDA, "engine bank allocation failed");
     }
     // warm-up: one window of zeros through the whole chain, so workspace,
@@ -262,12 +288,21 @@ ss_status ss_engine_open(int device, const ss_engine_cfg* cfg, const ss_detector
     if (s != SS_OK) return bad(s, ss_last_error(e->ctx));
     if (cudaStreamSynchronize(e->compute) != cudaSuccess) return bad(SS_ECUDA, "warm-up failed");
     e->t0 = Clock::now();
+    e->waiter = std::thread(waiter_main, e);
     *out = e;
     return SS_OK;
 }
 
 void ss_engine_close(ss_engine* e) {
     if (!e) return;
+    if (e->waiter.joinable()) {
+        {
+            std::lock_guard<std::mutex> lk(e->mu);
+            e->stop = true;
+        }
+        e->launched_cv.notify_all();
+        e->waiter.join();
+    }
     if (e->compute) cudaStreamSynchronize(e->compute);
     if (e->copy) {
         cudaStreamSynchronize(e->copy);
@@ -288,6 +323,8 @@ void ss_engine_close(ss_engine* e) {
         cudaFreeHost(b.h_boxes);
         cudaFreeHost(b.h_bin_boxes);
         if (b.rows_ready) cudaEventDestroy(b.rows_ready);
+        if (b.start_ev) cudaEventDestroy(b.start_ev);
+        if (b.done_ev) cudaEventDestroy(b.done_ev);
     }
     if (e->ctx) ss_close(e->ctx);
     delete e;
@@ -383,6 +420,7 @@ ss_status ss_engine_poll(ss_engine* e, int wait_ms, ss_plot_record* rec, ss_box*
         rec->threshold = b.host->floor_thr[1];
         rec->complete_s = e->secs(b.complete_at);
         rec->done_s = e->secs(b.done_at);
+        rec->gpu_s = b.gpu_s;
     }
     if (boxes && keep > 0) std::memcpy(boxes, b.h_boxes, sizeof(ss_box) * static_cast<size_t>(keep));
     if (bin_boxes && keep > 0) std::memcpy(bin_boxes, b.h_bin_boxes, sizeof(ss_bin_box) * static_cast<size_t>(keep));

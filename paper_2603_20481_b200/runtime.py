@@ -70,6 +70,7 @@ class PlotRecord:
     threshold: float = 0.0
     complete_s: float = 0.0
     done_s: float = 0.0
+    gpu_s: float = 0.0
 
 
 @dataclass
@@ -249,7 +250,7 @@ class Engine:
         bins = np.ctypeslib.as_array(C.cast(self._bins, C.POINTER(C.c_int32)), shape=(self.cap, 4))[:n].copy()
         r = PlotRecord(int(rec.plot_index), int(rec.start_seq), rec.latency_s, rec.deadline_s, bool(rec.met),
                        int(rec.n_boxes), int(rec.n_active), float(rec.noise_floor), float(rec.threshold),
-                       rec.complete_s, rec.done_s)
+                       rec.complete_s, rec.done_s, rec.gpu_s)
         self._check(st)
         return r, boxes, bins
 
