@@ -4,8 +4,9 @@
 // frontend.hpp (fft_row :47-48, TFPlotView / TFPlot :52-76, make_plot(s)
 // :79-84, FrontendConfig :12-24, resolution / stream_bit_rate_bps :32-38);
 // every call runs on the GPU through the C ABI (include/specsense_b200.h).
-// The streaming plumbing (PingPongBuffer, ChunkSources, UDP) is outside the
-// accelerated path and is not provided here.
+// The ChunkSource interface (:137-144) is declared so runtime::run
+// (specsense/runtime.hpp) accepts the reference's sources; the concrete
+// file / memory / UDP sources stay in the reference's I/O code.
 #pragma once
 
 #include "specsense/types.hpp"
@@ -44,6 +45,15 @@ struct IQChunk {
 };
 
 enum class SampleFormat { F32, I16 };
+
+// Pull-style chunk producer: next() fills one F-sample chunk, false at end of
+// stream; paced() sources deliver in real time and are shed, not blocked.
+class ChunkSource {
+  public:
+    virtual ~ChunkSource() = default;
+    virtual bool next(IQChunk& out) = 0;
+    virtual bool paced() const { return false; }
+};
 
 // out[k] = |DFT(chunk)[(k + F/2) mod F]|, F = chunk.size().
 void fft_row(std::span<const cfloat> chunk, std::span<float> out);

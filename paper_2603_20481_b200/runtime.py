@@ -53,6 +53,8 @@ class RuntimeConfig:
             raise ValidationError("worker counts must be positive")
         if self.halo_bins < 3:
             raise ValidationError("halo_bins must be >= 3")
+        if self.chunk_queue_capacity < 0:
+            raise ValidationError("chunk_queue_capacity must be >= 0")
         if self.deadline_s < 0:
             raise ValidationError("deadline_s must be >= 0")
 
@@ -104,7 +106,7 @@ def nearest_rank(sorted_values, q: float) -> float:
     """Element at 1-based index ceil(q*n), clamped to [1, n] (runtime.hpp:92-94)."""
     n = len(sorted_values)
     if n == 0:
-        raise ValidationError("nearest_rank of an empty sample")
+        return 0.0
     k = math.ceil(q * n)
     k = min(max(k, 1), n)
     return sorted_values[k - 1]

@@ -70,3 +70,58 @@ def test_dropin_demo_matches_reference(ref, tmp_path):
     assert np.array_equal(lab, elab)
     assert r.one(np.int32) == len(eext)
     assert r.one(np.int32) == 1
+
+
+RT_DEMO = ROOT / "paper_2603_20481_b200" / "_lib" / "runtime_demo"
+
+
+def _run_rt_demo(tmp_path, iq, fs, n_fft, rows, windows, paced):
+    f = tmp_path / "rt_iq.f32"
+    iq.astype(np.complex64).tofile(f)
+    out = tmp_path / "rt.bin"
+    subprocess.run([str(RT_DEMO), str(f), str(fs), str(n_fft), str(rows), str(windows), str(int(paced)), str(out)],
+                   check=True, timeout=120)
+    r = Reader(out.read_bytes())
+    per = {}
+    while True:
+        idx, nb = r.take(np.uint64, 2)
+        if idx == np.uint64(~np.uint64(0)):
+            plots = int(nb)
+            break
+        per[int(idx)] = r.take(np.float64, 4 * int(nb)).reshape(-1, 4)
+    stats = r.take(np.float64, 8)
+    ncc = int(r.one(np.uint64))
+    ccdf = r.take(np.float64, 2 * ncc).reshape(-1, 2)
+    slabs = r.take(np.int32, 12).reshape(3, 4)
+    return per, plots, stats, ccdf, slabs
+
+
+def test_runtime_dropin_matches_reference_engine(ref, tmp_path):
+    """specsense::runtime::run (C++ drop-in over the GPU engine) vs the reference's
+    own runtime::run on the same cycling source: every window's boxes identical."""
+    assert RT_DEMO.exists(), "build() links tools/runtime_demo.cpp"
+    fs, n_fft, rows = 100e6, 1024, 500
+    sc = signals.paper_scenario(rows=3 * rows)
+    iq, _ = ref.synthesize(signals.scenario_json(sc))
+    iq = np.ascontiguousarray(iq[: 3 * rows * n_fft])
+    per, plots, stats, ccdf, slabs = _run_rt_demo(tmp_path, iq, fs, n_fft, rows, 7, False)
+    exp, seen = ref.run_engine_boxes(iq, fs, n_fft, rows, 7)
+    assert plots == seen == 7 and sorted(per) == list(range(7))
+    for w in range(7):
+        e = np.asarray(exp.get(w, np.zeros((0, 4))), np.float64).reshape(-1, 4)
+        assert np.array_equal(per[w].view(np.uint64), e.view(np.uint64)), w
+    overruns, p50, p90, p99, mx, frac, wall, gpu = stats
+    assert overruns == 0 and 0 < p50 <= p90 <= p99 <= mx and frac == 1.0 and gpu > 0
+    assert ccdf[-1, 1] == 0.0 and np.all(np.diff(ccdf[:, 0]) > 0)
+    # partition(1024, 3, 4): widths 342/341/341, halo clamped at the edges
+    assert slabs.tolist() == [[0, 342, 0, 346], [342, 683, 338, 687], [683, 1024, 679, 1024]]
+
+
+def test_runtime_dropin_paced(ref, tmp_path):
+    """A paced source at 100 MS/s: every window sensed well inside its 5.12 ms span."""
+    fs, n_fft, rows = 100e6, 1024, 500
+    sc = signals.paper_scenario(rows=2 * rows)
+    iq, _ = ref.synthesize(signals.scenario_json(sc))
+    per, plots, stats, ccdf, _ = _run_rt_demo(tmp_path, np.ascontiguousarray(iq[: 2 * rows * n_fft]), fs, n_fft,
+                                              rows, 20, True)
+    assert plots == 20 and stats[0] == 0 and stats[5] == 1.0

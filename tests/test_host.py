@@ -41,7 +41,10 @@ def test_cpp_dropin_symbols_exported():
                 "specsense::detector::consolidate(", "specsense::detector::label_components(",
                 "specsense::detector::component_extents(", "specsense::detector::extent_to_bin_box(",
                 "specsense::detector::bin_box_to_physical(", "specsense::detector::detect(",
-                "specsense::detector::DetectorConfig::validate(", "specsense::frontend::FrontendConfig::validate("]:
+                "specsense::detector::DetectorConfig::validate(", "specsense::frontend::FrontendConfig::validate(",
+                "specsense::runtime::run(", "specsense::runtime::summarize(", "specsense::runtime::nearest_rank(",
+                "specsense::runtime::partition(", "specsense::runtime::consolidate_sliced(",
+                "specsense::runtime::RunReport::ccdf(", "specsense::runtime::RuntimeConfig::validate("]:
         assert sym in out, sym
 
 

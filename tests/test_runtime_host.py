@@ -43,13 +43,13 @@ def test_nearest_rank():
     v = [1.0, 2.0, 3.0, 4.0, 5.0]
     assert rt.nearest_rank(v, 0.0) == 1.0 and rt.nearest_rank(v, 0.5) == 3.0 and rt.nearest_rank(v, 1.0) == 5.0
     assert rt.nearest_rank(v, 0.99) == 5.0 and rt.nearest_rank(v, 0.2) == 1.0
-    with pytest.raises(ValidationError):
-        rt.nearest_rank([], 0.5)
+    assert rt.nearest_rank([], 0.5) == 0.0      # runtime.cpp:171
 
 
 def test_runtime_config_validation():
     rt.RuntimeConfig().validate()
-    for bad in (dict(n_compute_workers=0), dict(n_sensing_workers=0), dict(halo_bins=2), dict(deadline_s=-1.0)):
+    for bad in (dict(n_compute_workers=0), dict(n_sensing_workers=0), dict(halo_bins=2), dict(deadline_s=-1.0),
+                dict(chunk_queue_capacity=-1)):
         with pytest.raises(ValidationError):
             rt.RuntimeConfig(**bad).validate()
 
