@@ -365,9 +365,17 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     if (c_use[c]) {
         const float clo = c_lo[c], csc = c_scale[c];
         uint32_t* h = hist + c * kHistStride;
-        for (int r = tid >> 3; r < rows; r += kBinThreads / kTileCols) {
-            atomicAdd(h + bin_index(bt_vals[r * kTileCols + c], clo, csc), 1u);
+        constexpr int RS = kBinThreads / kTileCols;  // row stride
+        int r = tid >> 3;
+        // 4 rows per step: the loads and bin math of a step are independent
+        for (; r + 3 * RS < rows; r += 4 * RS) {
+            int b[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) b[q] = bin_index(bt_vals[(r + q * RS) * kTileCols + c], clo, csc);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) atomicAdd(h + b[q], 1u);
         }
+        for (; r < rows; r += RS) atomicAdd(h + bin_index(bt_vals[r * kTileCols + c], clo, csc), 1u);
     }
     __syncthreads();
 
