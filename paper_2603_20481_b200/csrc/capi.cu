@@ -267,7 +267,7 @@ ss_status run_ccl(ss_ctx* ctx, const uint32_t* bits, int n_plots, int rows, int 
     w.dense = dn;
     w.pool_cap = pool_cap;
     SS_CK(ctx, ssb::ccl_launch(L, ctx->stream));
-    ctx->launches += 7 + (rows > 1 ? 1 : 0) + (labels ? 1 : 0);
+    ctx->launches += 7 + (rows > 1 ? 1 : 0) + (rows > 16 ? 1 : 0) + (labels ? 1 : 0);
     if (overflow_host) SS_CK(ctx, cudaMemcpyAsync(overflow_host, of, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     return SS_OK;
 }

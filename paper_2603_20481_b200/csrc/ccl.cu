@@ -10,7 +10,9 @@
 //   5 union   : each run unites with the overlapping runs of the row above
 //               (4-connectivity = shared column, :543-555); lock-free
 //               union-by-min (CAS on roots), so every root is the smallest run
-//               index of its component = its first row-major pixel
+//               index of its component = its first row-major pixel.  First
+//               within 16-row blocks in shared memory, then across the block
+//               boundaries in global memory
 //   6 flatten : parent -> root; area, max_t, min_f, max_f by atomics
 //   7 compact : roots with area >= min_area, numbered densely in root order
 //               (= first-pixel order, area filter before numbering: :570-593)
@@ -26,21 +28,53 @@
 
 namespace ssb {
 
-// Masks are word-major (bits[p][w][r]); one thread walks one row's words,
-// so each warp reads 32 consecutive rows of a word: coalesced.
-__global__ void count_runs_kernel(const uint32_t* __restrict__ bits, int rows, int W, int* row_runs) {
+// Masks are word-major (bits[p][w][r]).  A CTA covers 32 consecutive rows x
+// kSeg word segments: warp k walks segment k of each row (lane = row, so a
+// warp reads 32 consecutive rows of a word: coalesced).  Starts and ends of
+// runs are counted per segment; a run's index is the number of starts before
+// its start bit in the row, its end the number of ends before its end bit,
+// so segments emit independently once their prefix counts are known.
+constexpr int kSeg = 4;
+
+struct SegRange {
+    int w0, w1;
+};
+__device__ __forceinline__ SegRange seg_range(int W, int k) {
+    const int per = (W + kSeg - 1) / kSeg;
+    const int w0 = min(W, k * per);
+    return {w0, min(W, w0 + per)};
+}
+
+// carry into word w0: bit 31 of the row's previous word
+__device__ __forceinline__ uint32_t seg_carry(const uint32_t* col, int rows, int w0) {
+    return w0 > 0 ? (col[static_cast<long long>(w0 - 1) * rows] >> 31) : 0u;
+}
+
+__global__ void __launch_bounds__(32 * kSeg) count_runs_kernel(const uint32_t* __restrict__ bits, int rows, int W,
+                                                               int* row_runs) {
+    __shared__ int cnt_s[kSeg][32];
     const int p = blockIdx.y;
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= rows) return;
-    const uint32_t* col = bits + static_cast<long long>(p) * W * rows + r;
-    uint32_t carry = 0u;
+    const int lane = threadIdx.x & 31, k = threadIdx.x >> 5;
+    const int r = blockIdx.x * 32 + lane;
     int cnt = 0;
-    for (int w = 0; w < W; ++w) {
-        const uint32_t x = col[static_cast<long long>(w) * rows];
-        cnt += __popc(x & ~((x << 1) | carry));
-        carry = x >> 31;
+    if (r < rows) {
+        const uint32_t* col = bits + static_cast<long long>(p) * W * rows + r;
+        const SegRange g = seg_range(W, k);
+        uint32_t carry = seg_carry(col, rows, g.w0);
+        for (int w = g.w0; w < g.w1; ++w) {
+            const uint32_t x = col[static_cast<long long>(w) * rows];
+            cnt += __popc(x & ~((x << 1) | carry));
+            carry = x >> 31;
+        }
     }
-    row_runs[static_cast<long long>(p) * rows + r] = cnt;
+    cnt_s[k][lane] = cnt;
+    __syncthreads();
+    if (k == 0 && r < rows) {
+        int t = 0;
+#pragma unroll
+        for (int q = 0; q < kSeg; ++q) t += cnt_s[q][lane];
+        row_runs[static_cast<long long>(p) * rows + r] = t;
+    }
 }
 
 __global__ void scan_rows_kernel(const int* row_runs, int rows, int* row_off) {
@@ -75,60 +109,121 @@ __global__ void scan_rows_kernel(const int* row_runs, int rows, int* row_off) {
     if (threadIdx.x == 0) out[rows] = carry_s;
 }
 
-__global__ void plot_base_kernel(const int* row_off, int n_plots, int rows, long long pool_cap,
-                                 long long* plot_base, int* plot_ok, int* overflow) {
-    if (threadIdx.x != 0) return;
-    long long acc = 0;
-    int of = 0;
-    for (int p = 0; p < n_plots; ++p) {
-        const long long total = row_off[static_cast<long long>(p) * (rows + 1) + rows];
-        plot_base[p] = acc;
-        const int ok = acc + total <= pool_cap ? 1 : 0;
-        plot_ok[p] = ok;
-        if (ok) acc += total;
-        else of = 1;
+// Pool base of every plot: exclusive prefix of the plots' run totals; a plot
+// whose runs would pass pool_cap is flagged (the host then re-runs every plot
+// alone with an exact pool, capi.cu).  One 1024-thread block, chunked scan.
+__global__ void __launch_bounds__(1024) plot_base_kernel(const int* row_off, int n_plots, int rows, long long pool_cap,
+                                                         long long* plot_base, int* plot_ok, int* overflow) {
+    __shared__ long long red[32];
+    __shared__ long long carry_s;
+    __shared__ int of_s;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        carry_s = 0;
+        of_s = 0;
     }
-    *overflow = of;
+    __syncthreads();
+    for (int c0 = 0; c0 < n_plots; c0 += blockDim.x) {
+        const int p = c0 + threadIdx.x;
+        const long long v = p < n_plots ? row_off[static_cast<long long>(p) * (rows + 1) + rows] : 0;
+        long long inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (l >= o) inc += t;
+        }
+        if (l == 31) red[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            const int nw = blockDim.x >> 5;
+            long long x = l < nw ? red[l] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long t = __shfl_up_sync(0xffffffffu, x, o);
+                if (l >= o) x += t;
+            }
+            if (l < nw) red[l] = x;
+        }
+        __syncthreads();
+        const long long base = carry_s + (w > 0 ? red[w - 1] : 0) + inc - v;
+        if (p < n_plots) {
+            plot_base[p] = base;
+            const int ok = base + v <= pool_cap ? 1 : 0;
+            plot_ok[p] = ok;
+            if (!ok) of_s = 1;
+        }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry_s = base + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *overflow = of_s;
 }
 
 // Runs of one row in column order (start bits x & ~(x<<1|carry), end bits
-// ~x & (x<<1|carry) alternate), appended at the row's offset in the pool.
-__global__ void emit_runs_kernel(const uint32_t* __restrict__ bits, int rows, int cols, const int* row_off,
-                                 const long long* plot_base, const int* plot_ok, CclWorkspace ws) {
+// ~x & (x<<1|carry)), appended at the row's offset in the pool; segment k of
+// the row writes the starts / ends that fall in its words.
+__global__ void __launch_bounds__(32 * kSeg) emit_runs_kernel(const uint32_t* __restrict__ bits, int rows, int cols,
+                                                              const int* row_off, const long long* plot_base,
+                                                              const int* plot_ok, CclWorkspace ws) {
+    __shared__ int st_s[kSeg][32], en_s[kSeg][32];
     const int W = (cols + 31) / 32;
     const int p = blockIdx.y;
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= rows || !plot_ok[p]) return;
+    const int lane = threadIdx.x & 31, k = threadIdx.x >> 5;
+    const int r = blockIdx.x * 32 + lane;
+    const bool live = r < rows && plot_ok[p];
     const uint32_t* col = bits + static_cast<long long>(p) * W * rows + r;
-    long long idx = plot_base[p] + row_off[static_cast<long long>(p) * (rows + 1) + r];
-    uint32_t carry = 0u;
-    int open = -1;
-    auto put = [&](int b, int e) {
-        ws.run_begin[idx] = b;
-        ws.run_end[idx] = e;
-        ws.run_row[idx] = r;
-        ws.parent[idx] = static_cast<int>(idx);
-        ws.area[idx] = 0ull;
-        ws.min_f[idx] = INT_MAX;
-        ws.max_f[idx] = -1;
-        ws.max_t[idx] = -1;
-        ws.dense[idx] = -1;
-        ++idx;
-    };
-    for (int w = 0; w < W; ++w) {
-        const uint32_t x = col[static_cast<long long>(w) * rows];
-        const uint32_t sh = (x << 1) | carry;
-        const uint32_t starts = x & ~sh;
-        uint32_t ev = starts | (~x & sh);
-        carry = x >> 31;
-        while (ev) {
-            const int bpos = __ffs(ev) - 1;
-            ev &= ev - 1;
-            if ((starts >> bpos) & 1u) open = 32 * w + bpos;
-            else put(open, 32 * w + bpos);
+    const SegRange g = seg_range(W, k);
+    int ns = 0, ne = 0;
+    if (live) {
+        uint32_t carry = seg_carry(col, rows, g.w0);
+        for (int w = g.w0; w < g.w1; ++w) {
+            const uint32_t x = col[static_cast<long long>(w) * rows];
+            const uint32_t sh = (x << 1) | carry;
+            ns += __popc(x & ~sh);
+            ne += __popc(~x & sh);
+            carry = x >> 31;
         }
     }
-    if (carry) put(open, cols);  // run reaching the last column (cols % 32 == 0)
+    st_s[k][lane] = ns;
+    en_s[k][lane] = ne;
+    __syncthreads();
+    if (!live) return;
+    int s0 = 0, e0 = 0;
+    for (int q = 0; q < k; ++q) {
+        s0 += st_s[q][lane];
+        e0 += en_s[q][lane];
+    }
+    const long long row0 = plot_base[p] + row_off[static_cast<long long>(p) * (rows + 1) + r];
+    long long si = row0 + s0, ei = row0 + e0;
+    uint32_t carry = seg_carry(col, rows, g.w0);
+    for (int w = g.w0; w < g.w1; ++w) {
+        const uint32_t x = col[static_cast<long long>(w) * rows];
+        const uint32_t sh = (x << 1) | carry;
+        uint32_t starts = x & ~sh, ends = ~x & sh;
+        carry = x >> 31;
+        while (starts) {
+            const int bpos = __ffs(starts) - 1;
+            starts &= starts - 1;
+            ws.run_begin[si] = 32 * w + bpos;
+            ws.run_row[si] = r;
+            ws.parent[si] = static_cast<int>(si);
+            ws.area[si] = 0ull;
+            ws.min_f[si] = INT_MAX;
+            ws.max_f[si] = -1;
+            ws.max_t[si] = -1;
+            ws.dense[si] = -1;
+            ++si;
+        }
+        while (ends) {
+            const int bpos = __ffs(ends) - 1;
+            ends &= ends - 1;
+            ws.run_end[ei++] = 32 * w + bpos;
+        }
+    }
+    if (k == kSeg - 1 || g.w1 == W) {
+        // a run still open after the last word reaches the last column (cols % 32 == 0)
+        if (g.w1 == W && g.w0 < g.w1 && carry) ws.run_end[ei] = cols;
+    }
 }
 
 __device__ __forceinline__ int uf_find(int* parent, int x) {
@@ -167,16 +262,12 @@ __device__ __forceinline__ void uf_unite(int* parent, int a, int b) {
     }
 }
 
-__global__ void union_kernel(int rows, const int* row_off, const long long* plot_base, const int* plot_ok,
-                             CclWorkspace ws) {
-    const int p = blockIdx.y;
-    const int r = blockIdx.x * 8 + (threadIdx.x >> 5) + 1;
-    const int lane = threadIdx.x & 31;
-    if (r >= rows || !plot_ok[p]) return;
-    const int* off = row_off + static_cast<long long>(p) * (rows + 1);
-    const long long base = plot_base[p];
+// Unite the runs of row r with the overlapping runs of row r - 1 (global
+// union-find); lanes stride over the row's runs.
+__device__ __forceinline__ void unite_row_global(int r, const int* off, long long base, CclWorkspace& ws, int lane,
+                                                 int nlanes) {
     const long long prev_b = base + off[r - 1], cur_b = base + off[r], cur_e = base + off[r + 1];
-    for (long long i = cur_b + lane; i < cur_e; i += 32) {
+    for (long long i = cur_b + lane; i < cur_e; i += nlanes) {
         const int b = ws.run_begin[i], e = ws.run_end[i];
         long long lo = prev_b, hi = cur_b;
         while (lo < hi) {
@@ -187,6 +278,97 @@ __global__ void union_kernel(int rows, const int* row_off, const long long* plot
         for (long long q = lo; q < cur_b && ws.run_begin[q] < e; ++q)
             uf_unite(ws.parent, static_cast<int>(i), static_cast<int>(q));
     }
+}
+
+// Shared-memory union-find on local run indices (union-by-min: the root is
+// the smallest index, i.e. the earliest run in row-major order).
+__device__ __forceinline__ int sm_find(int* par, int x) {
+    for (;;) {
+        const int p = par[x];
+        if (p == x) return x;
+        const int gp = par[p];
+        if (gp != p) par[x] = gp;
+        x = p;
+    }
+}
+__device__ __forceinline__ void sm_unite(int* par, int a, int b) {
+    for (;;) {
+        a = sm_find(par, a);
+        b = sm_find(par, b);
+        if (a == b) return;
+        if (a < b) {
+            const int t = a;
+            a = b;
+            b = t;
+        }
+        const int old = atomicCAS(par + a, a, b);
+        if (old == a) return;
+        a = old;
+    }
+}
+
+// Union within blocks of kUB rows: the block's runs (contiguous in the pool)
+// are united in shared memory, then every run's parent is set to its
+// block-local root.  Blocks whose runs exceed kUCap unite in global memory.
+// Rows r0 (a block's first row) are joined to the row above by
+// union_boundary_kernel afterwards.
+constexpr int kUB = 16;
+constexpr int kUCap = 2048;
+
+__global__ void __launch_bounds__(256) union_block_kernel(int rows, const int* row_off, const long long* plot_base,
+                                                          const int* plot_ok, CclWorkspace ws) {
+    __shared__ int sb[kUCap], se[kUCap], sp[kUCap];
+    __shared__ int roff[kUB + 1];
+    const int p = blockIdx.y;
+    const int r0 = blockIdx.x * kUB, r1 = min(rows, r0 + kUB);
+    if (!plot_ok[p] || r0 >= rows) return;
+    const int* off = row_off + static_cast<long long>(p) * (rows + 1);
+    const long long base = plot_base[p];
+    const int g0 = off[r0], n = off[r1] - g0;
+    if (n > kUCap) {  // dense block: rows r0+1 .. r1-1 in global memory, one warp per row
+        for (int r = r0 + 1 + (threadIdx.x >> 5); r < r1; r += blockDim.x >> 5)
+            unite_row_global(r, off, base, ws, threadIdx.x & 31, 32);
+        return;
+    }
+    const long long gb = base + g0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        sb[i] = ws.run_begin[gb + i];
+        se[i] = ws.run_end[gb + i];
+        sp[i] = i;
+    }
+    for (int j = threadIdx.x; j <= r1 - r0; j += blockDim.x) roff[j] = off[r0 + j] - g0;
+    __syncthreads();
+    // one warp per row pair (j-1, j), lanes over row j's runs
+    const int lane = threadIdx.x & 31;
+    for (int j = 1 + (threadIdx.x >> 5); j < r1 - r0; j += blockDim.x >> 5) {
+        const int pb = roff[j - 1], cb = roff[j], ce = roff[j + 1];
+        for (int i = cb + lane; i < ce; i += 32) {
+            const int b = sb[i], e = se[i];
+            int lo = pb, hi = cb;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (se[mid] > b) hi = mid;
+                else lo = mid + 1;
+            }
+            for (int q = lo; q < cb && sb[q] < e; ++q) sm_unite(sp, i, q);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        int x = i;
+        while (sp[x] != x) x = sp[x];
+        ws.parent[gb + i] = static_cast<int>(gb + x);
+    }
+}
+
+// Block boundaries: row k*kUB joins row k*kUB - 1 (global union-find).
+__global__ void union_boundary_kernel(int rows, const int* row_off, const long long* plot_base, const int* plot_ok,
+                                      CclWorkspace ws) {
+    const int p = blockIdx.y;
+    const int r = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5) + 1) * kUB;
+    if (r >= rows || !plot_ok[p]) return;
+    const int* off = row_off + static_cast<long long>(p) * (rows + 1);
+    unite_row_global(r, off, plot_base[p], ws, threadIdx.x & 31, 32);
 }
 
 __global__ void flatten_kernel(int rows, const int* row_off, const long long* plot_base, const int* plot_ok,
@@ -296,15 +478,19 @@ cudaError_t ccl_launch(const CclLaunch& L, cudaStream_t st) {
     if (L.n_plots <= 0 || L.rows <= 0 || L.cols <= 0) return cudaSuccess;
     const int W = (L.cols + 31) / 32;
     const CclWorkspace& ws = L.ws;
-    dim3 tgrid((L.rows + 127) / 128, L.n_plots);
-    count_runs_kernel<<<tgrid, 128, 0, st>>>(L.bits, L.rows, W, ws.row_runs);
+    dim3 tgrid((L.rows + 31) / 32, L.n_plots);
+    count_runs_kernel<<<tgrid, 32 * kSeg, 0, st>>>(L.bits, L.rows, W, ws.row_runs);
     scan_rows_kernel<<<L.n_plots, 1024, 0, st>>>(ws.row_runs, L.rows, ws.row_off);
-    plot_base_kernel<<<1, 32, 0, st>>>(ws.row_off, L.n_plots, L.rows, ws.pool_cap, ws.plot_base, ws.plot_ok,
-                                       ws.overflow);
-    emit_runs_kernel<<<tgrid, 128, 0, st>>>(L.bits, L.rows, L.cols, ws.row_off, ws.plot_base, ws.plot_ok, ws);
+    plot_base_kernel<<<1, 1024, 0, st>>>(ws.row_off, L.n_plots, L.rows, ws.pool_cap, ws.plot_base, ws.plot_ok,
+                                         ws.overflow);
+    emit_runs_kernel<<<tgrid, 32 * kSeg, 0, st>>>(L.bits, L.rows, L.cols, ws.row_off, ws.plot_base, ws.plot_ok, ws);
     if (L.rows > 1) {
-        dim3 ugrid((L.rows - 1 + 7) / 8, L.n_plots);
-        union_kernel<<<ugrid, 256, 0, st>>>(L.rows, ws.row_off, ws.plot_base, ws.plot_ok, ws);
+        const int nblk = (L.rows + kUB - 1) / kUB;
+        union_block_kernel<<<dim3(nblk, L.n_plots), 256, 0, st>>>(L.rows, ws.row_off, ws.plot_base, ws.plot_ok, ws);
+        if (nblk > 1) {
+            dim3 bgrid((nblk - 1 + 7) / 8, L.n_plots);
+            union_boundary_kernel<<<bgrid, 256, 0, st>>>(L.rows, ws.row_off, ws.plot_base, ws.plot_ok, ws);
+        }
     }
     int per_plot = 4096 / (L.n_plots > 0 ? L.n_plots : 1);
     if (per_plot < 2) per_plot = 2;
