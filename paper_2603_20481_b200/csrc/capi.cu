@@ -767,9 +767,11 @@ __global__ void seq_fill_kernel(unsigned long long* seq, int n, unsigned long lo
 
 // K1 (+PSD) and the detector chain on device-resident IQ; `tf` and every
 // non-null pointer in `dev` are device memory.  No host synchronisation.
+// seq_dev: per-plot start sequence numbers already on the device (the
+// engine's graph-captured path), else they are filled from first_seq.
 static ss_status sense_device(ss_ctx* ctx, const void* diq, ss_fmt fmt, int n_fft, int hop, int window, int rows,
                               int n_plots, uint64_t first_seq, double sample_rate_hz, const ss_detector_cfg& cfg,
-                              float* tf, const ss_batch_out& dev) {
+                              float* tf, const ss_batch_out& dev, const unsigned long long* seq_dev = nullptr) {
     const bool stft = hop != n_fft || window != SS_WIN_RECT;
     const int cols = n_fft;
     SS_WS(psd, float, "det.psd", static_cast<size_t>(n_plots) * cols);
@@ -815,10 +817,14 @@ static ss_status sense_device(ss_ctx* ctx, const void* diq, ss_fmt fmt, int n_ff
         tmark(ctx, 1, 1);
         ctx->launches += 1;
     }
-    SS_WS(seq, unsigned long long, "det.seq", n_plots);
-    seq_fill_kernel<<<(n_plots + 255) / 256, 256, 0, ctx->stream>>>(seq, n_plots, first_seq, rows);
-    SS_CK(ctx, cudaGetLastError());
-    ctx->launches += 1;
+    const unsigned long long* seq = seq_dev;
+    if (!seq) {
+        SS_WS(sq, unsigned long long, "det.seq", n_plots);
+        seq_fill_kernel<<<(n_plots + 255) / 256, 256, 0, ctx->stream>>>(sq, n_plots, first_seq, rows);
+        SS_CK(ctx, cudaGetLastError());
+        ctx->launches += 1;
+        seq = sq;
+    }
     return detect_device(ctx, tf, n_plots, rows, cols, seq, sample_rate_hz, cfg, praw, true, dev, hop);
 }
 
@@ -1031,10 +1037,15 @@ ss_status engine_check(ss_ctx* ctx, int n_fft, int rows, ss_fmt fmt, double fs, 
     return check_cfg(ctx, cfg, n_fft);
 }
 
-// one window, device-resident IQ -> device outputs, on the context stream, no host sync
+// one window, device-resident IQ -> device outputs, on the context stream, no
+// host sync; seq_dev (device, 1 value) replaces start_seq when non-null so
+// the launch sequence can be captured once into a CUDA graph per bank
 ss_status engine_sense(ss_ctx* ctx, const void* diq, ss_fmt fmt, int n_fft, int rows, uint64_t start_seq, double fs,
-                       const ss_detector_cfg& cfg, float* tf, const ss_batch_out& dev) {
-    return sense_device(ctx, diq, fmt, n_fft, n_fft, SS_WIN_RECT, rows, 1, start_seq, fs, cfg, tf, dev);
+                       const ss_detector_cfg& cfg, float* tf, const ss_batch_out& dev,
+                       const unsigned long long* seq_dev) {
+    return sense_device(ctx, diq, fmt, n_fft, n_fft, SS_WIN_RECT, rows, 1, start_seq, fs, cfg, tf, dev, seq_dev);
 }
+
+void engine_add_launches(ss_ctx* ctx, int64_t n) { ctx->launches += n; }
 
 } // namespace ssb

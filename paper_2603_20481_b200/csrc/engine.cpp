@@ -42,7 +42,9 @@ ss_status engine_ctx_open(int device, ss_ctx** out);
 cudaStream_t engine_ctx_stream(ss_ctx* ctx);
 ss_status engine_check(ss_ctx* ctx, int n_fft, int rows, ss_fmt fmt, double fs, const ss_detector_cfg& cfg);
 ss_status engine_sense(ss_ctx* ctx, const void* diq, ss_fmt fmt, int n_fft, int rows, uint64_t start_seq, double fs,
-                       const ss_detector_cfg& cfg, float* tf, const ss_batch_out& dev);
+                       const ss_detector_cfg& cfg, float* tf, const ss_batch_out& dev,
+                       const unsigned long long* seq_dev);
+void engine_add_launches(ss_ctx* ctx, int64_t n);
 } // namespace ssb
 
 namespace {
@@ -68,10 +70,18 @@ struct Bank {
     int32_t* n_boxes = nullptr;
     // pinned host record
     struct Host {
+        unsigned long long seq;  // the window's start_seq, copied to d_seq before the graph runs
         int32_t n_boxes;
         int32_t n_active;
         float floor_thr[2];
     }* host = nullptr;
+    unsigned long long* d_seq = nullptr;
+    // pinned host staging for small / pageable pushes: rows [st_lo, st_hi)
+    // are staged, not yet copied; one H2D per kFlushRows rows
+    unsigned char* h_stage = nullptr;
+    int st_lo = 0, st_hi = 0;
+    cudaGraphExec_t graph = nullptr;  // K1..K6 + record D2H of this bank, captured once
+    int64_t graph_launches = 0;
     ss_box* h_boxes = nullptr;
     ss_bin_box* h_bin_boxes = nullptr;
     cudaEvent_t rows_ready = nullptr;
@@ -115,6 +125,12 @@ struct ss_engine {
 };
 
 namespace {
+
+// pushes of at least this many rows from pinned / device memory go straight
+// to HBM; smaller or pageable ones are staged in the bank's pinned buffer and
+// leave in runs of kFlushRows rows (and at window completion)
+constexpr int kDirectRows = 64;
+constexpr int kFlushRows = 64;
 
 ss_status efail(ss_engine* e, ss_status s, const std::string& msg) {
     e->err = msg;
@@ -178,14 +194,10 @@ ss_status launch_window(ss_engine* e, int bi) {
     EN_CK(e, cudaEventRecord(b.rows_ready, e->copy));
     EN_CK(e, cudaStreamWaitEvent(e->compute, b.rows_ready, 0));
     EN_CK(e, cudaEventRecord(b.start_ev, e->compute));
-    const ss_status s = ssb::engine_sense(e->ctx, b.iq, e->cfg.fmt, F, T, b.window * static_cast<uint64_t>(T),
-                                          e->cfg.sample_rate_hz, e->det, b.tf, dev_out(b, K));
-    if (s != SS_OK) return efail(e, s, ss_last_error(e->ctx));
-    EN_CK(e, cudaMemcpyAsync(&b.host->n_boxes, b.n_boxes, sizeof(int32_t), cudaMemcpyDeviceToHost, e->compute));
-    EN_CK(e, cudaMemcpyAsync(&b.host->n_active, b.n_active, sizeof(int32_t), cudaMemcpyDeviceToHost, e->compute));
-    EN_CK(e, cudaMemcpyAsync(b.host->floor_thr, b.floor_thr, 2 * sizeof(float), cudaMemcpyDeviceToHost, e->compute));
-    EN_CK(e, cudaMemcpyAsync(b.h_boxes, b.boxes, sizeof(ss_box) * K, cudaMemcpyDeviceToHost, e->compute));
-    EN_CK(e, cudaMemcpyAsync(b.h_bin_boxes, b.bin_boxes, sizeof(ss_bin_box) * K, cudaMemcpyDeviceToHost, e->compute));
+    b.host->seq = b.window * static_cast<uint64_t>(T);
+    EN_CK(e, cudaMemcpyAsync(b.d_seq, &b.host->seq, sizeof(unsigned long long), cudaMemcpyHostToDevice, e->compute));
+    EN_CK(e, cudaGraphLaunch(b.graph, e->compute));
+    ssb::engine_add_launches(e->ctx, b.graph_launches);
     EN_CK(e, cudaEventRecord(b.done_ev, e->compute));
     b.state = BankState::Busy;
     e->inflight.push_back(bi);
@@ -212,6 +224,7 @@ int claim_bank(ss_engine* e, uint64_t w, std::unique_lock<std::mutex>& lk) {
             b.state = BankState::Filling;
             b.window = w;
             b.rows_in = 0;
+            b.st_lo = b.st_hi = 0;
             e->newest_window = std::max(e->newest_window, w);
             return bi;
         }
@@ -274,6 +287,8 @@ ss_status ss_engine_open(int device, const ss_engine_cfg* cfg, const ss_detector
                   cudaMalloc(&b.bin_boxes, sizeof(ss_bin_box) * K) == cudaSuccess &&
                   cudaMalloc(&b.n_boxes, sizeof(int32_t)) == cudaSuccess &&
                   cudaMallocHost(&b.host, sizeof(Bank::Host)) == cudaSuccess &&
+                  cudaMalloc(&b.d_seq, sizeof(unsigned long long)) == cudaSuccess &&
+                  cudaMallocHost(&b.h_stage, cells * e->sbytes) == cudaSuccess &&
                   cudaMallocHost(&b.h_boxes, sizeof(ss_box) * K) == cudaSuccess &&
                   cudaMallocHost(&b.h_bin_boxes, sizeof(ss_bin_box) * K) == cudaSuccess &&
                   cudaEventCreateWithFlags(&b.rows_ready, cudaEventDisableTiming) == cudaSuccess &&
@@ -284,9 +299,42 @@ ss_status ss_engine_open(int device, const ss_engine_cfg* cfg, const ss_detector
     // twiddles and weights exist before the first real window is timed
     Bank& b0 = e->banks[0];
     if (cudaMemsetAsync(b0.iq, 0, cells * e->sbytes, e->compute) != cudaSuccess) return bad(SS_ECUDA, "memset");
-    s = ssb::engine_sense(e->ctx, b0.iq, cfg->fmt, F, T, 0, cfg->sample_rate_hz, *det, b0.tf, dev_out(b0, K));
+    s = ssb::engine_sense(e->ctx, b0.iq, cfg->fmt, F, T, 0, cfg->sample_rate_hz, *det, b0.tf, dev_out(b0, K), nullptr);
     if (s != SS_OK) return bad(s, ss_last_error(e->ctx));
     if (cudaStreamSynchronize(e->compute) != cudaSuccess) return bad(SS_ECUDA, "warm-up failed");
+    // capture each bank's window chain + record copies once: a window then
+    // costs one H2D of its start_seq and one graph launch on the host
+    for (Bank& b : e->banks) {
+        if (cudaStreamBeginCapture(e->compute, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+            return bad(SS_ECUDA, "graph capture");
+        cudaGraph_t g = nullptr;
+        const ss_status cs = ssb::engine_sense(e->ctx, b.iq, cfg->fmt, F, T, 0, cfg->sample_rate_hz, *det, b.tf,
+                                               dev_out(b, K), b.d_seq);
+        bool ok = cs == SS_OK &&
+                  cudaMemcpyAsync(&b.host->n_boxes, b.n_boxes, sizeof(int32_t), cudaMemcpyDeviceToHost, e->compute) == cudaSuccess &&
+                  cudaMemcpyAsync(&b.host->n_active, b.n_active, sizeof(int32_t), cudaMemcpyDeviceToHost, e->compute) == cudaSuccess &&
+                  cudaMemcpyAsync(b.host->floor_thr, b.floor_thr, 2 * sizeof(float), cudaMemcpyDeviceToHost, e->compute) == cudaSuccess &&
+                  cudaMemcpyAsync(b.h_boxes, b.boxes, sizeof(ss_box) * K, cudaMemcpyDeviceToHost, e->compute) == cudaSuccess &&
+                  cudaMemcpyAsync(b.h_bin_boxes, b.bin_boxes, sizeof(ss_bin_box) * K, cudaMemcpyDeviceToHost, e->compute) == cudaSuccess;
+        const cudaError_t ce = cudaStreamEndCapture(e->compute, &g);
+        if (!ok || ce != cudaSuccess || !g) {
+            if (g) cudaGraphDestroy(g);
+            return bad(cs != SS_OK ? cs : SS_ECUDA, cs != SS_OK ? std::string(ss_last_error(e->ctx)) : "graph capture failed");
+        }
+        size_t nodes = 0;
+        cudaGraphGetNodes(g, nullptr, &nodes);
+        std::vector<cudaGraphNode_t> nv(nodes);
+        cudaGraphGetNodes(g, nv.data(), &nodes);
+        b.graph_launches = 0;
+        for (cudaGraphNode_t nd : nv) {
+            cudaGraphNodeType ty;
+            if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) ++b.graph_launches;
+        }
+        const cudaError_t ie = cudaGraphInstantiate(&b.graph, g, 0);
+        cudaGraphDestroy(g);
+        if (ie != cudaSuccess) return bad(SS_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+    }
+    if (cudaGraphUpload(e->banks[0].graph, e->compute) != cudaSuccess) return bad(SS_ECUDA, "graph upload");
     e->t0 = Clock::now();
     e->waiter = std::thread(waiter_main, e);
     *out = e;
@@ -323,6 +371,9 @@ void ss_engine_close(ss_engine* e) {
         cudaFreeHost(b.h_boxes);
         cudaFreeHost(b.h_bin_boxes);
         if (b.rows_ready) cudaEventDestroy(b.rows_ready);
+        if (b.graph) cudaGraphExecDestroy(b.graph);
+        cudaFreeHost(b.h_stage);
+        cudaFree(b.d_seq);
         if (b.start_ev) cudaEventDestroy(b.start_ev);
         if (b.done_ev) cudaEventDestroy(b.done_ev);
     }
@@ -332,11 +383,27 @@ void ss_engine_close(ss_engine* e) {
 
 const char* ss_engine_last_error(const ss_engine* e) { return e ? e->err.c_str() : "no engine"; }
 
+static ss_status flush_stage(ss_engine* e, Bank& b, size_t row_bytes) {
+    if (b.st_hi > b.st_lo) {
+        const size_t o = static_cast<size_t>(b.st_lo) * row_bytes;
+        EN_CK(e, cudaMemcpyAsync(b.iq + o, b.h_stage + o, static_cast<size_t>(b.st_hi - b.st_lo) * row_bytes,
+                                 cudaMemcpyHostToDevice, e->copy));
+    }
+    b.st_lo = b.st_hi;
+    return SS_OK;
+}
+
 ss_status ss_engine_push(ss_engine* e, const void* samples, int64_t n_chunks, uint64_t first_seq) {
     if (!e || (!samples && n_chunks > 0) || n_chunks < 0) return SS_EVALIDATION;
     const int F = e->cfg.n_fft, T = e->cfg.plot_rows;
     const size_t row_bytes = static_cast<size_t>(F) * e->sbytes;
     const unsigned char* src = static_cast<const unsigned char*>(samples);
+    bool dma_ok = false;  // source is pinned or device memory
+    if (n_chunks >= kDirectRows) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, samples) == cudaSuccess) dma_ok = a.type != cudaMemoryTypeUnregistered;
+        else cudaGetLastError();
+    }
     std::unique_lock<std::mutex> lk(e->mu);
     if (e->finished) return efail(e, SS_EVALIDATION, "push after finish");
     int64_t i = 0;
@@ -350,11 +417,30 @@ ss_status ss_engine_push(ss_engine* e, const void* samples, int64_t n_chunks, ui
         e->rows_retired += static_cast<uint64_t>(run);
         if (bi >= 0) {
             Bank& b = e->banks[static_cast<size_t>(bi)];
-            EN_CK(e, cudaMemcpyAsync(b.iq + static_cast<size_t>(r0) * row_bytes, src + static_cast<size_t>(i) * row_bytes,
-                                     static_cast<size_t>(run) * row_bytes, cudaMemcpyDefault, e->copy));
+            const unsigned char* from = src + static_cast<size_t>(i) * row_bytes;
+            if (dma_ok && run >= kDirectRows) {
+                ss_status s = flush_stage(e, b, row_bytes);
+                if (s != SS_OK) return s;
+                EN_CK(e, cudaMemcpyAsync(b.iq + static_cast<size_t>(r0) * row_bytes, from,
+                                         static_cast<size_t>(run) * row_bytes, cudaMemcpyDefault, e->copy));
+            } else {
+                if (r0 != b.st_hi) {  // not contiguous with the staged run
+                    ss_status s = flush_stage(e, b, row_bytes);
+                    if (s != SS_OK) return s;
+                    b.st_lo = b.st_hi = r0;
+                }
+                std::memcpy(b.h_stage + static_cast<size_t>(r0) * row_bytes, from, static_cast<size_t>(run) * row_bytes);
+                b.st_hi = r0 + static_cast<int>(run);
+                if (b.st_hi - b.st_lo >= kFlushRows) {
+                    ss_status s = flush_stage(e, b, row_bytes);
+                    if (s != SS_OK) return s;
+                }
+            }
             b.rows_in += static_cast<int>(run);
             if (b.rows_in >= T) {
-                const ss_status s = launch_window(e, bi);
+                ss_status s = flush_stage(e, b, row_bytes);
+                if (s != SS_OK) return s;
+                s = launch_window(e, bi);
                 if (s != SS_OK) return s;
             }
         }
