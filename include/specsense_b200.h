@@ -259,6 +259,33 @@ ss_status ss_engine_poll(ss_engine* eng, int wait_ms, ss_plot_record* rec, ss_bo
 ss_status ss_engine_stats(ss_engine* eng, uint64_t* completed, uint64_t* overruns, uint64_t* rows_retired,
                           uint64_t* pending);
 
+/* ---- baseline detector -------------------------------------------------
+   The reference's Searchlight-style comparison detector (baseline::
+   baseline_detect, proj/src/baseline.cpp:103-176): dyadic
+   mean-filter bank over the summed-area table of |x|^2, seeds where a kernel
+   mean exceeds conv_threshold x floor x 10^(offset/10), greedy box growth,
+   merge of overlapping boxes.  SAT and the kernel bank run on the GPU, the
+   sequential greedy walk on the host; results are bit-identical. */
+typedef struct {
+    double conv_threshold;          /* 2.0 */
+    double rate_change_threshold;   /* 0.5 */
+    double noise_offset_db;         /* 3.0 */
+    int max_kernel_rows;            /* 0 = plot height */
+    int max_kernel_cols;            /* 0 = plot width */
+} ss_baseline_cfg;
+
+void ss_default_baseline_cfg(ss_baseline_cfg* cfg);
+/* baseline::kernel_sizes (baseline.cpp:96-101): (kr, kc) pairs into sizes
+   (2*cap ints).  Returns the count; -1 invalid input, -2 cap too small.
+   Host only. */
+int ss_baseline_kernel_sizes(int rows, int cols, const ss_baseline_cfg* cfg, int32_t* sizes, int cap);
+/* baseline::baseline_detect on one rows x cols TF plot (host or device
+   memory); boxes / bin_boxes (HOST, may be NULL) sorted by (t0, f0, t1, f1),
+   at most cap kept, *n_boxes = true count. */
+ss_status ss_baseline_detect(ss_ctx* ctx, const float* tf, int rows, int cols, uint64_t start_seq,
+                             double sample_rate_hz, const ss_baseline_cfg* cfg, ss_box* boxes, ss_bin_box* bin_boxes,
+                             int cap, int* n_boxes);
+
 /* ---- test hooks -------------------------------------------------------- */
 /* Device ports of glibc log10f (which=0) / powf(10, x) (which=1) over n
    DEVICE floats; variant: 1 FMA build, 0 SSE2 build, -1 host-matched. */

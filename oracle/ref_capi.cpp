@@ -12,6 +12,7 @@
 // -2 FormatError, -3 SchemaError, -4 IoError, -5 other specsense::Error,
 // -6 std::exception, -7 capacity too small.
 
+#include "specsense/baseline.hpp"
 #include "specsense/detector.hpp"
 #include "specsense/frontend.hpp"
 #include "specsense/metrics.hpp"
@@ -447,6 +448,48 @@ long long ref_run_engine_boxes(const float* iq, long long n_samples, double fs, 
                                       });
         *plots_seen = rep.plots;
         return overflow ? -7 : nb;
+    });
+}
+
+
+static baseline::BaselineConfig bl_cfg(double conv, double rate, double offset, int mkr, int mkc) {
+    baseline::BaselineConfig c;
+    c.conv_threshold = conv;
+    c.rate_change_threshold = rate;
+    c.noise_offset_db = offset;
+    c.max_kernel_rows = mkr;
+    c.max_kernel_cols = mkc;
+    return c;
+}
+
+// baseline::kernel_sizes -> (kr, kc) pairs; returns the count.
+long long ref_kernel_sizes(int rows, int cols, double conv, double rate, double offset, int mkr, int mkc, int* out,
+                           long long cap) {
+    return guard([&]() -> long long {
+        const auto v = baseline::kernel_sizes(rows, cols, bl_cfg(conv, rate, offset, mkr, mkc));
+        if (static_cast<long long>(v.size()) > cap) return -7;
+        for (std::size_t i = 0; i < v.size(); ++i) {
+            out[2 * i] = v[i].first;
+            out[2 * i + 1] = v[i].second;
+        }
+        return static_cast<long long>(v.size());
+    });
+}
+
+// baseline::baseline_detect on one plot -> boxes (f0, f1, t0, t1); returns the count.
+long long ref_baseline_detect(const float* tf, int rows, int cols, unsigned long long start_seq, double fs, double conv,
+                              double rate, double offset, int mkr, int mkc, double* boxes, long long cap) {
+    return guard([&]() -> long long {
+        frontend::TFPlotView v{tf, rows, cols, start_seq, fs};
+        const auto b = baseline::baseline_detect(v, bl_cfg(conv, rate, offset, mkr, mkc));
+        if (static_cast<long long>(b.size()) > cap) return -7;
+        for (std::size_t i = 0; i < b.size(); ++i) {
+            boxes[4 * i] = b[i].f0_hz;
+            boxes[4 * i + 1] = b[i].f1_hz;
+            boxes[4 * i + 2] = b[i].t0_s;
+            boxes[4 * i + 3] = b[i].t1_s;
+        }
+        return static_cast<long long>(b.size());
     });
 }
 

@@ -39,6 +39,11 @@ class BatchOut(C.Structure):
                 ("bin_boxes", C.c_void_p), ("n_boxes", C.c_void_p), ("box_capacity", C.c_int32)]
 
 
+class BaselineCfg(C.Structure):
+    _fields_ = [("conv_threshold", C.c_double), ("rate_change_threshold", C.c_double), ("noise_offset_db", C.c_double),
+                ("max_kernel_rows", C.c_int), ("max_kernel_cols", C.c_int)]
+
+
 class EngineCfg(C.Structure):
     _fields_ = [("n_fft", C.c_int), ("plot_rows", C.c_int), ("fmt", C.c_int), ("sample_rate_hz", C.c_double),
                 ("n_banks", C.c_int), ("paced", C.c_int), ("deadline_s", C.c_double), ("box_capacity", C.c_int)]
@@ -84,6 +89,10 @@ SIGNATURES = {
     "ss_test_libm": (_I, [_P, _P, C.c_int64, _I, _I, _P]),
     "ss_fft_twiddle_count": (C.c_int64, [_I]),
     "ss_fft_twiddles": (_I, [_I, _P]),
+    "ss_default_baseline_cfg": (None, [C.POINTER(BaselineCfg)]),
+    "ss_baseline_kernel_sizes": (_I, [_I, _I, C.POINTER(BaselineCfg), _P, _I]),
+    "ss_baseline_detect": (_I, [_P, _P, _I, _I, C.c_uint64, C.c_double, C.POINTER(BaselineCfg), _P, _P, _I,
+                                C.POINTER(_I)]),
     "ss_engine_open": (_I, [_I, C.POINTER(EngineCfg), C.POINTER(DetectorCfg), C.POINTER(_P)]),
     "ss_engine_close": (None, [_P]),
     "ss_engine_last_error": (C.c_char_p, [_P]),

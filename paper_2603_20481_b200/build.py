@@ -28,9 +28,9 @@ NVCC_FLAGS = EXTRA + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "
 CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra",
              f"-I{ROOT / 'include'}", f"-I{CSRC}", "-I/usr/local/cuda/include"]
 
-CU = ["fft_mag.cu", "floor.cu", "binarize.cu", "morph.cu", "ccl.cu", "capi.cu"]
-CPP = ["host_consts.cpp", "dropin.cpp", "engine.cpp", "runtime_dropin.cpp"]
-HEADERS = ["common.cuh", "internal.h", "glibc_libm.cuh"]
+CU = ["fft_mag.cu", "floor.cu", "binarize.cu", "morph.cu", "ccl.cu", "baseline.cu", "capi.cu"]
+CPP = ["host_consts.cpp", "dropin.cpp", "engine.cpp", "runtime_dropin.cpp", "baseline_host.cpp"]
+HEADERS = ["common.cuh", "internal.h", "glibc_libm.cuh", "baseline_host.h"]
 
 
 def _deps_mtime() -> float:

@@ -3,6 +3,7 @@
 // semantics, and the fused batch pipelines that chain K1..K6 on one stream.
 #include "../../include/specsense_b200.h"
 #include "internal.h"
+#include "baseline_host.h"
 
 #include <algorithm>
 #include <cmath>
@@ -988,6 +989,126 @@ static ss_status sense_impl(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, 
         SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
         tcollect(ctx);
     }
+    return SS_OK;
+}
+
+void ss_default_baseline_cfg(ss_baseline_cfg* cfg) {
+    if (!cfg) return;
+    cfg->conv_threshold = 2.0;
+    cfg->rate_change_threshold = 0.5;
+    cfg->noise_offset_db = 3.0;
+    cfg->max_kernel_rows = 0;
+    cfg->max_kernel_cols = 0;
+}
+
+static const char* baseline_cfg_error(const ss_baseline_cfg& c) {
+    if (!(c.conv_threshold > 0.0)) return "conv_threshold must be > 0";
+    if (!(c.rate_change_threshold > 0.0)) return "rate_change_threshold must be > 0";
+    if (c.max_kernel_rows < 0 || c.max_kernel_cols < 0) return "kernel caps must be >= 0";
+    return nullptr;
+}
+
+static std::vector<int32_t> baseline_sizes(int rows, int cols, const ss_baseline_cfg& c) {
+    const int rcap = c.max_kernel_rows > 0 ? std::min(c.max_kernel_rows, rows) : rows;
+    const int ccap = c.max_kernel_cols > 0 ? std::min(c.max_kernel_cols, cols) : cols;
+    std::vector<int32_t> v;
+    for (int kr = 1; kr <= rcap; kr *= 2)
+        for (int kc = 1; kc <= ccap; kc *= 2) {
+            v.push_back(kr);
+            v.push_back(kc);
+        }
+    return v;
+}
+
+int ss_baseline_kernel_sizes(int rows, int cols, const ss_baseline_cfg* cfg, int32_t* sizes, int cap) {
+    if (!cfg || baseline_cfg_error(*cfg) || rows < 1 || cols < 1) return -1;
+    const std::vector<int32_t> v = baseline_sizes(rows, cols, *cfg);
+    const int n = static_cast<int>(v.size() / 2);
+    if (n > cap) return -2;
+    if (sizes) std::memcpy(sizes, v.data(), sizeof(int32_t) * v.size());
+    return n;
+}
+
+ss_status ss_baseline_detect(ss_ctx* ctx, const float* tf, int rows, int cols, uint64_t start_seq,
+                             double sample_rate_hz, const ss_baseline_cfg* cfg, ss_box* boxes, ss_bin_box* bin_boxes,
+                             int cap, int* n_boxes) {
+    if (!ctx || !tf || !cfg || !n_boxes) return SS_EVALIDATION;
+    if (const char* m = baseline_cfg_error(*cfg)) return fail(ctx, SS_EVALIDATION, m);
+    if (rows < 1 || cols < 1) return fail(ctx, SS_EVALIDATION, "plot must be non-empty");
+    if (!(sample_rate_hz > 0.0)) return fail(ctx, SS_EVALIDATION, "sample_rate_hz must be positive");
+    ss_detector_cfg dc;
+    ss_default_detector_cfg(&dc);  // the baseline's floor uses the default DetectorConfig (baseline.cpp:110-115)
+    ss_status s = check_cfg(ctx, dc, cols);
+    if (s != SS_OK) return s;
+    const size_t cells = static_cast<size_t>(rows) * cols;
+    const float* dtf = tf;
+    if (!is_device_ptr(tf)) {
+        SS_WS(st, float, "bl.tf", cells);
+        SS_CK(ctx, cudaMemcpyAsync(st, tf, sizeof(float) * cells, cudaMemcpyHostToDevice, ctx->stream));
+        dtf = st;
+    }
+    // PSD + smooth_and_floor (noise floor), as detect's stages
+    SS_WS(psd, float, "bl.psd", cols);
+    SS_CK(ctx, ssb::psd_cols_launch(dtf, 1, rows, cols, 0, cols, psd, ctx->stream));
+    const double* wts = nullptr;
+    s = weights(ctx, dc.savgol_window, dc.savgol_order, &wts);
+    if (s != SS_OK) return s;
+    const int W = (cols + 31) / 32;
+    SS_WS(sm, float, "bl.sm", cols);
+    SS_WS(ft, float, "bl.ft", 2);
+    SS_WS(act, int, "bl.act", cols);
+    SS_WS(nact, int, "bl.nact", 1);
+    SS_WS(abits, uint32_t, "bl.abits", W);
+    ssb::FloorLaunch F;
+    F.raw = psd;
+    F.n_plots = 1;
+    F.n = cols;
+    F.window = dc.savgol_window;
+    F.weights = wts;
+    F.pow10_margin = std::pow(10.0, dc.psd_margin_db / 10.0);
+    F.fma_variant = ctx->fma_variant;
+    F.smoothed = sm;
+    F.floor_thr = ft;
+    F.active = act;
+    F.n_active = nact;
+    F.active_bits = abits;
+    SS_CK(ctx, ssb::floor_launch(F, ctx->stream));
+    // summed-area table and the kernel bank's candidate bitmaps
+    SS_WS(racc, double, "bl.racc", cells);
+    SS_WS(sat, double, "bl.sat", static_cast<size_t>(rows + 1) * (cols + 1));
+    SS_CK(ctx, ssb::baseline_sat_launch(dtf, rows, cols, racc, sat, ctx->stream));
+    const std::vector<int32_t> sizes = baseline_sizes(rows, cols, *cfg);
+    const int K = static_cast<int>(sizes.size() / 2);
+    SS_WS(dsizes, int32_t, "bl.sizes", sizes.size());
+    SS_CK(ctx, cudaMemcpyAsync(dsizes, sizes.data(), sizeof(int32_t) * sizes.size(), cudaMemcpyHostToDevice, ctx->stream));
+    const size_t nbits = static_cast<size_t>(K) * rows * W;
+    SS_WS(cand, uint32_t, "bl.cand", nbits);
+    const double p10 = std::pow(10.0, cfg->noise_offset_db / 10.0);  // baseline.cpp:117 (host libm, config only)
+    SS_CK(ctx, ssb::baseline_cand_launch(sat, rows, cols, dsizes, K, ft, p10, cfg->conv_threshold, cand, ctx->stream));
+    ctx->launches += 6;
+    std::vector<double> hsat(static_cast<size_t>(rows + 1) * (cols + 1));
+    std::vector<uint32_t> hcand(nbits);
+    SS_CK(ctx, cudaMemcpyAsync(hsat.data(), sat, sizeof(double) * hsat.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    SS_CK(ctx, cudaMemcpyAsync(hcand.data(), cand, sizeof(uint32_t) * nbits, cudaMemcpyDeviceToHost, ctx->stream));
+    SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    const std::vector<ssb::BaselineRect> rects =
+        ssb::baseline_greedy(hsat.data(), hcand.data(), sizes.data(), K, rows, cols, cfg->rate_change_threshold);
+    *n_boxes = static_cast<int>(rects.size());
+    const double dt = static_cast<double>(cols) / sample_rate_hz;  // TFPlotView::dt_s / df_hz
+    const double df = sample_rate_hz / static_cast<double>(cols);
+    const int keep = std::min(static_cast<int>(rects.size()), std::max(cap, 0));
+    for (int i = 0; i < keep; ++i) {
+        const ssb::BaselineRect& r = rects[static_cast<size_t>(i)];
+        if (bin_boxes) bin_boxes[i] = ss_bin_box{r.t0, r.t1, r.f0, r.f1};
+        if (boxes) {
+            ss_box& b = boxes[i];
+            b.t0_s = (static_cast<double>(start_seq) + r.t0) * dt;
+            b.t1_s = (static_cast<double>(start_seq) + r.t1) * dt;
+            b.f0_hz = (r.f0 - cols / 2) * df;
+            b.f1_hz = (r.f1 - cols / 2) * df;
+        }
+    }
+    if (static_cast<int>(rects.size()) > cap) return fail(ctx, SS_ECAPACITY, "box capacity too small: " + std::to_string(rects.size()));
     return SS_OK;
 }
 

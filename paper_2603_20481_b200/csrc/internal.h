@@ -131,4 +131,9 @@ struct CclLaunch {
 };
 cudaError_t ccl_launch(const CclLaunch& L, cudaStream_t st);
 
+// ---- baseline.cu (F3: Searchlight-style baseline)
+cudaError_t baseline_sat_launch(const float* tf, int rows, int cols, double* racc, double* sat, cudaStream_t st);
+cudaError_t baseline_cand_launch(const double* sat, int rows, int cols, const int* sizes, int n_sizes,
+                                 const float* noise_floor, double p10, double conv, uint32_t* bits, cudaStream_t st);
+
 } // namespace ssb

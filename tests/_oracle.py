@@ -68,6 +68,9 @@ class _Ref:
                                _f64p],
             "ref_summarize": [_ll, C.POINTER(C.c_ulonglong), _f64p, _i32p, C.c_ulonglong, C.c_double, _f64p,
                               _f64p, _ll],
+            "ref_kernel_sizes": [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, _i32p, _ll],
+            "ref_baseline_detect": [_f32p, C.c_int, C.c_int, C.c_ulonglong, C.c_double, C.c_double, C.c_double,
+                                    C.c_double, C.c_int, C.c_int, _f64p, _ll],
             "ref_run_engine_boxes": [_f32p, _ll, C.c_double, C.c_int, C.c_int, _ll, C.c_int, C.c_int,
                                      C.POINTER(C.c_ulonglong), _f64p, _ll, C.POINTER(C.c_ulonglong)],
         }
@@ -232,6 +235,19 @@ class _Ref:
         keys = ["plots", "overruns", "deadline_s", "fraction_met", "realtime_met", "p50_s", "p90_s", "p99_s",
                 "max_s", "percentiles_valid"]
         return dict(zip(keys, stats.tolist())), [tuple(x) for x in cc[: 2 * k].reshape(-1, 2).tolist()]
+
+    def kernel_sizes(self, rows, cols, conv=2.0, rate=0.5, offset=3.0, mkr=0, mkc=0):
+        out = np.zeros(2 * 4096, np.int32)
+        n = self._chk(self.L.ref_kernel_sizes(rows, cols, conv, rate, offset, mkr, mkc, out, 4096))
+        return out[: 2 * n].reshape(-1, 2)
+
+    def baseline_detect(self, tf, start_seq=0, fs=1e6, conv=2.0, rate=0.5, offset=3.0, mkr=0, mkc=0, cap=1 << 16):
+        tf = np.ascontiguousarray(tf, np.float32)
+        rows, cols = tf.shape
+        boxes = np.zeros(4 * cap, np.float64)
+        n = self._chk(self.L.ref_baseline_detect(tf.reshape(-1), rows, cols, start_seq, fs, conv, rate, offset, mkr,
+                                                 mkc, boxes, cap))
+        return boxes[: 4 * n].reshape(-1, 4)
 
     def run_engine_boxes(self, samples, fs, n_fft, rows, n_plots, n_compute=2, n_sensing=4, cap=1 << 16):
         """The reference engine (runtime::run, unpaced MemorySource) -> {plot_index: boxes (n,4)}."""
