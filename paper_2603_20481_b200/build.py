@@ -29,7 +29,7 @@ CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextr
              f"-I{ROOT / 'include'}", f"-I{CSRC}", "-I/usr/local/cuda/include"]
 
 CU = ["fft_mag.cu", "floor.cu", "binarize.cu", "morph.cu", "ccl.cu", "baseline.cu", "capi.cu"]
-CPP = ["host_consts.cpp", "dropin.cpp", "engine.cpp", "runtime_dropin.cpp", "baseline_host.cpp"]
+CPP = ["host_consts.cpp", "dropin.cpp", "engine.cpp", "runtime_dropin.cpp", "baseline_host.cpp", "baseline_dropin.cpp"]
 HEADERS = ["common.cuh", "internal.h", "glibc_libm.cuh", "baseline_host.h"]
 
 

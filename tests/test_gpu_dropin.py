@@ -125,3 +125,37 @@ def test_runtime_dropin_paced(ref, tmp_path):
     per, plots, stats, ccdf, _ = _run_rt_demo(tmp_path, np.ascontiguousarray(iq[: 2 * rows * n_fft]), fs, n_fft,
                                               rows, 20, True)
     assert plots == 20 and stats[0] == 0 and stats[5] == 1.0
+
+
+BL_DEMO = ROOT / "paper_2603_20481_b200" / "_lib" / "baseline_demo"
+
+
+def test_baseline_dropin_matches_reference(ref, tmp_path):
+    """specsense::baseline / metrics through the C++ drop-in vs the reference."""
+    assert BL_DEMO.exists(), "build() links tools/baseline_demo.cpp"
+    sc = signals.paper_scenario(rows=500)
+    iq, truth = ref.synthesize(signals.scenario_json(sc))
+    fs, rows, cols = 100e6, 500, 1024
+    tf = ref.make_plots(iq, fs, cols, rows)[0]
+    (tmp_path / "tf.f32").write_bytes(tf.astype(np.float32).tobytes())
+    span = rows * cols / fs
+    gt = np.array([[b[0], b[1], max(b[2], 0.0), min(b[3], span)] for b in truth if b[2] < span], np.float64)
+    (tmp_path / "gt.f64").write_bytes(gt.tobytes())
+    out = tmp_path / "bl.bin"
+    subprocess.run([str(BL_DEMO), str(tmp_path / "tf.f32"), str(rows), str(cols), str(fs), "0",
+                    str(tmp_path / "gt.f64"), str(out)], check=True, timeout=120)
+    r = Reader(out.read_bytes())
+    nk = r.one(np.int32)
+    assert np.array_equal(r.take(np.int32, 2 * nk).reshape(-1, 2), ref.kernel_sizes(rows, cols))
+    nb = r.one(np.int32)
+    got = r.take(np.float64, 4 * nb).reshape(-1, 4)
+    exp = ref.baseline_detect(tf, 0, fs)
+    assert np.array_equal(got.view(np.uint64), exp.view(np.uint64))
+    pipe = r.take(np.float64, 4)
+    base = r.take(np.float64, 4)
+    speedup = r.one(np.float64)
+    assert pipe[0] > 0 and base[0] > 0 and speedup > 0 and 0 <= pipe[1] <= 1 and 0 <= base[1] <= 1
+    from paper_2603_20481_b200 import metrics
+    ev = metrics.evaluate(gt, exp, theta=0.3)
+    assert np.array_equal(r.take(np.float64, 4), np.array([ev.n_true, ev.n_false, ev.p_fa, ev.mean_iou]))
+    assert r.one(np.int32) == 1

@@ -44,7 +44,12 @@ def test_cpp_dropin_symbols_exported():
                 "specsense::detector::DetectorConfig::validate(", "specsense::frontend::FrontendConfig::validate(",
                 "specsense::runtime::run(", "specsense::runtime::summarize(", "specsense::runtime::nearest_rank(",
                 "specsense::runtime::partition(", "specsense::runtime::consolidate_sliced(",
-                "specsense::runtime::RunReport::ccdf(", "specsense::runtime::RuntimeConfig::validate("]:
+                "specsense::runtime::RunReport::ccdf(", "specsense::runtime::RuntimeConfig::validate(",
+                "specsense::baseline::baseline_detect(", "specsense::baseline::kernel_sizes(",
+                "specsense::baseline::compare(", "specsense::baseline::make_compare_row(",
+                "specsense::baseline::BaselineConfig::validate(", "specsense::metrics::iou(",
+                "specsense::metrics::iou_matrix(", "specsense::metrics::count_matches(", "specsense::metrics::evaluate(",
+                "specsense::metrics::sweep("]:
         assert sym in out, sym
 
 
