@@ -302,11 +302,53 @@ __global__ void __launch_bounds__(kPsdTileRows) psd_tile_kernel(const float* __r
     }
 }
 
+// Batch form: one warp per 32-column stripe of a plot (lane = column, every
+// row read is one 128-byte line), 16 rows of loads in flight per lane, then
+// the 16 sums in row order.  No shared memory, no barriers: with enough
+// plots there are far more column chains than the FP64 pipe needs, so the
+// kernel streams the TF plot at HBM rate.
+constexpr int kPsdStripeRows = 16;
+
+__global__ void __launch_bounds__(256) psd_stripe_kernel(const float* __restrict__ tf, int n_plots, int rows, int cols,
+                                                         int c0, int c1, int stripes, float* __restrict__ out) {
+    const long long gw = blockIdx.x * 8LL + (threadIdx.x >> 5);  // global warp = (plot, stripe)
+    const int p = static_cast<int>(gw / stripes), sidx = static_cast<int>(gw % stripes);
+    const int c = c0 + sidx * 32 + (threadIdx.x & 31);
+    if (p >= n_plots || c >= c1) return;
+    const float* base = tf + static_cast<long long>(p) * rows * cols + c;
+    double acc = 0.0;
+    int r = 0;
+    for (; r + kPsdStripeRows <= rows; r += kPsdStripeRows) {
+        float x[kPsdStripeRows];
+#pragma unroll
+        for (int q = 0; q < kPsdStripeRows; ++q) x[q] = __ldcs(base + static_cast<long long>(r + q) * cols);
+#pragma unroll
+        for (int q = 0; q < kPsdStripeRows; ++q) {
+            const double d = static_cast<double>(x[q]);
+            acc = __fma_rn(d, d, acc);
+        }
+    }
+    for (; r < rows; ++r) {
+        const double d = static_cast<double>(__ldcs(base + static_cast<long long>(r) * cols));
+        acc = __fma_rn(d, d, acc);
+    }
+    const double inv = __ddiv_rn(1.0, static_cast<double>(rows));
+    out[static_cast<long long>(p) * (c1 - c0) + (c - c0)] = __double2float_rn(__dmul_rn(acc, inv));
+}
+
 cudaError_t psd_cols_launch(const float* tf, int n_plots, int rows, int cols, int c0, int c1,
                             float* out, cudaStream_t st) {
     const int w = c1 - c0;
     if (w <= 0 || n_plots <= 0) return cudaSuccess;
     const bool aligned = reinterpret_cast<uintptr_t>(tf) % 16 == 0 && cols % 4 == 0 && c0 % 4 == 0;
+    // enough column chains to keep every SM's FP64 pipe busy: warp stripes
+    if (static_cast<long long>(n_plots) * w >= 148LL * 512) {
+        const int stripes = (w + 31) / 32;
+        const long long warps = static_cast<long long>(stripes) * n_plots;
+        psd_stripe_kernel<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, st>>>(tf, n_plots, rows, cols, c0, c1,
+                                                                                  stripes, out);
+        return cudaGetLastError();
+    }
     if (aligned && w % kPsdTileCols == 0) {
         dim3 grid(w / kPsdTileCols, n_plots);
         psd_tile_kernel<<<grid, kPsdTileRows, 0, st>>>(tf, rows, cols, c0, c1, out);
