@@ -195,3 +195,36 @@ def test_host_input_pipeline_matches_device(ss, hop, window, rows):
         assert np.array_equal(got["bins"][p][:k], d.bin_boxes)
         assert np.array_equal(got["boxes"][p][:k], d.boxes)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("n_fft,rows", [(8192, 60), (32, 700), (64, 1), (2048, 3), (1024, 6200)])
+def test_size_edges(ss, ref, n_fft, rows):
+    """Extreme geometries through the fused pipeline vs the reference: the largest
+    device FFT, the smallest F the default window accepts, single-row plots,
+    and a plot taller than the K4 tile limit (generic binarize path)."""
+    rng = np.random.default_rng(n_fft + rows)
+    n = 2 * rows * n_fft
+    x = (rng.normal(size=n) + 1j * rng.normal(size=n)).astype(np.complex64)
+    # a strong band in the second half of each plot so components exist
+    for p in range(2):
+        s0 = (p * rows + rows // 2) * n_fft
+        t = np.arange(s0, s0 + max(1, rows // 3) * n_fft)
+        x[t] += (8 * np.exp(2j * np.pi * 0.2 * t)).astype(np.complex64)
+    fs = 1e6
+    dets, tf = ss.sense(x, fs, n_fft, rows, return_tf=True, box_capacity=4096)
+    exp_tf = ref.make_plots(x, fs, n_fft, rows)
+    assert len(dets) == len(exp_tf) == 2
+    for p, det in enumerate(dets):
+        _check(det, ref.detect(exp_tf[p], start_seq=p * rows, fs=fs), tf[p], exp_tf[p])
+
+
+def test_all_zero_and_constant_plots(ss, ref):
+    """Degenerate spectra: zero input (PSD 0 -> -3000 dB floor path) and a pure
+    tone (constant columns -> invalid Otsu scale)."""
+    n_fft, rows = 256, 64
+    z = np.zeros(rows * n_fft, np.complex64)
+    tone = np.exp(2j * np.pi * 0.25 * np.arange(rows * n_fft)).astype(np.complex64)
+    for x in (z, tone):
+        dets, tf = ss.sense(x, 1e6, n_fft, rows, return_tf=True)
+        exp_tf = ref.make_plots(x, 1e6, n_fft, rows)
+        _check(dets[0], ref.detect(exp_tf[0], fs=1e6), tf[0], exp_tf[0])
