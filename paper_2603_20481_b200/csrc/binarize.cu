@@ -16,6 +16,10 @@
 #include "common.cuh"
 #include "internal.h"
 
+#include <cooperative_groups.h>
+
+namespace cg = cooperative_groups;
+
 namespace ssb {
 
 constexpr int kBinThreads = 256;
@@ -283,28 +287,38 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
 
+// NSPLIT = 2: a 2-CTA cluster shares one column group, each CTA holding half
+// of the rows (tall plots, e.g. the 4881-row Hann STFT, keep 2 CTAs per SM);
+// column extremes and histograms are combined through distributed shared
+// memory, and both CTAs run the same Otsu on the summed histograms.
+template <int NSPLIT>
 __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaunch a) {
-    extern __shared__ __align__(16) float bt_vals[];      // rows x 8
+    extern __shared__ __align__(16) float bt_vals[];      // (rows / NSPLIT) x 8
     __shared__ uint32_t hist[kTileCols * kHistStride];
     __shared__ float s_lo[kBinWarps][kTileCols], s_hi[kBinWarps][kTileCols];
+    __shared__ float part_lo[kTileCols], part_hi[kTileCols];
     __shared__ float c_lo[kTileCols], c_scale[kTileCols], c_thr[kTileCols];
     __shared__ double c_span[kTileCols];
     __shared__ int c_use[kTileCols];
 
-    const int grp = blockIdx.x;          // 8-column group
+    const int grp = blockIdx.x / NSPLIT;  // 8-column group
+    const int rank = NSPLIT == 1 ? 0 : static_cast<int>(cg::this_cluster().block_rank());
     const int p = blockIdx.y;
-    const int rows = a.rows, cols = a.cols;
+    const int rows_all = a.rows, cols = a.cols;
+    const int half = (rows_all + NSPLIT - 1) / NSPLIT;
+    const int rbase = rank * half;
+    const int rows = max(0, min(rows_all, rbase + half) - rbase);  // this CTA's rows
     const int W = (cols + 31) / 32;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t abyte = (a.active_bits[static_cast<long long>(p) * W + grp / 4] >> (8 * (grp & 3))) & 0xffu;
-    uint8_t* plane = a.mask_planes + (static_cast<long long>(p) * (cols / kTileCols) + grp) * rows;
+    uint8_t* plane = a.mask_planes + (static_cast<long long>(p) * (cols / kTileCols) + grp) * rows_all + rbase;
     const int col0 = grp * kTileCols;
-    if (abyte == 0) {
+    if (abyte == 0) {  // both CTAs of a cluster see the same byte and leave together
         for (int r = tid; r < rows; r += kBinThreads) plane[r] = 0;
         return;
     }
-    // ---- load the T x 8 block (2 x 16 B per row)
-    const float* src = a.tf + static_cast<long long>(p) * rows * cols + col0;
+    // ---- load the block (2 x 16 B per row)
+    const float* src = a.tf + (static_cast<long long>(p) * rows_all + rbase) * cols + col0;
     for (int e = tid; e < 2 * rows; e += kBinThreads) {
         const int r = e >> 1, h = e & 1;
         cp_async16(bt_vals + r * kTileCols + 4 * h, src + static_cast<long long>(r) * cols + 4 * h);
@@ -344,11 +358,37 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
         }
     }
     __syncthreads();
+    if constexpr (NSPLIT > 1) {
+        if (tid < kTileCols) {
+            float l = s_lo[0][tid], h = s_hi[0][tid];
+            for (int q = 1; q < kBinWarps; ++q) {
+                l = fminf(l, s_lo[q][tid]);
+                h = fmaxf(h, s_hi[q][tid]);
+            }
+            part_lo[tid] = l;
+            part_hi[tid] = h;
+        }
+        cg::this_cluster().sync();
+    }
     if (tid < kTileCols) {
-        float l = s_lo[0][tid], h = s_hi[0][tid];
-        for (int q = 1; q < kBinWarps; ++q) {
-            l = fminf(l, s_lo[q][tid]);
-            h = fmaxf(h, s_hi[q][tid]);
+        float l, h;
+        if constexpr (NSPLIT > 1) {
+            // min / max are order-free: every CTA of the cluster derives the same extremes
+            cg::cluster_group cl = cg::this_cluster();
+            l = part_lo[tid];
+            h = part_hi[tid];
+            for (int q = 0; q < NSPLIT; ++q) {
+                if (q == rank) continue;
+                l = fminf(l, *cl.map_shared_rank(&part_lo[tid], q));
+                h = fmaxf(h, *cl.map_shared_rank(&part_hi[tid], q));
+            }
+        } else {
+            l = s_lo[0][tid];
+            h = s_hi[0][tid];
+            for (int q = 1; q < kBinWarps; ++q) {
+                l = fminf(l, s_lo[q][tid]);
+                h = fmaxf(h, s_hi[q][tid]);
+            }
         }
         const float scale = __fdiv_rn(256.0f, __fsub_rn(h, l));
         const bool valid = h > l && isfinite(scale);
@@ -379,12 +419,22 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     }
     __syncthreads();
 
+    if constexpr (NSPLIT > 1) cg::this_cluster().sync();  // every partial histogram complete
     // ---- Otsu: warp w handles column w
     if (warp < kTileCols && c_use[warp]) {
         const int cc = warp;
         uint32_t hq[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) hq[q] = hist[cc * kHistStride + lane * 8 + q];
+        if constexpr (NSPLIT > 1) {
+            cg::cluster_group cl = cg::this_cluster();
+            for (int o = 0; o < NSPLIT; ++o) {
+                if (o == rank) continue;
+                const uint32_t* rh = cl.map_shared_rank(hist, o);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) hq[q] += rh[cc * kHistStride + lane * 8 + q];
+            }
+        }
         const int best_i = otsu_split_warp(hq, lane);
         if (lane == 0) {
             const double lod = static_cast<double>(c_lo[cc]);
@@ -393,7 +443,9 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
         }
     }
     __syncthreads();
-    if (a.col_thr && tid < kTileCols && col0 + tid < cols)
+    // no CTA may leave while a partner still reads its histogram
+    if constexpr (NSPLIT > 1) cg::this_cluster().sync();
+    if (a.col_thr && tid < kTileCols && col0 + tid < cols && rank == 0)
         a.col_thr[static_cast<long long>(p) * cols + col0 + tid] = c_thr[tid];
 
     // ---- sweep C: one row per thread, 8 compares -> one mask byte
@@ -410,20 +462,43 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     }
 }
 
-bool binarize_tile_ok(int rows, int cols) { return cols % 32 == 0 && rows <= kTileMaxRows && rows > 0; }
+// one CTA per column group while its block leaves room for 2 CTAs per SM,
+// else a 2-CTA cluster per group (rows split in halves)
+constexpr int kTileSplitRows = 3264;
+
+bool binarize_tile_ok(int rows, int cols) { return cols % 32 == 0 && rows <= 2 * kTileMaxRows && rows > 0; }
 
 cudaError_t binarize_tile_launch(const BinarizeLaunch& L, cudaStream_t st) {
-    const size_t smem = sizeof(float) * kTileCols * static_cast<size_t>(L.rows);
-    static int attr_set = 0;
-    if (attr_set < static_cast<int>(smem)) {
-        cudaError_t e = cudaFuncSetAttribute(binarize_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kTileCols * kTileMaxRows * static_cast<int>(sizeof(float)));
+    const int split = L.rows > kTileSplitRows ? 2 : 1;
+    const int rows_cta = (L.rows + split - 1) / split;
+    const size_t smem = sizeof(float) * kTileCols * static_cast<size_t>(rows_cta);
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[split - 1]) {
+        cudaError_t e = split == 1 ? cudaFuncSetAttribute(binarize_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                          kTileCols * kTileMaxRows * static_cast<int>(sizeof(float)))
+                                   : cudaFuncSetAttribute(binarize_tile_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                          kTileCols * kTileMaxRows * static_cast<int>(sizeof(float)));
         if (e != cudaSuccess) return e;
-        attr_set = kTileCols * kTileMaxRows * static_cast<int>(sizeof(float));
+        attr_set[split - 1] = true;
     }
-    dim3 grid(L.cols / kTileCols, L.n_plots);
-    binarize_tile_kernel<<<grid, kBinThreads, smem, st>>>(L);
-    return cudaGetLastError();
+    if (split == 1) {
+        dim3 grid(L.cols / kTileCols, L.n_plots);
+        binarize_tile_kernel<1><<<grid, kBinThreads, smem, st>>>(L);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * (L.cols / kTileCols), L.n_plots);
+    cfg.blockDim = dim3(kBinThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, binarize_tile_kernel<2>, L);
 }
 
 } // namespace ssb
