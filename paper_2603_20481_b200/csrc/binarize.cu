@@ -311,10 +311,12 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     const int W = (cols + 31) / 32;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t abyte = (a.active_bits[static_cast<long long>(p) * W + grp / 4] >> (8 * (grp & 3))) & 0xffu;
-    uint8_t* plane = a.mask_planes + (static_cast<long long>(p) * (cols / kTileCols) + grp) * rows_all + rbase;
+    // byte (grp & 3) of the word-major mask words (grp >> 2, r): the tile path
+    // writes the packed mask K5 reads, 4 bytes apart per row
+    uint8_t* plane = a.mask_planes + ((static_cast<long long>(p) * W + (grp >> 2)) * rows_all + rbase) * 4 + (grp & 3);
     const int col0 = grp * kTileCols;
     if (abyte == 0) {  // both CTAs of a cluster see the same byte and leave together
-        for (int r = tid; r < rows; r += kBinThreads) plane[r] = 0;
+        for (int r = tid; r < rows; r += kBinThreads) plane[4 * r] = 0;
         return;
     }
     // ---- load the block (2 x 16 B per row)
@@ -458,7 +460,7 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
         const uint32_t b = (x0.x > thr[0] ? 1u : 0u) | (x0.y > thr[1] ? 2u : 0u) | (x0.z > thr[2] ? 4u : 0u) |
                            (x0.w > thr[3] ? 8u : 0u) | (x1.x > thr[4] ? 16u : 0u) | (x1.y > thr[5] ? 32u : 0u) |
                            (x1.z > thr[6] ? 64u : 0u) | (x1.w > thr[7] ? 128u : 0u);
-        plane[r] = static_cast<uint8_t>(b);
+        plane[4 * r] = static_cast<uint8_t>(b);
     }
 }
 

@@ -325,14 +325,13 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
     B.cols = cols;
     B.active_bits = abits;
     const bool planes = ssb::binarize_tile_ok(rows, cols);
-    if (planes) B.mask_planes = reinterpret_cast<uint8_t*>(m0);  // same byte count as the bit mask
+    if (planes) B.mask_planes = reinterpret_cast<uint8_t*>(m0);  // the bit mask, written bytewise
     else B.mask_bits = m0;
     tmark(ctx, 3, 0);
     SS_CK(ctx, ssb::binarize_launch(B, ctx->stream));
     tmark(ctx, 3, 1);
     tmark(ctx, 4, 0);
-    SS_CK(ctx, ssb::consolidate_bits_launch(planes ? nullptr : m0, planes ? reinterpret_cast<uint8_t*>(m0) : nullptr,
-                                            n_plots, rows, cols, cfg.one_d_opening_along_time != 0, m1, ctx->stream));
+    SS_CK(ctx, ssb::consolidate_bits_launch(m0, n_plots, rows, cols, cfg.one_d_opening_along_time != 0, m1, ctx->stream));
     tmark(ctx, 4, 1);
     ctx->launches += 3;
     const long long cap = out_dev.box_capacity > 0 ? out_dev.box_capacity : 0;
@@ -684,7 +683,7 @@ ss_status ss_consolidate(ss_ctx* ctx, const uint8_t* src, int rows, int cols, in
     SS_WS(a, uint32_t, "cons.a", static_cast<size_t>(rows) * W);
     SS_WS(b, uint32_t, "cons.b", static_cast<size_t>(rows) * W);
     SS_CK(ctx, ssb::pack_u8_launch(src, 1, rows, cols, a, ctx->stream));
-    SS_CK(ctx, ssb::consolidate_bits_launch(a, nullptr, 1, rows, cols, along_time != 0, b, ctx->stream));
+    SS_CK(ctx, ssb::consolidate_bits_launch(a, 1, rows, cols, along_time != 0, b, ctx->stream));
     SS_CK(ctx, ssb::unpack_launch(b, 1, rows, cols, dst, ctx->stream));
     ctx->launches += 3;
     return SS_OK;

@@ -69,7 +69,7 @@ struct BinarizeLaunch {
     int cols = 0;
     const uint32_t* active_bits = nullptr;  // n_plots x W
     uint32_t* mask_bits = nullptr;      // n_plots x W x rows word-major bits (bit mode) or null
-    uint8_t* mask_planes = nullptr;     // n_plots x (cols/8) x rows byte planes (tile path) or null
+    uint8_t* mask_planes = nullptr;     // tile path: the word-major bit mask as bytes (byte k of word w = columns 32w+8k..+7) or null
     uint8_t* mask_u8 = nullptr;         // rows x cols (u8 mode, columns [c0,c1)) or null
     int c0 = 0, c1 = 0;                 // u8 mode column range
     float* col_thr = nullptr;           // optional n_plots x cols thresholds (+inf inactive)
@@ -87,7 +87,7 @@ cudaError_t unpack_launch(const uint32_t* bits, int n_plots, int rows, int cols,
 // close 3x3 -> open 3x3 -> open 1x3 (3x1 if along_time), bit-packed, fused.
 // Input: row-major bit words `in`, or (when in_planes != null) the byte planes
 // [p][cols/8][rows] the binarize tile kernel writes.
-cudaError_t consolidate_bits_launch(const uint32_t* in, const uint8_t* in_planes, int n_plots, int rows,
+cudaError_t consolidate_bits_launch(const uint32_t* in, int n_plots, int rows,
                                     int cols, bool along_time, uint32_t* out, cudaStream_t st);
 // Generic single-plot u8 morphology of columns [c0, c1) (stage API): op 0 erode,
 // 1 dilate, 2 open, 3 close; tmp: rows x cols scratch.

@@ -8,23 +8,12 @@
 // rows (coalesced global access, conflict-free shared access).
 //
 // consolidate_kernel fuses the whole chain close3x3 -> open3x3 -> open1x3
-// (3x1 when one_d_opening_along_time) in shared memory: one CTA owns a tile of
-// 64 buffer rows (56 output rows + 4 halo rows each side; 52 + 6 for the
-// vertical line) across all W words, column-major in smem (a[w][i]), and
-// applies the six erode/dilate steps as separable vertical (row AND/OR) and
-// horizontal (shift/carry AND/OR across neighbouring words) passes.  Outside
-// the image counts as background for erosion and dilation alike (:359-362,
-// :393-410): out-of-image rows are re-zeroed after every step and bits past
-// the last column are masked, so each step sees the reference's clipped
-// neighbourhood.  The two buffer edge rows are never recomputed; the invalid
-// band grows one row per vertical step and the halo absorbs it.
+// (3x1 when one_d_opening_along_time) in registers (see below).
 #include "common.cuh"
 #include "internal.h"
 
 namespace ssb {
 
-constexpr int kMorphThreads = 256;
-constexpr int kTileNR = 64;  // buffer rows per CTA (a power of two: thread -> (word, row) is shifts)
 
 // byte mask [p][rows][cols] -> word-major bits [p][W][rows]
 __global__ void pack_u8_kernel(const uint8_t* __restrict__ m, int rows, int cols, uint32_t* __restrict__ bits) {
@@ -75,129 +64,101 @@ cudaError_t unpack_launch(const uint32_t* bits, int n_plots, int rows, int cols,
 }
 
 // ------------------------------------------------------------- fused chain
+// Register-resident form: a warp owns a band of kRegRows output rows x 30
+// mask words.  Lane l holds word (band*30 + l - 1) for kRegNR = kRegRows +
+// 2*kRegHalo consecutive rows in registers; lanes 0 and 31 are halo words.
+// Vertical erode/dilate is register-to-register (rows i-1, i, i+1 of the same
+// lane), horizontal is shift/carry with the neighbouring lanes' words
+// (__shfl_up/down).  The six steps move information at most 6 rows and 6
+// columns, so the halo rows / words absorb the invalid band: no shared
+// memory, no barriers.  Out-of-image rows and words are zeroed and the last
+// word masked after every step (out-of-image = background for erode and
+// dilate, detector.cpp:359-362, 393-410).
+constexpr int kRegRows = 32;
+constexpr int kRegHalo = 8;  // >= 6: the largest vertical reach (3x3 close + open + 3x1 line)
+constexpr int kRegNR = kRegRows + 2 * kRegHalo;
+constexpr int kRegOwn = 30;  // owned words per warp
 
-struct MTile {
-    uint32_t* a;       // [W][kTileNR] current image (column-major)
-    uint32_t* b;       // [W][kTileNR] scratch
-    int W;
-    uint32_t last_mask;
-    int out_top, out_bot;  // buffer rows [0,out_top) and [out_bot,kTileNR) lie outside the image
+struct RegBand {
+    uint32_t x[kRegNR];
+    int lo, hi;        // buffer rows [lo, hi) lie inside the image
+    uint32_t wmask;    // 0 outside the image's words; last word: valid columns only
 
-    // every thread visits (w, i) for i in [1, NR-1): e = w*NR + i
-    __device__ __forceinline__ void vpass(bool erode) const {
-        for (int e = threadIdx.x; e < W * kTileNR; e += kMorphThreads) {
-            const int i = e & (kTileNR - 1);
-            if (i == 0 || i == kTileNR - 1) continue;
-            const uint32_t u = a[e - 1], c = a[e], d = a[e + 1];
-            b[e] = erode ? (u & c & d) : (u | c | d);
+    __device__ __forceinline__ void clip() {
+#pragma unroll
+        for (int i = 0; i < kRegNR; ++i) x[i] = (i >= lo && i < hi) ? (x[i] & wmask) : 0u;
+    }
+    __device__ __forceinline__ void vert(bool erode) {
+        uint32_t prev = x[0];
+#pragma unroll
+        for (int i = 1; i < kRegNR - 1; ++i) {
+            const uint32_t cur = x[i];
+            x[i] = erode ? (prev & cur & x[i + 1]) : (prev | cur | x[i + 1]);
+            prev = cur;
         }
     }
-    __device__ __forceinline__ void hpass(const uint32_t* src, uint32_t* dst, bool erode) const {
-        for (int e = threadIdx.x; e < W * kTileNR; e += kMorphThreads) {
-            const int w = e >> 6;  // kTileNR == 64
-            const uint32_t x = src[e];
-            const uint32_t prev = w > 0 ? src[e - kTileNR] : 0u;
-            const uint32_t next = w + 1 < W ? src[e + kTileNR] : 0u;
-            const uint32_t left = (x << 1) | (prev >> 31);   // column c-1 at bit c
-            const uint32_t right = (x >> 1) | (next << 31);  // column c+1 at bit c
-            uint32_t y = erode ? (x & left & right) : (x | left | right);
-            if (w == W - 1) y &= last_mask;
-            dst[e] = y;
+    __device__ __forceinline__ void horiz(bool erode) {
+#pragma unroll
+        for (int i = 0; i < kRegNR; ++i) {
+            const uint32_t v = x[i];
+            const uint32_t prev = __shfl_up_sync(0xffffffffu, v, 1);    // word w-1 (lane 0: its own, halo)
+            const uint32_t next = __shfl_down_sync(0xffffffffu, v, 1);  // word w+1 (lane 31: its own, halo)
+            const uint32_t left = (v << 1) | (prev >> 31);
+            const uint32_t right = (v >> 1) | (next << 31);
+            x[i] = erode ? (v & left & right) : (v | left | right);
         }
     }
-    __device__ __forceinline__ void clip() const {
-        if (out_top == 0 && out_bot == kTileNR) return;
-        for (int e = threadIdx.x; e < W * kTileNR; e += kMorphThreads) {
-            const int i = e & (kTileNR - 1);
-            if (i < out_top || i >= out_bot) a[e] = 0u;
-        }
-    }
-    // one erosion / dilation: 3x3 (vert && horiz), 3x1 (vert), 1x3 (horiz)
-    __device__ __forceinline__ void step(bool erode, bool vert, bool horiz) {
-        if (vert) {
-            vpass(erode);
-            __syncthreads();
-            if (horiz) {
-                hpass(b, a, erode);
-            } else {
-                uint32_t* t = a;  // result is in b (edge rows: stale, invalid anyway)
-                a = b;
-                b = t;
-            }
-        } else {
-            hpass(a, b, erode);
-            uint32_t* t = a;
-            a = b;
-            b = t;
-        }
-        __syncthreads();
+    // one erosion / dilation: 3x3 (vert then horiz), 3x1 (vert), 1x3 (horiz)
+    __device__ __forceinline__ void step(bool erode, bool v, bool h) {
+        if (v) vert(erode);
+        if (h) horiz(erode);
         clip();
-        __syncthreads();
     }
 };
 
-// in_bits: word-major bits [p][W][rows], or in_planes: byte planes [p][4W][rows].
-__global__ void __launch_bounds__(kMorphThreads)
-consolidate_kernel(const uint32_t* __restrict__ in_bits, const uint8_t* __restrict__ in_planes, int rows, int cols,
-                   int halo, bool along_time, uint32_t* __restrict__ out) {
-    extern __shared__ uint32_t mo_smem[];
+// in/out: word-major bits [p][W][rows].  One warp per (row band, word band).
+__global__ void __launch_bounds__(128) consolidate_kernel(const uint32_t* __restrict__ in, int rows, int cols,
+                                                          int wbands, long long bands, bool along_time,
+                                                          uint32_t* __restrict__ out) {
     const int W = (cols + 31) / 32;
+    const int lane = threadIdx.x & 31;
+    const long long gwarp = blockIdx.x * 4LL + (threadIdx.x >> 5);
+    if (gwarp >= bands) return;  // uniform per warp
     const int p = blockIdx.y;
-    const int tile_rows = kTileNR - 2 * halo;
-    const int r0 = blockIdx.x * tile_rows;
-    const int row0 = r0 - halo;  // global row of buffer row 0
-    MTile t;
-    t.W = W;
-    t.a = mo_smem;
-    t.b = mo_smem + W * kTileNR;
-    t.last_mask = (cols & 31) ? ((1u << (cols & 31)) - 1u) : 0xffffffffu;
-    t.out_top = row0 < 0 ? -row0 : 0;
-    t.out_bot = rows - row0 < kTileNR ? rows - row0 : kTileNR;
-    for (int e = threadIdx.x; e < W * kTileNR; e += kMorphThreads) {
-        const int w = e >> 6, i = e & (kTileNR - 1);
-        const int g = row0 + i;
-        uint32_t word = 0u;
-        if (g >= 0 && g < rows) {
-            if (in_planes) {
-                const uint8_t* bp = in_planes + (static_cast<long long>(p) * 4 * W + 4 * w) * rows + g;
-                word = static_cast<uint32_t>(bp[0]) | (static_cast<uint32_t>(bp[rows]) << 8) |
-                       (static_cast<uint32_t>(bp[2 * static_cast<long long>(rows)]) << 16) |
-                       (static_cast<uint32_t>(bp[3 * static_cast<long long>(rows)]) << 24);
-            } else {
-                word = in_bits[(static_cast<long long>(p) * W + w) * rows + g];
-            }
-        }
-        t.a[e] = word;
-    }
-    __syncthreads();
+    const int rb = static_cast<int>(gwarp / wbands), wb = static_cast<int>(gwarp % wbands);
+    const int r0 = rb * kRegRows, row0 = r0 - kRegHalo;
+    const int gw = wb * kRegOwn + lane - 1;
+    const bool wvalid = gw >= 0 && gw < W;
+    RegBand t;
+    t.lo = max(0, -row0);
+    t.hi = min(kRegNR, rows - row0);
+    t.wmask = !wvalid ? 0u : ((gw == W - 1 && (cols & 31)) ? ((1u << (cols & 31)) - 1u) : 0xffffffffu);
+    const uint32_t* src = in + (static_cast<long long>(p) * W + (wvalid ? gw : 0)) * rows + row0;
+#pragma unroll
+    for (int i = 0; i < kRegNR; ++i) t.x[i] = (wvalid && i >= t.lo && i < t.hi) ? __ldg(src + i) : 0u;
+    t.clip();
     t.step(false, true, true);  // close 3x3: dilate, erode
     t.step(true, true, true);
     t.step(true, true, true);   // open 3x3: erode, dilate
     t.step(false, true, true);
     t.step(true, along_time, !along_time);  // open with the line element
     t.step(false, along_time, !along_time);
-    const int nrow = min(tile_rows, rows - r0);
-    for (int e = threadIdx.x; e < W * kTileNR; e += kMorphThreads) {
-        const int w = e >> 6, i = e & (kTileNR - 1);
-        if (i >= halo && i < halo + nrow) out[(static_cast<long long>(p) * W + w) * rows + r0 + (i - halo)] = t.a[e];
-    }
+    if (!wvalid || lane == 0 || lane == 31) return;
+    uint32_t* dst = out + (static_cast<long long>(p) * W + gw) * rows + r0;
+    const int nrow = min(kRegRows, rows - r0);
+#pragma unroll
+    for (int i = 0; i < kRegRows; ++i)
+        if (i < nrow) dst[i] = t.x[kRegHalo + i];
 }
 
-cudaError_t consolidate_bits_launch(const uint32_t* in, const uint8_t* planes, int n_plots, int rows, int cols,
-                                    bool along_time, uint32_t* out, cudaStream_t st) {
+cudaError_t consolidate_bits_launch(const uint32_t* in, int n_plots, int rows, int cols, bool along_time,
+                                    uint32_t* out, cudaStream_t st) {
     if (n_plots <= 0 || rows <= 0 || cols <= 0) return cudaSuccess;
     const int W = (cols + 31) / 32;
-    const int halo = along_time ? 6 : 4;
-    const int tile_rows = kTileNR - 2 * halo;
-    const size_t smem = sizeof(uint32_t) * 2 * static_cast<size_t>(W) * kTileNR;
-    if (smem > 227 * 1024) return cudaErrorInvalidValue;  // cols > 14,000: not on the device path
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(consolidate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-    }
-    dim3 grid((rows + tile_rows - 1) / tile_rows, n_plots);
-    consolidate_kernel<<<grid, kMorphThreads, smem, st>>>(in, planes, rows, cols, halo, along_time, out);
+    const int wbands = (W + kRegOwn - 1) / kRegOwn;
+    const long long bands = static_cast<long long>((rows + kRegRows - 1) / kRegRows) * wbands;
+    dim3 grid(static_cast<unsigned>((bands + 3) / 4), n_plots);
+    consolidate_kernel<<<grid, 128, 0, st>>>(in, rows, cols, wbands, bands, along_time, out);
     return cudaGetLastError();
 }
 
