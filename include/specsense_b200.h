@@ -198,8 +198,11 @@ ss_status ss_stft_sense_batch(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft
    GPU form of the reference's real-time engine (runtime::run,
    proj/src/runtime.cpp:221-487, with frontend::PingPongBuffer,
    proj/include/specsense/frontend.hpp:86-135): F-sample chunks with a
-   sequence number stream into HBM banks; window w = seq / T fills bank
-   w % n_banks; when its T rows are in, the whole window runs K1..K6 on the
+   sequence number stream into HBM banks; window w (T frames: samples
+   [w*T*hop, w*T*hop + (T-1)*hop + F), i.e. chunks w*T .. w*T+T-1 for the
+   reference's hop = F) fills bank w % n_banks (a chunk straddling two
+   overlapping STFT windows goes to both); when its samples are in, the
+   whole window runs K1..K6 on the
    engine's stream and its boxes land in pinned host memory.  A bank stays
    held until its record is polled (the reference releases after the
    detection handler).  Rows for a window whose bank is still held are
@@ -218,8 +221,10 @@ typedef struct {
     double sample_rate_hz;
     int n_banks;           /* >= 2; 2 = the reference's ping-pong */
     int paced;             /* 1: shed windows (overruns); 0: push blocks */
-    double deadline_s;     /* <= 0: the plot span T*F/fs */
+    double deadline_s;     /* <= 0: the plot span T*hop/fs */
     int box_capacity;      /* boxes kept per plot */
+    int hop;               /* STFT extension: frame step in samples (0: n_fft, the reference's frames) */
+    int window;            /* STFT extension: ss_window (0: rectangular) */
 } ss_engine_cfg;
 
 /* runtime::PlotRecord (proj/include/specsense/runtime.hpp:62-69) + extras */

@@ -1160,10 +1160,14 @@ ss_status engine_check(ss_ctx* ctx, int n_fft, int rows, ss_fmt fmt, double fs, 
 // one window, device-resident IQ -> device outputs, on the context stream, no
 // host sync; seq_dev (device, 1 value) replaces start_seq when non-null so
 // the launch sequence can be captured once into a CUDA graph per bank
-ss_status engine_sense(ss_ctx* ctx, const void* diq, ss_fmt fmt, int n_fft, int rows, uint64_t start_seq, double fs,
-                       const ss_detector_cfg& cfg, float* tf, const ss_batch_out& dev,
+ss_status engine_sense(ss_ctx* ctx, const void* diq, ss_fmt fmt, int n_fft, int hop, int window, int rows,
+                       uint64_t start_seq, double fs, const ss_detector_cfg& cfg, float* tf, const ss_batch_out& dev,
                        const unsigned long long* seq_dev) {
-    return sense_device(ctx, diq, fmt, n_fft, n_fft, SS_WIN_RECT, rows, 1, start_seq, fs, cfg, tf, dev, seq_dev);
+    return sense_device(ctx, diq, fmt, n_fft, hop, window, rows, 1, start_seq, fs, cfg, tf, dev, seq_dev);
+}
+
+ss_status engine_check_stft(ss_ctx* ctx, int n_fft, int hop, int window, ss_fmt fmt) {
+    return check_stft(ctx, n_fft, hop, window, fmt);
 }
 
 void engine_add_launches(ss_ctx* ctx, int64_t n) { ctx->launches += n; }

@@ -41,9 +41,10 @@ namespace ssb {
 ss_status engine_ctx_open(int device, ss_ctx** out);
 cudaStream_t engine_ctx_stream(ss_ctx* ctx);
 ss_status engine_check(ss_ctx* ctx, int n_fft, int rows, ss_fmt fmt, double fs, const ss_detector_cfg& cfg);
-ss_status engine_sense(ss_ctx* ctx, const void* diq, ss_fmt fmt, int n_fft, int rows, uint64_t start_seq, double fs,
-                       const ss_detector_cfg& cfg, float* tf, const ss_batch_out& dev,
+ss_status engine_sense(ss_ctx* ctx, const void* diq, ss_fmt fmt, int n_fft, int hop, int window, int rows,
+                       uint64_t start_seq, double fs, const ss_detector_cfg& cfg, float* tf, const ss_batch_out& dev,
                        const unsigned long long* seq_dev);
+ss_status engine_check_stft(ss_ctx* ctx, int n_fft, int hop, int window, ss_fmt fmt);
 void engine_add_launches(ss_ctx* ctx, int64_t n);
 } // namespace ssb
 
@@ -56,7 +57,7 @@ enum class BankState { Free, Filling, Busy };
 struct Bank {
     BankState state = BankState::Free;
     uint64_t window = 0;
-    int rows_in = 0;
+    uint64_t samples_in = 0;  // of the window's span
     // device
     unsigned char* iq = nullptr;
     float* tf = nullptr;
@@ -76,10 +77,10 @@ struct Bank {
         float floor_thr[2];
     }* host = nullptr;
     unsigned long long* d_seq = nullptr;
-    // pinned host staging for small / pageable pushes: rows [st_lo, st_hi)
-    // are staged, not yet copied; one H2D per kFlushRows rows
+    // pinned host staging for small / pageable pushes: window samples
+    // [st_lo, st_hi) are staged, not yet copied; one H2D per kFlushRows chunks
     unsigned char* h_stage = nullptr;
-    int st_lo = 0, st_hi = 0;
+    uint64_t st_lo = 0, st_hi = 0;
     cudaGraphExec_t graph = nullptr;  // K1..K6 + record D2H of this bank, captured once
     int64_t graph_launches = 0;
     ss_box* h_boxes = nullptr;
@@ -103,6 +104,8 @@ struct ss_engine {
     int device = 0;
     size_t sbytes = 8;
     double deadline_s = 0.0;
+    int hop = 0, window = 0;
+    uint64_t stride = 0, span = 0;  // samples between window starts; samples per window
     Clock::time_point t0{};
     std::vector<Bank> banks;
 
@@ -189,7 +192,7 @@ ss_batch_out dev_out(const Bank& b, int cap) {
 // Window of bank b is complete: launch its sensing.  Called with mu held.
 ss_status launch_window(ss_engine* e, int bi) {
     Bank& b = e->banks[static_cast<size_t>(bi)];
-    const int F = e->cfg.n_fft, T = e->cfg.plot_rows, K = e->cfg.box_capacity;
+    const int T = e->cfg.plot_rows;
     b.complete_at = Clock::now();
     EN_CK(e, cudaEventRecord(b.rows_ready, e->copy));
     EN_CK(e, cudaStreamWaitEvent(e->compute, b.rows_ready, 0));
@@ -223,7 +226,7 @@ int claim_bank(ss_engine* e, uint64_t w, std::unique_lock<std::mutex>& lk) {
         if (b.state == BankState::Free) {
             b.state = BankState::Filling;
             b.window = w;
-            b.rows_in = 0;
+            b.samples_in = 0;
             b.st_lo = b.st_hi = 0;
             e->newest_window = std::max(e->newest_window, w);
             return bi;
@@ -270,14 +273,21 @@ ss_status ss_engine_open(int device, const ss_engine_cfg* cfg, const ss_detector
     if (e->cfg.n_banks < 2) return bad(SS_EVALIDATION, "n_banks must be >= 2");
     if (cfg->deadline_s < 0.0) return bad(SS_EVALIDATION, "deadline_s must be >= 0");
     const int F = cfg->n_fft, T = cfg->plot_rows, K = e->cfg.box_capacity;
+    e->hop = cfg->hop > 0 ? cfg->hop : F;
+    e->window = cfg->window;
+    s = ssb::engine_check_stft(e->ctx, F, e->hop, e->window, cfg->fmt);
+    if (s != SS_OK) return bad(s, ss_last_error(e->ctx));
     e->sbytes = cfg->fmt == SS_FMT_F32 ? 8 : 4;
-    e->deadline_s = cfg->deadline_s > 0.0 ? cfg->deadline_s : static_cast<double>(T) * F / cfg->sample_rate_hz;
+    e->stride = static_cast<uint64_t>(T) * e->hop;
+    e->span = static_cast<uint64_t>(T - 1) * e->hop + F;
+    e->deadline_s = cfg->deadline_s > 0.0 ? cfg->deadline_s : static_cast<double>(e->stride) / cfg->sample_rate_hz;
     e->compute = ssb::engine_ctx_stream(e->ctx);
     if (cudaStreamCreateWithFlags(&e->copy, cudaStreamNonBlocking) != cudaSuccess) return bad(SS_ECUDA, "copy stream");
     e->banks.resize(static_cast<size_t>(e->cfg.n_banks));
-    const size_t cells = static_cast<size_t>(T) * F;
+    const size_t cells = static_cast<size_t>(T) * F;  // TF plot
+    const size_t iq_n = static_cast<size_t>(e->span);  // IQ samples per window
     for (Bank& b : e->banks) {
-        bool ok = cudaMalloc(&b.iq, cells * e->sbytes) == cudaSuccess && cudaMalloc(&b.tf, cells * sizeof(float)) == cudaSuccess &&
+        bool ok = cudaMalloc(&b.iq, iq_n * e->sbytes) == cudaSuccess && cudaMalloc(&b.tf, cells * sizeof(float)) == cudaSuccess &&
                   cudaMalloc(&b.psd_raw, sizeof(float) * F) == cudaSuccess &&
                   cudaMalloc(&b.psd_smoothed, sizeof(float) * F) == cudaSuccess &&
                   cudaMalloc(&b.floor_thr, sizeof(float) * 2) == cudaSuccess &&
@@ -288,7 +298,7 @@ ss_status ss_engine_open(int device, const ss_engine_cfg* cfg, const ss_detector
                   cudaMalloc(&b.n_boxes, sizeof(int32_t)) == cudaSuccess &&
                   cudaMallocHost(&b.host, sizeof(Bank::Host)) == cudaSuccess &&
                   cudaMalloc(&b.d_seq, sizeof(unsigned long long)) == cudaSuccess &&
-                  cudaMallocHost(&b.h_stage, cells * e->sbytes) == cudaSuccess &&
+                  cudaMallocHost(&b.h_stage, iq_n * e->sbytes) == cudaSuccess &&
                   cudaMallocHost(&b.h_boxes, sizeof(ss_box) * K) == cudaSuccess &&
                   cudaMallocHost(&b.h_bin_boxes, sizeof(ss_bin_box) * K) == cudaSuccess &&
                   cudaEventCreateWithFlags(&b.rows_ready, cudaEventDisableTiming) == cudaSuccess &&
@@ -298,8 +308,9 @@ ss_status ss_engine_open(int device, const ss_engine_cfg* cfg, const ss_detector
     // warm-up: one window of zeros through the whole chain, so workspace,
     // twiddles and weights exist before the first real window is timed
     Bank& b0 = e->banks[0];
-    if (cudaMemsetAsync(b0.iq, 0, cells * e->sbytes, e->compute) != cudaSuccess) return bad(SS_ECUDA, "memset");
-    s = ssb::engine_sense(e->ctx, b0.iq, cfg->fmt, F, T, 0, cfg->sample_rate_hz, *det, b0.tf, dev_out(b0, K), nullptr);
+    if (cudaMemsetAsync(b0.iq, 0, iq_n * e->sbytes, e->compute) != cudaSuccess) return bad(SS_ECUDA, "memset");
+    s = ssb::engine_sense(e->ctx, b0.iq, cfg->fmt, F, e->hop, e->window, T, 0, cfg->sample_rate_hz, *det, b0.tf,
+                          dev_out(b0, K), nullptr);
     if (s != SS_OK) return bad(s, ss_last_error(e->ctx));
     if (cudaStreamSynchronize(e->compute) != cudaSuccess) return bad(SS_ECUDA, "warm-up failed");
     // capture each bank's window chain + record copies once: a window then
@@ -308,8 +319,8 @@ ss_status ss_engine_open(int device, const ss_engine_cfg* cfg, const ss_detector
         if (cudaStreamBeginCapture(e->compute, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
             return bad(SS_ECUDA, "graph capture");
         cudaGraph_t g = nullptr;
-        const ss_status cs = ssb::engine_sense(e->ctx, b.iq, cfg->fmt, F, T, 0, cfg->sample_rate_hz, *det, b.tf,
-                                               dev_out(b, K), b.d_seq);
+        const ss_status cs = ssb::engine_sense(e->ctx, b.iq, cfg->fmt, F, e->hop, e->window, T, 0, cfg->sample_rate_hz,
+                                               *det, b.tf, dev_out(b, K), b.d_seq);
         bool ok = cs == SS_OK &&
                   cudaMemcpyAsync(&b.host->n_boxes, b.n_boxes, sizeof(int32_t), cudaMemcpyDeviceToHost, e->compute) == cudaSuccess &&
                   cudaMemcpyAsync(&b.host->n_active, b.n_active, sizeof(int32_t), cudaMemcpyDeviceToHost, e->compute) == cudaSuccess &&
@@ -383,20 +394,26 @@ void ss_engine_close(ss_engine* e) {
 
 const char* ss_engine_last_error(const ss_engine* e) { return e ? e->err.c_str() : "no engine"; }
 
-static ss_status flush_stage(ss_engine* e, Bank& b, size_t row_bytes) {
+static ss_status flush_stage(ss_engine* e, Bank& b) {
     if (b.st_hi > b.st_lo) {
-        const size_t o = static_cast<size_t>(b.st_lo) * row_bytes;
-        EN_CK(e, cudaMemcpyAsync(b.iq + o, b.h_stage + o, static_cast<size_t>(b.st_hi - b.st_lo) * row_bytes,
+        const size_t o = static_cast<size_t>(b.st_lo) * e->sbytes;
+        EN_CK(e, cudaMemcpyAsync(b.iq + o, b.h_stage + o, static_cast<size_t>(b.st_hi - b.st_lo) * e->sbytes,
                                  cudaMemcpyHostToDevice, e->copy));
     }
     b.st_lo = b.st_hi;
     return SS_OK;
 }
 
+// Windows whose sample span meets the sample range [a0, a1).
+static void windows_of(const ss_engine* e, uint64_t a0, uint64_t a1, uint64_t* w_lo, uint64_t* w_hi) {
+    *w_lo = a0 >= e->span ? (a0 - e->span) / e->stride + 1 : 0;  // first w with w*stride + span > a0
+    *w_hi = (a1 - 1) / e->stride;                               // last w with w*stride < a1
+}
+
 ss_status ss_engine_push(ss_engine* e, const void* samples, int64_t n_chunks, uint64_t first_seq) {
     if (!e || (!samples && n_chunks > 0) || n_chunks < 0) return SS_EVALIDATION;
-    const int F = e->cfg.n_fft, T = e->cfg.plot_rows;
-    const size_t row_bytes = static_cast<size_t>(F) * e->sbytes;
+    if (n_chunks == 0) return SS_OK;
+    const uint64_t F = static_cast<uint64_t>(e->cfg.n_fft);
     const unsigned char* src = static_cast<const unsigned char*>(samples);
     bool dma_ok = false;  // source is pinned or device memory
     if (n_chunks >= kDirectRows) {
@@ -406,45 +423,45 @@ ss_status ss_engine_push(ss_engine* e, const void* samples, int64_t n_chunks, ui
     }
     std::unique_lock<std::mutex> lk(e->mu);
     if (e->finished) return efail(e, SS_EVALIDATION, "push after finish");
-    int64_t i = 0;
-    while (i < n_chunks) {
-        const uint64_t seq = first_seq + static_cast<uint64_t>(i);
-        const uint64_t w = seq / static_cast<uint64_t>(T);
-        const int r0 = static_cast<int>(seq % static_cast<uint64_t>(T));
-        // rows of this window in this push
-        const int64_t run = std::min<int64_t>(n_chunks - i, T - r0);
+    e->rows_retired += static_cast<uint64_t>(n_chunks);
+    // the push's samples: [a0, a1); every window they meet gets its part
+    const uint64_t a0 = first_seq * F, a1 = (first_seq + static_cast<uint64_t>(n_chunks)) * F;
+    uint64_t w_lo, w_hi;
+    windows_of(e, a0, a1, &w_lo, &w_hi);
+    for (uint64_t w = w_lo; w <= w_hi; ++w) {
+        const uint64_t base = w * e->stride;
+        const uint64_t s0 = std::max(a0, base), s1 = std::min(a1, base + e->span);
+        if (s0 >= s1) continue;
         const int bi = claim_bank(e, w, lk);
-        e->rows_retired += static_cast<uint64_t>(run);
-        if (bi >= 0) {
-            Bank& b = e->banks[static_cast<size_t>(bi)];
-            const unsigned char* from = src + static_cast<size_t>(i) * row_bytes;
-            if (dma_ok && run >= kDirectRows) {
-                ss_status s = flush_stage(e, b, row_bytes);
+        if (bi < 0) continue;
+        Bank& b = e->banks[static_cast<size_t>(bi)];
+        const uint64_t o0 = s0 - base, n = s1 - s0;  // window offset and count, samples
+        const unsigned char* from = src + static_cast<size_t>(s0 - a0) * e->sbytes;
+        if (dma_ok && n >= static_cast<uint64_t>(kDirectRows) * F) {
+            ss_status s = flush_stage(e, b);
+            if (s != SS_OK) return s;
+            EN_CK(e, cudaMemcpyAsync(b.iq + static_cast<size_t>(o0) * e->sbytes, from, static_cast<size_t>(n) * e->sbytes,
+                                     cudaMemcpyDefault, e->copy));
+        } else {
+            if (o0 != b.st_hi) {  // not contiguous with the staged run
+                ss_status s = flush_stage(e, b);
                 if (s != SS_OK) return s;
-                EN_CK(e, cudaMemcpyAsync(b.iq + static_cast<size_t>(r0) * row_bytes, from,
-                                         static_cast<size_t>(run) * row_bytes, cudaMemcpyDefault, e->copy));
-            } else {
-                if (r0 != b.st_hi) {  // not contiguous with the staged run
-                    ss_status s = flush_stage(e, b, row_bytes);
-                    if (s != SS_OK) return s;
-                    b.st_lo = b.st_hi = r0;
-                }
-                std::memcpy(b.h_stage + static_cast<size_t>(r0) * row_bytes, from, static_cast<size_t>(run) * row_bytes);
-                b.st_hi = r0 + static_cast<int>(run);
-                if (b.st_hi - b.st_lo >= kFlushRows) {
-                    ss_status s = flush_stage(e, b, row_bytes);
-                    if (s != SS_OK) return s;
-                }
+                b.st_lo = b.st_hi = o0;
             }
-            b.rows_in += static_cast<int>(run);
-            if (b.rows_in >= T) {
-                ss_status s = flush_stage(e, b, row_bytes);
-                if (s != SS_OK) return s;
-                s = launch_window(e, bi);
+            std::memcpy(b.h_stage + static_cast<size_t>(o0) * e->sbytes, from, static_cast<size_t>(n) * e->sbytes);
+            b.st_hi = o0 + n;
+            if (b.st_hi - b.st_lo >= static_cast<uint64_t>(kFlushRows) * F) {
+                ss_status s = flush_stage(e, b);
                 if (s != SS_OK) return s;
             }
         }
-        i += run;
+        b.samples_in += n;
+        if (b.samples_in >= e->span) {
+            ss_status s = flush_stage(e, b);
+            if (s != SS_OK) return s;
+            s = launch_window(e, bi);
+            if (s != SS_OK) return s;
+        }
     }
     return SS_OK;
 }
@@ -452,10 +469,12 @@ ss_status ss_engine_push(ss_engine* e, const void* samples, int64_t n_chunks, ui
 ss_status ss_engine_mark_lost(ss_engine* e, uint64_t first, uint64_t last) {
     if (!e) return SS_EVALIDATION;
     if (last <= first) return SS_OK;
-    const uint64_t T = static_cast<uint64_t>(e->cfg.plot_rows);
+    const uint64_t F = static_cast<uint64_t>(e->cfg.n_fft);
     std::lock_guard<std::mutex> lk(e->mu);
     e->rows_retired += last - first;
-    for (uint64_t w = first / T; w <= (last - 1) / T; ++w) {
+    uint64_t w_lo, w_hi;
+    windows_of(e, first * F, last * F, &w_lo, &w_hi);
+    for (uint64_t w = w_lo; w <= w_hi; ++w) {
         const int bi = static_cast<int>(w % static_cast<uint64_t>(e->cfg.n_banks));
         Bank& b = e->banks[static_cast<size_t>(bi)];
         if (b.state == BankState::Filling && b.window == w) b.state = BankState::Free;

@@ -192,7 +192,9 @@ class Engine:
 
     def __init__(self, frontend_config: FrontendConfig, detector_config: DetectorConfig | None = None,
                  runtime_config: RuntimeConfig | None = None, fmt: int = N.SS_FMT_F32, paced: bool = False,
-                 device: int = 0):
+                 device: int = 0, hop: int = 0, window: int = 0):
+        """hop / window: the STFT extension (frames every hop samples, 1 = periodic
+        Hann); the defaults are the reference's back-to-back rectangular frames."""
         import torch
 
         if not torch.cuda.is_available():
@@ -205,7 +207,8 @@ class Engine:
         self.fs = frontend_config.sample_rate_hz
         self.fmt = fmt
         self.cap = rc.box_capacity
-        cfg = N.EngineCfg(self.F, self.T, fmt, self.fs, rc.n_banks, int(paced), rc.deadline_s, rc.box_capacity)
+        cfg = N.EngineCfg(self.F, self.T, fmt, self.fs, rc.n_banks, int(paced), rc.deadline_s, rc.box_capacity,
+                          hop, window)
         det = (detector_config or DetectorConfig()).c()
         h = C.c_void_p()
         st = self.lib.ss_engine_open(device, C.byref(cfg), C.byref(det), C.byref(h))
@@ -274,14 +277,14 @@ class Engine:
 
 
 def run(source, frontend_config: FrontendConfig, detector_config: DetectorConfig | None = None,
-        runtime_config: RuntimeConfig | None = None, on_detections=None) -> RunReport:
+        runtime_config: RuntimeConfig | None = None, on_detections=None, hop: int = 0, window: int = 0) -> RunReport:
     """runtime::run (runtime.hpp:103-110): ingest thread -> HBM banks -> GPU
     sensing, one PlotRecord per window handed to on_detections(record, boxes)
     before its bank is released.  Worker errors abort the run and rethrow."""
     rc = runtime_config or RuntimeConfig()
-    eng = Engine(frontend_config, detector_config, rc, fmt=source.fmt, paced=source.paced())
+    eng = Engine(frontend_config, detector_config, rc, fmt=source.fmt, paced=source.paced(), hop=hop, window=window)
     errors = []
-    wall0 = time.perf_counter()
+    wall0 = time.perf_counter()  # after the engine's one-time setup (banks, graphs, warm-up window)
 
     def ingest():
         expected = 0
@@ -316,7 +319,8 @@ def run(source, frontend_config: FrontendConfig, detector_config: DetectorConfig
     if errors:
         raise Error(f"engine aborted, {errors[0]}")
     st = eng.stats()
-    deadline = rc.deadline_s if rc.deadline_s > 0 else frontend_config.plot_span_s()
+    span = frontend_config.plot_rows * (hop or frontend_config.n_fft) / frontend_config.sample_rate_hz
+    deadline = rc.deadline_s if rc.deadline_s > 0 else span
     eng.close()
     rep = summarize(records, st["overruns"], deadline)
     rep.wall_time_s = time.perf_counter() - wall0

@@ -185,3 +185,40 @@ def test_engine_validation():
         rt.Engine(rt.FrontendConfig(FS, 1000, T))
     with pytest.raises(ValidationError):
         rt.Engine(rt.FrontendConfig(FS, F, T), runtime_config=rt.RuntimeConfig(n_banks=1))
+
+
+@pytest.mark.parametrize("hop,window", [(512, 1), (256, 1), (1024, 1)])
+def test_stft_engine_matches_batch(ss, ref, hop, window):
+    """The engine with the STFT extension (frames every hop samples, Hann):
+    windows overlap by F - hop samples, so boundary chunks feed two banks.
+    Every window equals ss_stft_sense_batch on the same stream."""
+    n_win, T = 4, 300
+    n = n_win * T * hop + F - hop
+    n_chunks = (n + F - 1) // F
+    iq = np.resize(_stream(ref, 3 * T), n_chunks * F).astype(np.complex64)
+    eng = rt.Engine(rt.FrontendConfig(FS, F, T), hop=hop, window=window)
+    out = []
+
+    def reader():
+        while (got := eng.poll(10000)) is not None:
+            out.append(got)
+
+    th = threading.Thread(target=reader)
+    th.start()
+    seq, k, sizes = 0, 0, [5, 97, 1, 300, 2, 64, 128, 700, 33]
+    while seq < n_chunks:
+        m = min(sizes[k % len(sizes)], n_chunks - seq)
+        eng.push(iq[seq * F:(seq + m) * F], seq)
+        seq += m
+        k += 1
+    eng.finish()
+    th.join()
+    dets = ss.sense(iq, FS, F, T, hop=hop, window=window, box_capacity=1024)
+    assert [r.plot_index for r, _, _ in out] == list(range(len(dets))) and len(dets) >= n_win
+    for r, boxes, bins in out:
+        d = dets[r.plot_index]
+        assert r.start_seq == r.plot_index * T
+        assert np.array_equal(boxes.view(np.uint64), d.boxes.view(np.uint64)), r.plot_index
+        assert np.array_equal(bins, d.bin_boxes)
+    assert eng.stats()["overruns"] == 0
+    eng.close()
