@@ -224,7 +224,7 @@ typedef struct {
     double deadline_s;     /* <= 0: the plot span T*hop/fs */
     int box_capacity;      /* boxes kept per plot */
     int hop;               /* STFT extension: frame step in samples (0: n_fft, the reference's frames) */
-    int window;            /* STFT extension: ss_window (0: rectangular) */
+    int window;            /* STFT extension: an ss_window value, 0 = rectangular */
 } ss_engine_cfg;
 
 /* runtime::PlotRecord (proj/include/specsense/runtime.hpp:62-69) + extras */
