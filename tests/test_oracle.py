@@ -265,3 +265,19 @@ def test_stft_restatement_rect_is_tf_plot(ora):
     assert np.array_equal(ora.stft_plot(x, 512, 512, 0, 30), ora.tf_plot(x, 512, 30))
     h = ora.stft_plot(x, 512, 256, 1, 50)
     assert h.shape == (50, 512) and np.all(np.isfinite(h))
+
+
+@pytest.mark.parametrize("n_fft,hop", [(1024, 512), (4096, 2048), (256, 64)])
+def test_stft_restatement_matches_numpy(ora, n_fft, hop):
+    """The STFT extension has no reference oracle: pin the restatement against an
+    independent fp64 FFT (numpy) of the Hann-windowed frames at the fp32 level
+    (the same criterion the FFT shim meets for the reference's frontend)."""
+    rng = np.random.default_rng(n_fft + hop)
+    rows = 24
+    x = (rng.normal(size=(rows - 1) * hop + n_fft) + 1j * rng.normal(size=(rows - 1) * hop + n_fft)).astype(np.complex64)
+    got = ora.stft_plot(x, n_fft, hop, 1, rows)
+    n = np.arange(n_fft)
+    w = 0.5 * (1.0 - np.cos(2 * np.pi * n / n_fft))
+    frames = np.stack([x[r * hop: r * hop + n_fft].astype(np.complex128) * w for r in range(rows)])
+    exp = np.abs(np.fft.fftshift(np.fft.fft(frames, axis=1), axes=1)).astype(np.float32)
+    assert np.sum(got != exp) == 0
