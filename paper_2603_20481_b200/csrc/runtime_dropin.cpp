@@ -163,36 +163,20 @@ RunReport run(frontend::ChunkSource& source, const frontend::FrontendConfig& fc,
         if (!failed.exchange(true)) err = std::string(where) + ": " + e.what();
     };
 
-    // ingest: consecutive chunks go out in batches (one H2D per run)
+    // ingest: every chunk goes straight to the engine, which stages it in the
+    // bank's pinned buffer and sends runs of 64 chunks per H2D (no batch copy)
     std::thread ingest([&] {
         try {
-            constexpr std::size_t kBatch = 64;
-            std::vector<cfloat> batch;
-            batch.reserve(kBatch * static_cast<std::size_t>(F));
-            std::uint64_t first = 0, expected = 0;
-            std::size_t n = 0;
-            auto flush = [&] {
-                if (n) eng.check(ss_engine_push(eng.h, batch.data(), static_cast<int64_t>(n), first));
-                batch.clear();
-                n = 0;
-            };
+            std::uint64_t expected = 0;
             frontend::IQChunk chunk;
             while (!failed.load() && source.next(chunk)) {
                 if (chunk.samples.size() != static_cast<std::size_t>(F))
                     throw ValidationError("chunk size " + std::to_string(chunk.samples.size()) + " != n_fft");
                 if (chunk.seq < expected) continue;  // stale / duplicate
-                if (chunk.seq > expected || n == kBatch) {
-                    flush();
-                    if (chunk.seq > expected) eng.check(ss_engine_mark_lost(eng.h, expected, chunk.seq));
-                }
-                if (n == 0) first = chunk.seq;
-                batch.insert(batch.end(), chunk.samples.begin(), chunk.samples.end());
-                ++n;
+                if (chunk.seq > expected) eng.check(ss_engine_mark_lost(eng.h, expected, chunk.seq));
+                eng.check(ss_engine_push(eng.h, chunk.samples.data(), 1, chunk.seq));
                 expected = chunk.seq + 1;
-                // a paced source must not wait for a full batch
-                if (source.paced()) flush();
             }
-            flush();
         } catch (const std::exception& e) {
             capture("ingest", e);
         }
