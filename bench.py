@@ -44,13 +44,15 @@ class Workload:
     frontend, frontend.cpp:127-183) -> plots are back-to-back 100 ms captures.
     hann: config 5 as written (periodic Hann, 50 % overlap, STFT extension)."""
 
-    def __init__(self, name, hop, window, desc):
+    def __init__(self, name, hop, window, desc, i16=False):
         self.name, self.hop, self.window, self.desc = name, hop, window, desc
+        self.i16 = i16
+        self.sb = 4 if i16 else 8                                      # bytes per complex sample
         self.rows = (int(CAPTURE_S * FS) - N_FFT) // hop + 1          # 2441 | 4881
         self.stride = self.rows * hop                                  # new samples per plot
         self.tail = N_FFT - hop                                        # extra samples after the last plot
         # K1 algorithmic bytes per plot: read its new IQ once + write the TF plot
-        self.alg_bytes = self.stride * 8 + self.rows * N_FFT * 4
+        self.alg_bytes = self.stride * self.sb + self.rows * N_FFT * 4
         self.alg_flop64 = self.rows * 5 * N_FFT * 12                   # conventional 5 N log2 N per row
 
     def samples(self, plots):
@@ -62,6 +64,8 @@ WORKLOADS = {
                                       "default DetectorConfig"),
     "hann": Workload("hann", N_FFT // 2, 1, "C5h: 100 ms fp32 IQ @ 100 MS/s, F=4096 periodic Hann hop 2048 "
                                             "(T=4881, STFT extension), default DetectorConfig"),
+    "c5r16": Workload("c5r16", N_FFT, 0, "C5r with int16 IQ (the reference's quantiser, gain 2^-6; decoded "
+                                         "exactly as frontend.cpp:376-385), F=4096 rect hop 4096 (T=2441)", i16=True),
 }
 METRIC = "spectrum-occupancy frames/s (config 5: 100 ms fp32 IQ capture @ 100 MS/s -> 2441x4096 TF plot -> boxes)"
 
@@ -152,7 +156,7 @@ def cpu_reference(wl, threads: int, seconds_budget: float):
     from _oracle import ora, ref
 
     caps = _cpu_caps(wl)
-    if wl.name == "c5r":
+    if wl.hop == N_FFT and wl.window == 0:  # the reference's own frontend (int16 decodes exactly to these floats)
         R = ref()
         iq = np.concatenate(caps)
         t0 = time.perf_counter()
@@ -180,7 +184,7 @@ def cpu_reference(wl, threads: int, seconds_budget: float):
 
 
 def _cpu_sample(wl, n, secs):
-    if wl.name == "c5r":
+    if wl.hop == N_FFT and wl.window == 0:
         return (f"{n} C5r captures (make_plot + detect each, one capture per thread) in {secs:.1f} s; "
                 "reference sources + builder FFTW-API shim (FFTW absent)")
     return (f"{n} C5h plots (oracle_stft_plot + oracle_detect each, one plot per thread) in {secs:.1f} s; "
@@ -216,6 +220,8 @@ def run_reference(args):
 def _metric(wl):
     if wl.name == "c5r":
         return METRIC
+    if wl.name == "c5r16":
+        return METRIC.replace("fp32 IQ", "int16 IQ")
     return ("spectrum-occupancy frames/s (config 5 as written: 100 ms fp32 IQ @ 100 MS/s -> "
             "4881x4096 Hann/50% TF plot -> boxes)")
 
@@ -243,10 +249,17 @@ def run_ours(args):
     D = min(args.distinct, B)
     caps = [signals.synthesize_torch(signals.c5_scenario(1000 * rank + i), device="cuda")[:wl.stride]
             for i in range(D)]
-    iq = torch.zeros(wl.samples(B), dtype=torch.complex64, device="cuda")
-    for b in range(B):
-        iq[b * wl.stride:(b + 1) * wl.stride] = caps[b % D]
+    if wl.i16:  # int16 interleaved, quantised as the reference's int16 path
+        caps = [signals.quantize_i16(c)[0] for c in caps]
+        iq = torch.zeros(2 * wl.samples(B), dtype=torch.int16, device="cuda")
+        for b in range(B):
+            iq[2 * b * wl.stride:2 * (b + 1) * wl.stride] = caps[b % D]
+    else:
+        iq = torch.zeros(wl.samples(B), dtype=torch.complex64, device="cuda")
+        for b in range(B):
+            iq[b * wl.stride:(b + 1) * wl.stride] = caps[b % D]
     del caps
+    fmt = NAT.SS_FMT_I16 if wl.i16 else NAT.SS_FMT_F32
     tf = torch.empty(B * wl.rows * N_FFT, dtype=torch.float32, device="cuda")
     outs = dict(
         psd_raw=torch.empty((B, N_FFT), dtype=torch.float32, device="cuda"),
@@ -266,10 +279,10 @@ def run_ours(args):
         gathered_n = torch.empty((ws, B), dtype=torch.int32, device="cuda")
 
     def sense(src_ptr, nb, tf_ptr, out):
-        if wl.name == "c5r":    # the reference-parity entry point
-            return lib.ss_sense_batch(ctx.h, C.c_void_p(src_ptr), NAT.SS_FMT_F32, N_FFT, wl.rows, nb,
+        if wl.hop == N_FFT and wl.window == 0:    # the reference-parity entry point
+            return lib.ss_sense_batch(ctx.h, C.c_void_p(src_ptr), fmt, N_FFT, wl.rows, nb,
                                       C.c_uint64(0), C.c_double(FS), C.byref(cfg), tf_ptr, C.byref(out))
-        return lib.ss_stft_sense_batch(ctx.h, C.c_void_p(src_ptr), NAT.SS_FMT_F32, N_FFT, wl.hop, wl.window,
+        return lib.ss_stft_sense_batch(ctx.h, C.c_void_p(src_ptr), fmt, N_FFT, wl.hop, wl.window,
                                        wl.rows, nb, C.c_uint64(0), C.c_double(FS), C.byref(cfg), tf_ptr,
                                        C.byref(out))
 
@@ -322,8 +335,9 @@ def run_ours(args):
 
     # ---- e2e: host (pinned) IQ in, host boxes out, through the same C-ABI call
     Be = max(1, min(B, args.e2e_batch))
-    host_iq = torch.empty(wl.samples(Be), dtype=torch.complex64, pin_memory=True)
-    host_iq.copy_(iq[: wl.samples(Be)])
+    per = 2 if wl.i16 else 1
+    host_iq = torch.empty(per * wl.samples(Be), dtype=iq.dtype, pin_memory=True)
+    host_iq.copy_(iq[: per * wl.samples(Be)])
     host_out = {k: torch.empty((Be,) + tuple(v.shape[1:]), dtype=v.dtype, pin_memory=True) for k, v in outs.items()}
     hout = NAT.BatchOut(*(C.c_void_p(v.data_ptr()) for v in host_out.values()), K)
 
@@ -391,7 +405,7 @@ def run_ours(args):
             "data": "synthetic: seeded config-5 captures (16 rectangular bursts, 5-40 MHz, 0.1-5 ms, 0-20 dB) on unit AWGN",
             "config": {"workload": wl.desc,
                        "captures_per_step_per_gpu": B, "distinct_captures": D,
-                       "l2": f"inputs > L2 ({wl.samples(B) * 8 / 1e9:.1f} GB IQ per step, no flush needed)",
+                       "l2": f"inputs > L2 ({wl.samples(B) * wl.sb / 1e9:.1f} GB IQ per step, no flush needed)",
                        "parallelism": f"capture-sharded x{ws}"},
             "iq_gbps": value * wl.stride * 32 / 1e9,
             "stage_ms_per_step": stage_ms,
@@ -399,7 +413,7 @@ def run_ours(args):
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                          "alg_bytes_per_capture": wl.alg_bytes,
                          "fp64_tflops": B * wl.alg_flop64 / (k1_ms / 1e3) / 1e12, "fp64_peak_tflops": FP64_PEAK_TFLOPS},
-            "e2e": {"value": e2e_val, "unit": "frames/s", "h2d_bytes_per_step": wl.samples(Be) * 8 if Be else 0,
+            "e2e": {"value": e2e_val, "unit": "frames/s", "h2d_bytes_per_step": wl.samples(Be) * wl.sb if Be else 0,
                     "d2h_bytes_per_step": d2h, "captures_per_step": Be},
             "gpu_launches": launches,
             "clocks": clocks,
