@@ -267,7 +267,11 @@ __device__ __forceinline__ double rsqrt_seed(double x) {
 // returns true on the fast path (result a normal float).
 // Magnitudes of the thread's P outputs, branch-free on the fast path; lanes
 // flagged in the warp-uniform slow pass redo theirs with __dsqrt_rn.
-template <int P>
+// SH: the transform ran on inputs scaled by 2^SH (int16 IQ without its exact
+// 2^-15 decode factor); power-of-two scaling commutes with every rounding of
+// the FFT, so the true magnitude is the computed one times 2^-SH, applied as
+// an exponent offset (fast path) or an exact multiply (slow path).
+template <int P, int SH>
 __device__ __forceinline__ void mags(const cd* v, float* m) {
     uint32_t slow = 0;
 #pragma unroll
@@ -285,10 +289,10 @@ __device__ __forceinline__ void mags(const cd* v, float* m) {
         const uint32_t lo = static_cast<uint32_t>(__double2loint(s1));
         const int dist = static_cast<int>(lo & 0x1FFFFFFFu) - (1 << 28);
         const uint32_t qe = static_cast<uint32_t>(__double2hiint(q)) >> 20;  // q >= 0: biased exponent
-        const bool ok = (qe - (1023u - 120u)) <= 240u && (dist > 65536 || dist < -65536);
+        const bool ok = (qe - (1023u - 120u + 2u * SH)) <= 240u && (dist > 65536 || dist < -65536);
         // s1 in [2^-60, 2^60]: float exponent = double exponent - 896, mantissa
         // = top 23 bits, +1 ulp when the dropped 29 bits exceed half (no ties here)
-        const uint32_t fb = ((hi - (896u << 20)) << 3) | (lo >> 29);
+        const uint32_t fb = ((hi - ((896u + SH) << 20)) << 3) | (lo >> 29);
         m[i] = __uint_as_float(fb + (dist > 0 ? 1u : 0u));
         slow |= ok ? 0u : (1u << i);
     }
@@ -296,7 +300,8 @@ __device__ __forceinline__ void mags(const cd* v, float* m) {
 #pragma unroll
         for (int i = 0; i < P; ++i)
             if ((slow >> i) & 1u)
-                m[i] = __double2float_rn(__dsqrt_rn(__fma_rn(v[i].re, v[i].re, __dmul_rn(v[i].im, v[i].im))));
+                m[i] = __double2float_rn(__dmul_rn(
+                    __dsqrt_rn(__fma_rn(v[i].re, v[i].re, __dmul_rn(v[i].im, v[i].im))), 1.0 / (1 << SH)));
     }
 }
 
@@ -441,9 +446,9 @@ fft_mag_kernel(FftArgs a) {
                         v[u * R0 + r] = {static_cast<double>(x.x), static_cast<double>(x.y)};
                     } else {
                         const short2 x = valid ? reinterpret_cast<const short2*>(stage)[s] : make_short2(0, 0);
-                        // frontend.cpp:383: raw * (1.0f/32768) is exact, so (double)raw * 2^-15
-                        v[u * R0 + r] = {__dmul_rn(static_cast<double>(x.x), 0x1p-15),
-                                         __dmul_rn(static_cast<double>(x.y), 0x1p-15)};
+                        // frontend.cpp:383: raw * (1.0f/32768) is exact; the 2^-15 is applied
+                        // to the magnitudes instead (mags<P, 15>), bit-identically
+                        v[u * R0 + r] = {static_cast<double>(x.x), static_cast<double>(x.y)};
                     }
                     if constexpr (WIN) {  // STFT extension: one rounded product per component
                         const double w = __ldg(a.win + n);
@@ -462,7 +467,7 @@ fft_mag_kernel(FftArgs a) {
 
         // epilogue: outputs of the last pass, index q = b + r*NS_last
         float m[PL::P];
-        mags<PL::P>(v, m);
+        mags<PL::P, FMT == 1 ? 15 : 0>(v, m);
         if constexpr (G == 1) {
             float* out = a.tf ? a.tf + row * N : nullptr;
 #pragma unroll
