@@ -225,6 +225,9 @@ typedef struct {
     int box_capacity;      /* boxes kept per plot */
     int hop;               /* STFT extension: frame step in samples (0: n_fft, the reference's frames) */
     int window;            /* STFT extension: an ss_window value, 0 = rectangular */
+    int shard_count;       /* multi-GPU: windows are dealt round-robin over shard_count engines */
+    int shard_index;       /* ... this engine senses windows w with w % shard_count == shard_index
+                              (0 / 0: every window); others are skipped, not counted as lost */
 } ss_engine_cfg;
 
 /* runtime::PlotRecord (proj/include/specsense/runtime.hpp:62-69) + extras */

@@ -47,7 +47,7 @@ class BaselineCfg(C.Structure):
 class EngineCfg(C.Structure):
     _fields_ = [("n_fft", C.c_int), ("plot_rows", C.c_int), ("fmt", C.c_int), ("sample_rate_hz", C.c_double),
                 ("n_banks", C.c_int), ("paced", C.c_int), ("deadline_s", C.c_double), ("box_capacity", C.c_int),
-                ("hop", C.c_int), ("window", C.c_int)]
+                ("hop", C.c_int), ("window", C.c_int), ("shard_count", C.c_int), ("shard_index", C.c_int)]
 
 
 class PlotRecord(C.Structure):

@@ -106,6 +106,9 @@ struct ss_engine {
     double deadline_s = 0.0;
     int hop = 0, window = 0;
     uint64_t stride = 0, span = 0;  // samples between window starts; samples per window
+    uint64_t shards = 1, shard = 0;  // this engine owns windows w % shards == shard
+
+    bool owns(uint64_t w) const { return w % shards == shard; }
     Clock::time_point t0{};
     std::vector<Bank> banks;
 
@@ -211,10 +214,12 @@ ss_status launch_window(ss_engine* e, int bi) {
 }
 
 // Bank for window w, or -1 when its rows must be dropped.  Called with lk held.
+// w is a window this engine owns; its banks cycle over the owned windows
+// (w / shards) so a sharded engine sees consecutive bank indices.
 int claim_bank(ss_engine* e, uint64_t w, std::unique_lock<std::mutex>& lk) {
     if (e->have_dropped && w == e->dropped_window) return -1;
-    if (w + static_cast<uint64_t>(e->cfg.n_banks) <= e->newest_window) return -1;  // stale row
-    const int bi = static_cast<int>(w % static_cast<uint64_t>(e->cfg.n_banks));
+    if (w + static_cast<uint64_t>(e->cfg.n_banks) * e->shards <= e->newest_window) return -1;  // stale row
+    const int bi = static_cast<int>((w / e->shards) % static_cast<uint64_t>(e->cfg.n_banks));
     for (;;) {
         Bank& b = e->banks[static_cast<size_t>(bi)];
         if (b.state == BankState::Filling && b.window == w) return bi;
@@ -275,6 +280,10 @@ ss_status ss_engine_open(int device, const ss_engine_cfg* cfg, const ss_detector
     const int F = cfg->n_fft, T = cfg->plot_rows, K = e->cfg.box_capacity;
     e->hop = cfg->hop > 0 ? cfg->hop : F;
     e->window = cfg->window;
+    if (cfg->shard_count < 0 || (cfg->shard_count > 0 && (cfg->shard_index < 0 || cfg->shard_index >= cfg->shard_count)))
+        return bad(SS_EVALIDATION, "shard_index must be in [0, shard_count)");
+    e->shards = cfg->shard_count > 0 ? static_cast<uint64_t>(cfg->shard_count) : 1;
+    e->shard = cfg->shard_count > 0 ? static_cast<uint64_t>(cfg->shard_index) : 0;
     s = ssb::engine_check_stft(e->ctx, F, e->hop, e->window, cfg->fmt);
     if (s != SS_OK) return bad(s, ss_last_error(e->ctx));
     e->sbytes = cfg->fmt == SS_FMT_F32 ? 8 : 4;
@@ -429,6 +438,7 @@ ss_status ss_engine_push(ss_engine* e, const void* samples, int64_t n_chunks, ui
     uint64_t w_lo, w_hi;
     windows_of(e, a0, a1, &w_lo, &w_hi);
     for (uint64_t w = w_lo; w <= w_hi; ++w) {
+        if (!e->owns(w)) continue;  // another shard's window
         const uint64_t base = w * e->stride;
         const uint64_t s0 = std::max(a0, base), s1 = std::min(a1, base + e->span);
         if (s0 >= s1) continue;
@@ -475,7 +485,8 @@ ss_status ss_engine_mark_lost(ss_engine* e, uint64_t first, uint64_t last) {
     uint64_t w_lo, w_hi;
     windows_of(e, first * F, last * F, &w_lo, &w_hi);
     for (uint64_t w = w_lo; w <= w_hi; ++w) {
-        const int bi = static_cast<int>(w % static_cast<uint64_t>(e->cfg.n_banks));
+        if (!e->owns(w)) continue;
+        const int bi = static_cast<int>((w / e->shards) % static_cast<uint64_t>(e->cfg.n_banks));
         Bank& b = e->banks[static_cast<size_t>(bi)];
         if (b.state == BankState::Filling && b.window == w) b.state = BankState::Free;
         if (!(e->have_dropped && e->dropped_window == w)) ++e->overruns;

@@ -192,9 +192,11 @@ class Engine:
 
     def __init__(self, frontend_config: FrontendConfig, detector_config: DetectorConfig | None = None,
                  runtime_config: RuntimeConfig | None = None, fmt: int = N.SS_FMT_F32, paced: bool = False,
-                 device: int = 0, hop: int = 0, window: int = 0):
+                 device: int = 0, hop: int = 0, window: int = 0, shard: tuple[int, int] = (0, 1)):
         """hop / window: the STFT extension (frames every hop samples, 1 = periodic
-        Hann); the defaults are the reference's back-to-back rectangular frames."""
+        Hann); the defaults are the reference's back-to-back rectangular frames.
+        shard = (index, count): this engine senses windows w % count == index
+        (multi-GPU: one engine per device, every chunk pushed to all)."""
         import torch
 
         if not torch.cuda.is_available():
@@ -208,7 +210,7 @@ class Engine:
         self.fmt = fmt
         self.cap = rc.box_capacity
         cfg = N.EngineCfg(self.F, self.T, fmt, self.fs, rc.n_banks, int(paced), rc.deadline_s, rc.box_capacity,
-                          hop, window)
+                          hop, window, shard[1], shard[0])
         det = (detector_config or DetectorConfig()).c()
         h = C.c_void_p()
         st = self.lib.ss_engine_open(device, C.byref(cfg), C.byref(det), C.byref(h))
@@ -217,6 +219,7 @@ class Engine:
             msg = self.lib.ss_engine_last_error(h).decode() if h else f"ss_engine_open status {st}"
             self.close()
             raise (ValidationError if st == N.SS_EVALIDATION else Error)(msg)
+        self._finished = False
         self._boxes = (N.Box * self.cap)()
         self._bins = (N.BinBox * self.cap)()
 
@@ -241,6 +244,7 @@ class Engine:
 
     def finish(self):
         self._check(self.lib.ss_engine_finish(self.h))
+        self._finished = True
 
     def poll(self, wait_ms: int = -1):
         """(PlotRecord, boxes (n,4) f64 [f0,f1,t0,t1], bin_boxes (n,4) i32) or None."""
@@ -258,6 +262,11 @@ class Engine:
                        rec.complete_s, rec.done_s, rec.gpu_s)
         self._check(st)
         return r, boxes, bins
+
+    def finished_and_drained(self) -> bool:
+        """True once finish() was called and every launched window was polled."""
+        st = self.stats()
+        return self._finished and st["pending"] == 0
 
     def stats(self) -> dict:
         v = [C.c_uint64() for _ in range(4)]
@@ -277,12 +286,17 @@ class Engine:
 
 
 def run(source, frontend_config: FrontendConfig, detector_config: DetectorConfig | None = None,
-        runtime_config: RuntimeConfig | None = None, on_detections=None, hop: int = 0, window: int = 0) -> RunReport:
+        runtime_config: RuntimeConfig | None = None, on_detections=None, hop: int = 0, window: int = 0,
+        devices=None) -> RunReport:
     """runtime::run (runtime.hpp:103-110): ingest thread -> HBM banks -> GPU
     sensing, one PlotRecord per window handed to on_detections(record, boxes)
     before its bank is released.  Worker errors abort the run and rethrow."""
     rc = runtime_config or RuntimeConfig()
-    eng = Engine(frontend_config, detector_config, rc, fmt=source.fmt, paced=source.paced(), hop=hop, window=window)
+    devices = list(devices) if devices else [0]
+    G = len(devices)
+    engines = [Engine(frontend_config, detector_config, rc, fmt=source.fmt, paced=source.paced(), device=d, hop=hop,
+                      window=window, shard=(g, G)) for g, d in enumerate(devices)]
+    eng = engines[0]
     errors = []
     wall0 = time.perf_counter()  # after the engine's one-time setup (banks, graphs, warm-up window)
 
@@ -290,38 +304,52 @@ def run(source, frontend_config: FrontendConfig, detector_config: DetectorConfig
         expected = 0
         try:
             for seq, block in source.blocks():
-                if seq > expected:
-                    eng.mark_lost(expected, seq)
-                eng.push(block, seq)
+                for e_ in engines:  # each engine keeps only its own windows' samples
+                    if seq > expected:
+                        e_.mark_lost(expected, seq)
+                    e_.push(block, seq)
                 expected = seq + block.size // (frontend_config.n_fft * (2 if source.fmt == N.SS_FMT_I16 else 1))
         except Exception as e:  # noqa: BLE001
             errors.append(e)
         finally:
-            try:
-                eng.finish()
-            except Exception as e:  # noqa: BLE001
-                errors.append(e)
+            for e_ in engines:
+                try:
+                    e_.finish()
+                except Exception as e:  # noqa: BLE001
+                    errors.append(e)
 
     th = threading.Thread(target=ingest, daemon=True)
     th.start()
     records = []
     try:
-        while True:
-            got = eng.poll(-1)
-            if got is None:
-                break
-            rec, boxes, _ = got
-            records.append(rec)
-            if on_detections is not None:
-                on_detections(rec, boxes)
+        if G == 1:
+            while (got := eng.poll(-1)) is not None:
+                records.append(got[0])
+                if on_detections is not None:
+                    on_detections(got[0], got[1])
+        else:
+            # each engine returns its own windows in order; across engines the
+            # handler sees them as they complete (the report is sorted by window)
+            live = set(range(G))
+            while live:
+                for g in list(live):
+                    got = engines[g].poll(1)
+                    if got is None:
+                        if engines[g].finished_and_drained():
+                            live.discard(g)
+                        continue
+                    records.append(got[0])
+                    if on_detections is not None:
+                        on_detections(got[0], got[1])
     finally:
         th.join()
     if errors:
         raise Error(f"engine aborted, {errors[0]}")
-    st = eng.stats()
+    overruns = sum(e_.stats()["overruns"] for e_ in engines)
     span = frontend_config.plot_rows * (hop or frontend_config.n_fft) / frontend_config.sample_rate_hz
     deadline = rc.deadline_s if rc.deadline_s > 0 else span
-    eng.close()
-    rep = summarize(records, st["overruns"], deadline)
+    for e_ in engines:
+        e_.close()
+    rep = summarize(records, overruns, deadline)
     rep.wall_time_s = time.perf_counter() - wall0
     return rep
