@@ -18,7 +18,7 @@
 
 namespace specsense::frontend {
 
-// Capture geometry: fs, F (power of two >= 8; <= 8192 on the device), T.
+// Capture geometry: fs, F (power of two >= 8; <= 2^20 on the device), T.
 struct FrontendConfig {
     double sample_rate_hz = 0.0;
     int n_fft = 1024;

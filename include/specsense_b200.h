@@ -40,7 +40,7 @@ typedef enum {
     SS_EFORMAT = 2,     /* malformed payloads (FormatError) */
     SS_ECUDA = 3,       /* CUDA runtime failure or no device */
     SS_ENOMEM = 4,      /* device allocation failed */
-    SS_EUNSUPPORTED = 5,/* valid for the reference, not supported on device (e.g. n_fft > 8192) */
+    SS_EUNSUPPORTED = 5,/* valid for the reference, not supported on device (e.g. n_fft > 2^20) */
     SS_ECAPACITY = 6    /* caller-provided output capacity too small */
 } ss_status;
 
@@ -123,8 +123,10 @@ ss_status ss_stage_times(const ss_ctx* ctx, double* ms8);
    consecutive plots of `rows` rows: iq holds n_plots*rows*n_fft samples
    (interleaved I,Q; 16-byte aligned), tf receives n_plots*rows*n_fft floats,
    row r column k = |X_r[(k + n_fft/2) mod n_fft]| (frontend.cpp:127-149).
-   n_fft: power of two, 8 <= n_fft <= 8192 on device (reference: any power of
-   two >= 8, frontend.cpp:37-42; larger sizes -> SS_EUNSUPPORTED). */
+   n_fft: power of two, 8 <= n_fft <= 2^20 on device (reference: any power of
+   two >= 8, frontend.cpp:37-42; larger sizes -> SS_EUNSUPPORTED).  Up to
+   8192 one CTA transforms a row in shared memory (K1); above, the same
+   SSFFT-2 passes run as a chain of global-memory kernels. */
 ss_status ss_tf_plots(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int rows, int n_plots,
                       float* tf);
 
@@ -215,7 +217,7 @@ ss_status ss_stft_sense_batch(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft
 typedef struct ss_engine ss_engine;
 
 typedef struct {
-    int n_fft;             /* F: power of two, 8..8192 */
+    int n_fft;             /* F: power of two, 8..2^20 */
     int plot_rows;         /* T */
     ss_fmt fmt;            /* chunk sample format */
     double sample_rate_hz;

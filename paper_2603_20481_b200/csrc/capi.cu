@@ -135,7 +135,8 @@ ss_status twiddles(ss_ctx* ctx, int n_fft, const double2** out) {
     auto it = ctx->tw.find(lg);
     if (it == ctx->tw.end()) {
         std::vector<double2> host;
-        ssb::fft_twiddles(lg, host);
+        if (lg <= 13) ssb::fft_twiddles(lg, host);
+        else ssb::fft_large_w1(lg, host);  // large N: the compact per-pass w1 table
         double2* d = nullptr;
         SS_CK(ctx, cudaMalloc(&d, sizeof(double2) * host.size()));
         SS_CK(ctx, cudaMemcpy(d, host.data(), sizeof(double2) * host.size(), cudaMemcpyHostToDevice));
@@ -144,6 +145,9 @@ ss_status twiddles(ss_ctx* ctx, int n_fft, const double2** out) {
     *out = it->second;
     return SS_OK;
 }
+
+// K1 for n_fft <= 8192; above, the global-memory pass chain (no fused PSD)
+ss_status frontend_launch(ss_ctx* ctx, const ssb::FftLaunch& L);
 
 ss_status window_table(ss_ctx* ctx, int n_fft, int kind, const double** out) {
     auto key = std::make_pair(n_fft, kind);
@@ -315,6 +319,10 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
     F.active = out_dev.active ? out_dev.active : act;
     F.n_active = out_dev.n_active ? out_dev.n_active : nact;
     F.active_bits = abits;
+    if (ssb::floor_needs_scratch(F.n, F.window)) {
+        SS_WS(fscr, float, "floor.scratch", 2 * static_cast<size_t>(F.n_plots) * F.n);
+        F.scratch = fscr;
+    }
     tmark(ctx, 2, 0);
     SS_CK(ctx, ssb::floor_launch(F, ctx->stream));
     tmark(ctx, 2, 1);
@@ -369,6 +377,23 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
         }
         SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
     }
+    return SS_OK;
+}
+
+ss_status frontend_launch(ss_ctx* ctx, const ssb::FftLaunch& L) {
+    if (L.logn <= 13) {
+        SS_CK(ctx, ssb::fft_mag_launch(L, ctx->stream));
+        ctx->launches += 1;
+        return SS_OK;
+    }
+    if (L.psd) return fail(ctx, SS_EUNSUPPORTED, "fused PSD needs n_fft <= 8192");
+    const long long n = 1LL << L.logn;
+    const long long chunk = std::max(1LL, std::min(L.total_rows, (1LL << 26) / n));  // <= 1 GiB per scratch
+    SS_WS(a, double2, "large.a", static_cast<size_t>(chunk * n));
+    SS_WS(b, double2, "large.b", static_cast<size_t>(chunk * n));
+    int nl = 0;
+    SS_CK(ctx, ssb::fft_large_launch(L, L.tw, a, b, chunk, ctx->stream, &nl));
+    ctx->launches += nl;
     return SS_OK;
 }
 
@@ -472,7 +497,7 @@ ss_status ss_tf_plots(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int ro
     if (!ctx) return SS_EVALIDATION;
     if (n_fft < 8 || !is_pow2(n_fft))
         return fail(ctx, SS_EVALIDATION, "FFT size must be a power of two >= 8, got " + std::to_string(n_fft));
-    if (n_fft > 8192) return fail(ctx, SS_EUNSUPPORTED, "device FFT supports n_fft <= 8192");
+    if (n_fft > (1 << ssb::kLargeLogNMax)) return fail(ctx, SS_EUNSUPPORTED, "device FFT supports n_fft <= 1048576");
     if (rows < 0 || n_plots < 0) return fail(ctx, SS_EVALIDATION, "negative plot geometry");
     if (fmt != SS_FMT_F32 && fmt != SS_FMT_I16) return fail(ctx, SS_EVALIDATION, "unknown sample format");
     if (static_cast<long long>(rows) * n_plots == 0) return SS_OK;
@@ -491,9 +516,7 @@ ss_status ss_tf_plots(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int ro
     L.rows_per_plot = rows;
     L.n_plots = n_plots;
     L.num_sms = ctx->num_sms;
-    SS_CK(ctx, ssb::fft_mag_launch(L, ctx->stream));
-    ctx->launches += 1;
-    return SS_OK;
+    return frontend_launch(ctx, L);
 }
 
 ss_status ss_stft_plots(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int hop, int window, int rows,
@@ -501,7 +524,7 @@ ss_status ss_stft_plots(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int 
     if (!ctx) return SS_EVALIDATION;
     if (n_fft < 8 || !is_pow2(n_fft))
         return fail(ctx, SS_EVALIDATION, "FFT size must be a power of two >= 8, got " + std::to_string(n_fft));
-    if (n_fft > 8192) return fail(ctx, SS_EUNSUPPORTED, "device FFT supports n_fft <= 8192");
+    if (n_fft > (1 << ssb::kLargeLogNMax)) return fail(ctx, SS_EUNSUPPORTED, "device FFT supports n_fft <= 1048576");
     if (rows < 0 || n_plots < 0) return fail(ctx, SS_EVALIDATION, "negative plot geometry");
     ss_status s = check_stft(ctx, n_fft, hop, window, fmt);
     if (s != SS_OK) return s;
@@ -525,9 +548,7 @@ ss_status ss_stft_plots(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, int 
     L.num_sms = ctx->num_sms;
     L.hop = hop;
     L.win = w;
-    SS_CK(ctx, ssb::fft_mag_launch(L, ctx->stream));
-    ctx->launches += 1;
-    return SS_OK;
+    return frontend_launch(ctx, L);
 }
 
 ss_status ss_psd_cols(ss_ctx* ctx, const float* tf, int rows, int cols, int c0, int c1, float* out) {
@@ -574,6 +595,10 @@ ss_status ss_floor(ss_ctx* ctx, const float* raw, int n, const ss_detector_cfg* 
     F.floor_thr = floor_thr;
     F.active = active;
     F.n_active = nact;
+    if (ssb::floor_needs_scratch(F.n, F.window)) {
+        SS_WS(fscr, float, "floor.scratch", 2 * static_cast<size_t>(F.n));
+        F.scratch = fscr;
+    }
     SS_CK(ctx, ssb::floor_launch(F, ctx->stream));
     ctx->launches += 1;
     int h = 0;
@@ -808,9 +833,9 @@ static ss_status sense_device(ss_ctx* ctx, const void* diq, ss_fmt fmt, int n_ff
         L.win = w;
     }
     tmark(ctx, 0, 0);
-    SS_CK(ctx, ssb::fft_mag_launch(L, ctx->stream));
+    s = frontend_launch(ctx, L);
+    if (s != SS_OK) return s;
     tmark(ctx, 0, 1);
-    ctx->launches += 1;
     if (!fused) {
         tmark(ctx, 1, 0);
         SS_CK(ctx, ssb::psd_cols_launch(tf, n_plots, rows, cols, 0, cols, praw, ctx->stream));
@@ -862,7 +887,7 @@ static ss_status sense_impl(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, 
     if (!ctx || !cfg || !out) return SS_EVALIDATION;
     if (n_fft < 8 || !is_pow2(n_fft))
         return fail(ctx, SS_EVALIDATION, "FFT size must be a power of two >= 8, got " + std::to_string(n_fft));
-    if (n_fft > 8192) return fail(ctx, SS_EUNSUPPORTED, "device FFT supports n_fft <= 8192");
+    if (n_fft > (1 << ssb::kLargeLogNMax)) return fail(ctx, SS_EUNSUPPORTED, "device FFT supports n_fft <= 1048576");
     if (rows < 1) return fail(ctx, SS_EVALIDATION, "plot_rows must be >= 1");
     if (!(sample_rate_hz > 0.0)) return fail(ctx, SS_EVALIDATION, "sample_rate_hz must be positive");
     if (fmt != SS_FMT_F32 && fmt != SS_FMT_I16) return fail(ctx, SS_EVALIDATION, "unknown sample format");
@@ -1071,6 +1096,10 @@ ss_status ss_baseline_detect(ss_ctx* ctx, const float* tf, int rows, int cols, u
     F.active = act;
     F.n_active = nact;
     F.active_bits = abits;
+    if (ssb::floor_needs_scratch(F.n, F.window)) {
+        SS_WS(fscr, float, "floor.scratch", 2 * static_cast<size_t>(F.n_plots) * F.n);
+        F.scratch = fscr;
+    }
     SS_CK(ctx, ssb::floor_launch(F, ctx->stream));
     // summed-area table and the kernel bank's candidate bitmaps
     SS_WS(racc, double, "bl.racc", cells);
@@ -1150,7 +1179,7 @@ cudaStream_t engine_ctx_stream(ss_ctx* ctx) { return ctx->stream; }
 ss_status engine_check(ss_ctx* ctx, int n_fft, int rows, ss_fmt fmt, double fs, const ss_detector_cfg& cfg) {
     if (n_fft < 8 || !is_pow2(n_fft))
         return fail(ctx, SS_EVALIDATION, "FFT size must be a power of two >= 8, got " + std::to_string(n_fft));
-    if (n_fft > 8192) return fail(ctx, SS_EUNSUPPORTED, "device FFT supports n_fft <= 8192");
+    if (n_fft > (1 << ssb::kLargeLogNMax)) return fail(ctx, SS_EUNSUPPORTED, "device FFT supports n_fft <= 1048576");
     if (rows < 1) return fail(ctx, SS_EVALIDATION, "plot_rows must be >= 1");
     if (!(fs > 0.0)) return fail(ctx, SS_EVALIDATION, "sample_rate_hz must be positive");
     if (fmt != SS_FMT_F32 && fmt != SS_FMT_I16) return fail(ctx, SS_EVALIDATION, "unknown sample format");

@@ -25,6 +25,7 @@
 #include "common.cuh"
 #include "internal.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <vector>
@@ -694,6 +695,180 @@ int fft_psd_slots_per_sm(int logn, int fmt, bool win) {
     case 13: return psd_slots_fmt<13>(fmt, win);
     default: return 0;
     }
+}
+
+// ------------------------------------------------------------- large N
+// n_fft = 2^14 .. 2^20 (one row no longer fits one CTA's shared memory): the
+// same SSFFT-2 passes, one kernel per pass over global double2 scratch,
+// then a magnitude kernel with the reference's exact expression.  Slower than
+// K1, but the arithmetic -- and so every output bit -- is identical.
+struct RtPlan {
+    int logn, n, np;
+    int radix[8], ns[8];
+    long long w1off[8];  // offset of pass p's w1 block (Ns entries) in the compact table
+    long long w1size;
+};
+
+static RtPlan rt_plan(int logn) {
+    RtPlan P{};
+    P.logn = logn;
+    P.n = 1 << logn;
+    P.np = logn / 4 + (logn % 4 ? 1 : 0);
+    int ns = 1;
+    long long off = 0;
+    for (int p = 0; p < P.np; ++p) {
+        P.radix[p] = p < logn / 4 ? 16 : (1 << (logn % 4));
+        P.ns[p] = ns;
+        P.w1off[p] = off;
+        if (p > 0) off += ns;
+        ns *= P.radix[p];
+    }
+    P.w1size = off > 0 ? off : 1;
+    return P;
+}
+
+// w1 of pass p (Ns > 1), butterfly class k: canonical tw[k * N / (Ns * R)]
+static void build_w1(const RtPlan& P, std::vector<double2>& out) {
+    out.assign(static_cast<size_t>(P.w1size), make_double2(0, 0));
+    const double two_pi = 2.0 * 3.14159265358979323846;
+    for (int p = 1; p < P.np; ++p) {
+        const long long s = P.n / (static_cast<long long>(P.ns[p]) * P.radix[p]);
+        for (int k = 0; k < P.ns[p]; ++k) {
+            const double t = (two_pi * static_cast<double>(k * s)) / static_cast<double>(P.n);
+            out[static_cast<size_t>(P.w1off[p] + k)] = make_double2(std::cos(t), -std::sin(t));
+        }
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void twiddle_tree(cd* v, cd w1) {
+    // SSFFT-2 powers of w1, applied in the spec's product order (run_pass)
+    cd w[16];
+    w[1] = w1;
+    if constexpr (R > 2) w[2] = c_mul(w[1], w[1]);
+    if constexpr (R > 3) w[3] = c_mul(w[2], w[1]);
+    if constexpr (R > 4) {
+        w[4] = c_mul(w[2], w[2]);
+        w[5] = c_mul(w[4], w[1]);
+        w[6] = c_mul(w[4], w[2]);
+        w[7] = c_mul(w[4], w[3]);
+    }
+    if constexpr (R > 8) {
+        w[8] = c_mul(w[4], w[4]);
+#pragma unroll
+        for (int q = 9; q < 16; ++q) w[q] = c_mul(w[8], w[q - 8]);
+    }
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = c_mul(v[r], w[r]);
+}
+
+// One Stockham pass.  FIRST: read the IQ rows (frames every hop samples,
+// optional window) instead of the scratch.
+template <int R, bool FIRST, int FMT>
+__global__ void large_pass_kernel(const void* __restrict__ src, double2* __restrict__ dst, int n, int ns, int hop,
+                                  const double* __restrict__ win, const double2* __restrict__ w1, long long rows) {
+    const int nb = n / R;
+    const long long total = rows * nb;
+    for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long row = idx / nb;
+        const int j = static_cast<int>(idx % nb);
+        cd v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int e = j + r * nb;
+            if constexpr (FIRST) {
+                const long long at = row * hop + e;
+                if constexpr (FMT == 0) {
+                    const float2 x = static_cast<const float2*>(src)[at];
+                    v[r] = {static_cast<double>(x.x), static_cast<double>(x.y)};
+                } else {
+                    const short2 x = static_cast<const short2*>(src)[at];
+                    v[r] = {__dmul_rn(static_cast<double>(x.x), 0x1p-15), __dmul_rn(static_cast<double>(x.y), 0x1p-15)};
+                }
+                if (win) {
+                    const double w = __ldg(win + e);
+                    v[r] = {__dmul_rn(v[r].re, w), __dmul_rn(v[r].im, w)};
+                }
+            } else {
+                const double2 x = static_cast<const double2*>(src)[row * n + e];
+                v[r] = {x.x, x.y};
+            }
+        }
+        const int k = j % ns;
+        if (ns > 1) {
+            const double2 t = __ldg(w1 + k);
+            twiddle_tree<R>(v, cd{t.x, t.y});
+        }
+        dft_r<R>(v);
+        const long long base = row * n + static_cast<long long>(j - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) dst[base + static_cast<long long>(r) * ns] = make_double2(v[r].re, v[r].im);
+    }
+}
+
+// out[row][k] = float(sqrt(fma(re, re, im * im))) of X[(k + N/2) mod N]
+__global__ void large_mag_kernel(const double2* __restrict__ x, float* __restrict__ out, int n, long long rows) {
+    const long long total = rows * n;
+    for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long row = idx / n;
+        const int k = static_cast<int>(idx % n);
+        const double2 v = x[row * n + ((k + n / 2) & (n - 1))];
+        out[idx] = __double2float_rn(__dsqrt_rn(__fma_rn(v.x, v.x, __dmul_rn(v.y, v.y))));
+    }
+}
+
+template <bool FIRST, int FMT>
+static void large_pass(int R, const void* src, double2* dst, int n, int ns, int hop, const double* win,
+                       const double2* w1, long long rows, int num_sms, cudaStream_t st) {
+    const long long work = rows * (n / R);
+    const unsigned grid = static_cast<unsigned>(std::min<long long>((work + 255) / 256, 32LL * num_sms));
+    switch (R) {
+    case 16: large_pass_kernel<16, FIRST, FMT><<<grid, 256, 0, st>>>(src, dst, n, ns, hop, win, w1, rows); break;
+    case 8: large_pass_kernel<8, FIRST, FMT><<<grid, 256, 0, st>>>(src, dst, n, ns, hop, win, w1, rows); break;
+    case 4: large_pass_kernel<4, FIRST, FMT><<<grid, 256, 0, st>>>(src, dst, n, ns, hop, win, w1, rows); break;
+    default: large_pass_kernel<2, FIRST, FMT><<<grid, 256, 0, st>>>(src, dst, n, ns, hop, win, w1, rows); break;
+    }
+}
+
+size_t fft_large_w1_count(int logn) { return static_cast<size_t>(rt_plan(logn).w1size); }
+void fft_large_w1(int logn, std::vector<double2>& out) { build_w1(rt_plan(logn), out); }
+
+// rows of frames -> TF rows, in row chunks that keep the two double2 scratch
+// buffers (a, b: chunk_rows * n each) bounded.  Returns the kernels launched.
+cudaError_t fft_large_launch(const FftLaunch& L, const double2* w1, double2* a, double2* b, long long chunk_rows,
+                             cudaStream_t st, int* launches) {
+    const RtPlan P = rt_plan(L.logn);
+    const int hop = L.hop > 0 ? L.hop : P.n;
+    const size_t sb = L.fmt == 0 ? sizeof(float2) : sizeof(short2);
+    int nl = 0;
+    for (long long r0 = 0; r0 < L.total_rows; r0 += chunk_rows) {
+        const long long rows = std::min(chunk_rows, L.total_rows - r0);
+        const void* src = static_cast<const unsigned char*>(L.iq) + r0 * hop * sb;
+        double2* in = a;
+        double2* out = b;
+        for (int pidx = 0; pidx < P.np; ++pidx) {
+            const double2* wp = w1 + P.w1off[pidx];
+            if (pidx == 0) {
+                if (L.fmt == 0) large_pass<true, 0>(P.radix[0], src, out, P.n, 1, hop, L.win, wp, rows, L.num_sms, st);
+                else large_pass<true, 1>(P.radix[0], src, out, P.n, 1, hop, L.win, wp, rows, L.num_sms, st);
+            } else {
+                large_pass<false, 0>(P.radix[pidx], in, out, P.n, P.ns[pidx], hop, nullptr, wp, rows, L.num_sms, st);
+            }
+            ++nl;
+            double2* t = in;
+            in = out;
+            out = t;
+        }
+        const unsigned grid = static_cast<unsigned>(std::min<long long>((rows * P.n + 255) / 256, 32LL * L.num_sms));
+        large_mag_kernel<<<grid, 256, 0, st>>>(in, L.tf + r0 * P.n, P.n, rows);
+        ++nl;
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    if (launches) *launches = nl;
+    return cudaSuccess;
 }
 
 void fft_twiddles(int logn, std::vector<double2>& out) {

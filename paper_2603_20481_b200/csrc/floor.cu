@@ -81,12 +81,13 @@ __global__ void __launch_bounds__(kFloorThreads) floor_kernel(FloorLaunch a) {
     const int n = a.n;
     const int h = (a.window - 1) / 2;
     double* w = fl_smem;
-    float* db = reinterpret_cast<float*>(w + a.window);
+    const int p = blockIdx.x;
+    // dB and smoothed rows: shared memory, or global scratch for very wide plots
+    float* db = a.scratch ? a.scratch + 2LL * p * n : reinterpret_cast<float*>(w + a.window);
     float* s = db + n;
     __shared__ float red_f[32];
     __shared__ int red_i[32];
 
-    const int p = blockIdx.x;
     const float* raw = a.raw + static_cast<long long>(p) * n;
     const int tid = threadIdx.x, nt = blockDim.x;
 
@@ -171,7 +172,8 @@ __global__ void __launch_bounds__(kFloorThreads) floor_kernel(FloorLaunch a) {
 
 cudaError_t floor_launch(const FloorLaunch& L, cudaStream_t st) {
     if (L.n_plots <= 0) return cudaSuccess;
-    const size_t smem = sizeof(double) * L.window + sizeof(float) * 2 * L.n;
+    if (floor_needs_scratch(L.n, L.window) && !L.scratch) return cudaErrorInvalidValue;
+    const size_t smem = sizeof(double) * L.window + (L.scratch ? 0 : sizeof(float) * 2 * L.n);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(floor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));

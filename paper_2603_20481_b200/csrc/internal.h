@@ -28,6 +28,12 @@ cudaError_t fft_mag_launch(const FftLaunch& L, cudaStream_t st);
 // plots per SM the fused-PSD K1 grid runs concurrently (one plot per row group)
 int fft_psd_slots_per_sm(int logn, int fmt, bool win);
 void fft_window(int n_fft, int kind, std::vector<double>& out);  // kind 0 rect, 1 periodic Hann
+// n_fft = 2^14 .. 2^20: global-memory SSFFT-2 passes + magnitudes (no PSD)
+constexpr int kLargeLogNMax = 20;
+size_t fft_large_w1_count(int logn);
+void fft_large_w1(int logn, std::vector<double2>& out);
+cudaError_t fft_large_launch(const FftLaunch& L, const double2* w1, double2* a, double2* b, long long chunk_rows,
+                             cudaStream_t st, int* launches);
 void fft_twiddles(int logn, std::vector<double2>& out);
 
 // ---- K2/K3 floor.cu
@@ -49,7 +55,10 @@ struct FloorLaunch {
     int* active = nullptr;        // n_plots x n (compacted, ascending)
     int* n_active = nullptr;      // n_plots
     uint32_t* active_bits = nullptr;  // n_plots x W (W = ceil(n/32)), may be null
+    float* scratch = nullptr;     // n_plots x 2n floats: the dB / smoothed rows when they exceed shared memory
 };
+// true when the floor stage needs FloorLaunch::scratch (rows of n floats do not fit shared memory)
+inline bool floor_needs_scratch(int n, int window) { return 8ull * window + 8ull * n > 200ull * 1024; }
 cudaError_t floor_launch(const FloorLaunch& L, cudaStream_t st);
 cudaError_t prune_launch(const float* raw, int n, float thr, int* active, int* n_active, cudaStream_t st);
 cudaError_t savgol_launch(const float* v, int n, int window, const double* weights, float* out,

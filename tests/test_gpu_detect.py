@@ -228,3 +228,18 @@ def test_all_zero_and_constant_plots(ss, ref):
         dets, tf = ss.sense(x, 1e6, n_fft, rows, return_tf=True)
         exp_tf = ref.make_plots(x, 1e6, n_fft, rows)
         _check(dets[0], ref.detect(exp_tf[0], fs=1e6), tf[0], exp_tf[0])
+
+
+@pytest.mark.parametrize("n_fft,rows", [(16384, 40), (65536, 12)])
+def test_large_fft_detect(ss, ref, n_fft, rows):
+    """Wide plots through the whole chain (large-N FFT, K2 PSD, global-scratch
+    floor for F > 25,000 columns, K4-K6) vs the reference."""
+    rng = np.random.default_rng(n_fft + rows)
+    n = 2 * rows * n_fft
+    x = (rng.normal(size=n) + 1j * rng.normal(size=n)).astype(np.complex64)
+    t = np.arange(n)
+    x[(t // n_fft) % rows > rows // 3] += (6 * np.exp(2j * np.pi * 0.1 * t[(t // n_fft) % rows > rows // 3])).astype(np.complex64)
+    dets, tf = ss.sense(x, 1e6, n_fft, rows, return_tf=True, box_capacity=8192)
+    exp_tf = ref.make_plots(x, 1e6, n_fft, rows)
+    for p, det in enumerate(dets):
+        _check(det, ref.detect(exp_tf[p], start_seq=p * rows, fs=1e6), tf[p], exp_tf[p])

@@ -118,3 +118,28 @@ def test_stft_int16(ss, ora):
     got = ss.stft_plots(raw, 1e6, 1024, 512, 1, 20, fmt=1)
     exp = ora.stft_plot(raw, 1024, 512, 1, 40).reshape(2, 20, 1024)
     assert np.array_equal(got.view(np.uint32), exp.view(np.uint32))
+
+
+@pytest.mark.parametrize("n_fft,rows", [(16384, 6), (32768, 3), (65536, 2), (262144, 1)])
+def test_large_fft_bit_exact(ss, ref, n_fft, rows):
+    """n_fft beyond one CTA's shared memory: the global-memory SSFFT-2 pass chain
+    (fft_mag.cu, large N) against the reference's make_plots."""
+    rng = np.random.default_rng(n_fft)
+    x = _rand_iq(rng, 2 * rows * n_fft + 3)
+    got = ss.make_plots(x, 1e6, n_fft, rows)
+    exp = ref.make_plots(x, 1e6, n_fft, rows)
+    assert got.shape == exp.shape == (2, rows, n_fft)
+    assert np.array_equal(got.view(np.uint32), exp.view(np.uint32))
+
+
+def test_large_fft_int16_and_stft(ss, ref, ora):
+    rng = np.random.default_rng(5)
+    n_fft = 16384
+    raw = rng.integers(-32768, 32768, size=2 * 4 * n_fft, dtype=np.int16)
+    got = ss.make_plots(raw, 1e6, n_fft, 2, fmt=1)
+    as_f32 = (raw.astype(np.float32) * np.float32(1 / 32768)).view(np.complex64)
+    assert np.array_equal(got.view(np.uint32), ref.make_plots(as_f32, 1e6, n_fft, 2).view(np.uint32))
+    x = _rand_iq(rng, 9 * 8192 + n_fft)
+    got = ss.stft_plots(x, 1e6, n_fft, 8192, 1, 5)
+    exp = ora.stft_plot(x, n_fft, 8192, 1, 10).reshape(2, 5, n_fft)
+    assert np.array_equal(got.view(np.uint32), exp.view(np.uint32))
