@@ -158,6 +158,123 @@ static cd* make_table(int n) {
     return tw;
 }
 
+#if defined(__AVX2__) && defined(__FMA__)
+/* AVX2 form of the radix-16 pass: four butterflies per iteration, one per
+   vector lane, every operation the scalar code's (IEEE per lane, the same
+   explicit fma in cmul, no contraction), so the bits are identical; only the
+   CPU baseline gets faster.  Lanes hold butterflies j, j+2, j+1, j+3 (the
+   order unpacklo/hi produce from interleaved complex pairs). */
+#include <immintrin.h>
+typedef struct {
+    __m256d re, im;
+} cv;
+static inline cv cv_add(cv a, cv b) { cv r = {_mm256_add_pd(a.re, b.re), _mm256_add_pd(a.im, b.im)}; return r; }
+static inline cv cv_sub(cv a, cv b) { cv r = {_mm256_sub_pd(a.re, b.re), _mm256_sub_pd(a.im, b.im)}; return r; }
+static inline cv cv_mul(cv a, cv w) {
+    const __m256d t1 = _mm256_mul_pd(a.im, w.im);
+    const __m256d t2 = _mm256_mul_pd(a.im, w.re);
+    cv r = {_mm256_fmadd_pd(a.re, w.re, _mm256_sub_pd(_mm256_setzero_pd(), t1)), _mm256_fmadd_pd(a.re, w.im, t2)};
+    return r;
+}
+static inline cv cv_mi(cv a) { cv r = {a.im, _mm256_sub_pd(_mm256_setzero_pd(), a.re)}; return r; }
+static inline cv cv_w8(cv a) {
+    const __m256d k = _mm256_set1_pd(SS_R2);
+    cv r = {_mm256_mul_pd(_mm256_add_pd(a.re, a.im), k), _mm256_mul_pd(_mm256_sub_pd(a.im, a.re), k)};
+    return r;
+}
+static inline cv cv_w83(cv a) {
+    const __m256d k = _mm256_set1_pd(SS_R2);
+    cv r = {_mm256_mul_pd(_mm256_sub_pd(a.im, a.re), k),
+            _mm256_sub_pd(_mm256_setzero_pd(), _mm256_mul_pd(_mm256_add_pd(a.re, a.im), k))};
+    return r;
+}
+static inline cv cv_set1(cd w) { cv r = {_mm256_set1_pd(w.re), _mm256_set1_pd(w.im)}; return r; }
+static inline void dft4v(cv* t) {
+    const cv t0 = cv_add(t[0], t[2]), t1 = cv_sub(t[0], t[2]);
+    const cv t2 = cv_add(t[1], t[3]), t3 = cv_sub(t[1], t[3]);
+    t[0] = cv_add(t0, t2);
+    t[2] = cv_sub(t0, t2);
+    t[1].re = _mm256_add_pd(t1.re, t3.im);
+    t[1].im = _mm256_sub_pd(t1.im, t3.re);
+    t[3].re = _mm256_sub_pd(t1.re, t3.im);
+    t[3].im = _mm256_add_pd(t1.im, t3.re);
+}
+static void dft16v(cv* v) {
+    cv y[16];
+    for (int n1 = 0; n1 < 4; ++n1) {
+        cv t[4] = {v[n1], v[n1 + 4], v[n1 + 8], v[n1 + 12]};
+        dft4v(t);
+        for (int k2 = 0; k2 < 4; ++k2) y[n1 * 4 + k2] = t[k2];
+    }
+    const cd w1 = {SS_C1, -SS_S1}, w3 = {SS_S1, -SS_C1}, w9 = {-SS_C1, SS_S1};
+    y[5] = cv_mul(y[5], cv_set1(w1));
+    y[6] = cv_w8(y[6]);
+    y[7] = cv_mul(y[7], cv_set1(w3));
+    y[9] = cv_w8(y[9]);
+    y[10] = cv_mi(y[10]);
+    y[11] = cv_w83(y[11]);
+    y[13] = cv_mul(y[13], cv_set1(w3));
+    y[14] = cv_w83(y[14]);
+    y[15] = cv_mul(y[15], cv_set1(w9));
+    for (int k2 = 0; k2 < 4; ++k2) {
+        cv t[4] = {y[k2], y[4 + k2], y[8 + k2], y[12 + k2]};
+        dft4v(t);
+        for (int k1 = 0; k1 < 4; ++k1) v[k2 + 4 * k1] = t[k1];
+    }
+}
+/* one radix-16 Stockham pass (n/16 butterflies, a multiple of 4) */
+static void pass16_avx(const cd* src, cd* dst, int n, int ns, const cd* tw, int step) {
+    const int nr = n / 16;
+    for (int j = 0; j < nr; j += 4) {
+        cv v[16];
+        for (int q = 0; q < 16; ++q) {
+            const double* a = (const double*)(src + j + q * nr);
+            const __m256d lo = _mm256_loadu_pd(a), hi = _mm256_loadu_pd(a + 4);
+            v[q].re = _mm256_unpacklo_pd(lo, hi);  /* butterflies j, j+2, j+1, j+3 */
+            v[q].im = _mm256_unpackhi_pd(lo, hi);
+        }
+        const int k = j % ns;
+        if (ns > 1) {
+            /* ns >= 16 here: the four butterflies share a block, k .. k+3 */
+            const cd a0 = tw[(k + 0) * step], a1 = tw[(k + 1) * step], a2 = tw[(k + 2) * step], a3 = tw[(k + 3) * step];
+            cv w[16];
+            w[1].re = _mm256_set_pd(a3.re, a1.re, a2.re, a0.re);
+            w[1].im = _mm256_set_pd(a3.im, a1.im, a2.im, a0.im);
+            w[2] = cv_mul(w[1], w[1]);
+            w[3] = cv_mul(w[2], w[1]);
+            w[4] = cv_mul(w[2], w[2]);
+            w[5] = cv_mul(w[4], w[1]);
+            w[6] = cv_mul(w[4], w[2]);
+            w[7] = cv_mul(w[4], w[3]);
+            w[8] = cv_mul(w[4], w[4]);
+            for (int q = 9; q < 16; ++q) w[q] = cv_mul(w[8], w[q - 8]);
+            for (int q = 1; q < 16; ++q) v[q] = cv_mul(v[q], w[q]);
+        }
+        dft16v(v);
+        if (ns > 1) {
+            const int base = (j - k) * 16 + k;  /* four consecutive outputs per q */
+            for (int q = 0; q < 16; ++q) {
+                double* o = (double*)(dst + base + q * ns);
+                _mm256_storeu_pd(o, _mm256_unpacklo_pd(v[q].re, v[q].im));
+                _mm256_storeu_pd(o + 4, _mm256_unpackhi_pd(v[q].re, v[q].im));
+            }
+        } else {
+            for (int q = 0; q < 16; ++q) {
+                double re[4], im[4];
+                _mm256_storeu_pd(re, v[q].re);
+                _mm256_storeu_pd(im, v[q].im);
+                static const int lane_of[4] = {0, 2, 1, 3};  /* butterfly j+i sits in lane lane_of[i] */
+                for (int i = 0; i < 4; ++i) {
+                    dst[(j + i) * 16 + q].re = re[lane_of[i]];
+                    dst[(j + i) * 16 + q].im = im[lane_of[i]];
+                }
+            }
+        }
+    }
+}
+#define SSFFT_HAVE_AVX2 1
+#endif
+
 /* Forward power-of-two SSFFT-1; in and out may alias. */
 static void ssfft_forward(int n, const cd* tw, const cd* in, cd* out, cd* scratch) {
     const int m = ilog2(n);
@@ -180,6 +297,16 @@ static void ssfft_forward(int n, const cd* tw, const cd* in, cd* out, cd* scratc
         const int r = radices[p];
         const int nr = n / r;
         const int step = n / (ns * r);
+#ifdef SSFFT_HAVE_AVX2
+        if (r == 16 && nr % 4 == 0 && (ns == 1 || ns >= 16)) {
+            pass16_avx(src, dst, n, ns, tw, step);
+            ns *= r;
+            cd* t = src;
+            src = dst;
+            dst = t;
+            continue;
+        }
+#endif
         for (int j = 0; j < nr; ++j) {
             const int k = j % ns;
             cd v[16];
