@@ -422,6 +422,20 @@ static void small_pow2(int n, int sign, const cd* in, cd* out) {
     for (int i = 0; i < n; ++i) out[i] = v[i];
 }
 
+/* per-thread scratch (2n complex), grown on demand: the reference calls
+   fftw_execute_dft once per row, and a fresh 2n-element malloc per call is an
+   mmap + page faults for n >= 4096 */
+static _Thread_local cd* tls_scratch = NULL;
+static _Thread_local size_t tls_cap = 0;
+static cd* scratch_for(size_t count) {
+    if (count > tls_cap) {
+        free(tls_scratch);
+        tls_scratch = (cd*)malloc(sizeof(cd) * count);
+        tls_cap = tls_scratch ? count : 0;
+    }
+    return tls_scratch;
+}
+
 void fftw_execute_dft(const fftw_plan p, fftw_complex* in_, fftw_complex* out_) {
     const int n = p->n;
     cd* in = (cd*)in_;
@@ -435,7 +449,7 @@ void fftw_execute_dft(const fftw_plan p, fftw_complex* in_, fftw_complex* out_) 
             small_pow2(n, p->sign, in, out);
             return;
         }
-        cd* scratch = (cd*)malloc(sizeof(cd) * 2 * (size_t)n);
+        cd* scratch = scratch_for(2 * (size_t)n);
         if (p->sign < 0) {
             ssfft_forward(n, p->tw, in, out, scratch);
         } else {
@@ -448,7 +462,6 @@ void fftw_execute_dft(const fftw_plan p, fftw_complex* in_, fftw_complex* out_) 
             for (int i = 0; i < n; ++i) out[i].im = -out[i].im;
             free(tmp);
         }
-        free(scratch);
         return;
     }
     /* Bluestein */
