@@ -258,7 +258,7 @@ cudaError_t binarize_tile_launch(const BinarizeLaunch& L, cudaStream_t st);
 
 cudaError_t binarize_launch(const BinarizeLaunch& L, cudaStream_t st) {
     if (L.n_plots <= 0 || L.rows <= 0 || L.cols <= 0) return cudaSuccess;
-    if (L.mask_planes) return binarize_tile_launch(L, st);  // caller checked binarize_tile_ok
+    if (L.mask_bytes) return binarize_tile_launch(L, st);  // caller checked binarize_tile_ok
     const int W = (L.cols + 31) / 32;
     dim3 grid(W, L.n_plots);
     binarize_kernel<<<grid, kBinThreads, 0, st>>>(L);
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     const uint32_t abyte = (a.active_bits[static_cast<long long>(p) * W + grp / 4] >> (8 * (grp & 3))) & 0xffu;
     // byte (grp & 3) of the word-major mask words (grp >> 2, r): the tile path
     // writes the packed mask K5 reads, 4 bytes apart per row
-    uint8_t* plane = a.mask_planes + ((static_cast<long long>(p) * W + (grp >> 2)) * rows_all + rbase) * 4 + (grp & 3);
+    uint8_t* plane = a.mask_bytes + ((static_cast<long long>(p) * W + (grp >> 2)) * rows_all + rbase) * 4 + (grp & 3);
     const int col0 = grp * kTileCols;
     if (abyte == 0) {  // both CTAs of a cluster see the same byte and leave together
         for (int r = tid; r < rows; r += kBinThreads) plane[4 * r] = 0;

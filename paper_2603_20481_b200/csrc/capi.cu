@@ -332,8 +332,8 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
     B.rows = rows;
     B.cols = cols;
     B.active_bits = abits;
-    const bool planes = ssb::binarize_tile_ok(rows, cols);
-    if (planes) B.mask_planes = reinterpret_cast<uint8_t*>(m0);  // the bit mask, written bytewise
+    const bool tile = ssb::binarize_tile_ok(rows, cols);
+    if (tile) B.mask_bytes = reinterpret_cast<uint8_t*>(m0);  // the bit mask, written bytewise
     else B.mask_bits = m0;
     tmark(ctx, 3, 0);
     SS_CK(ctx, ssb::binarize_launch(B, ctx->stream));

@@ -78,14 +78,14 @@ struct BinarizeLaunch {
     int cols = 0;
     const uint32_t* active_bits = nullptr;  // n_plots x W
     uint32_t* mask_bits = nullptr;      // n_plots x W x rows word-major bits (bit mode) or null
-    uint8_t* mask_planes = nullptr;     // tile path: the word-major bit mask as bytes (byte k of word w = columns 32w+8k..+7) or null
+    uint8_t* mask_bytes = nullptr;     // tile path: the word-major bit mask as bytes (byte k of word w = columns 32w+8k..+7) or null
     uint8_t* mask_u8 = nullptr;         // rows x cols (u8 mode, columns [c0,c1)) or null
     int c0 = 0, c1 = 0;                 // u8 mode column range
     float* col_thr = nullptr;           // optional n_plots x cols thresholds (+inf inactive)
     int* col_valid = nullptr;           // optional n_plots x cols: active && non-constant
 };
 cudaError_t binarize_launch(const BinarizeLaunch& L, cudaStream_t st);
-// true when the smem-resident tile kernel (byte-plane output) handles this shape
+// true when the smem-resident tile kernel (bytewise writes into the bit mask) handles this shape
 bool binarize_tile_ok(int rows, int cols);
 
 // ---- K5 morph.cu
@@ -93,9 +93,8 @@ cudaError_t pack_u8_launch(const uint8_t* m, int n_plots, int rows, int cols, ui
                            cudaStream_t st);
 cudaError_t unpack_launch(const uint32_t* bits, int n_plots, int rows, int cols, uint8_t* m,
                           cudaStream_t st);
-// close 3x3 -> open 3x3 -> open 1x3 (3x1 if along_time), bit-packed, fused.
-// Input: row-major bit words `in`, or (when in_planes != null) the byte planes
-// [p][cols/8][rows] the binarize tile kernel writes.
+// close 3x3 -> open 3x3 -> open 1x3 (3x1 if along_time), bit-packed, fused in
+// registers.  in / out: word-major bit masks [p][ceil(cols/32)][rows].
 cudaError_t consolidate_bits_launch(const uint32_t* in, int n_plots, int rows,
                                     int cols, bool along_time, uint32_t* out, cudaStream_t st);
 // Generic single-plot u8 morphology of columns [c0, c1) (stage API): op 0 erode,
