@@ -64,7 +64,7 @@ cudaError_t unpack_launch(const uint32_t* bits, int n_plots, int rows, int cols,
 }
 
 // ------------------------------------------------------------- fused chain
-// Register-resident form: a warp owns a band of kRegRows output rows x 30
+// Register-resident form: a warp owns a band of kRegRows (16) output rows x 30
 // mask words.  Lane l holds word (band*30 + l - 1) for kRegNR = kRegRows +
 // 2*kRegHalo consecutive rows in registers; lanes 0 and 31 are halo words.
 // Vertical erode/dilate is register-to-register (rows i-1, i, i+1 of the same
@@ -74,7 +74,7 @@ cudaError_t unpack_launch(const uint32_t* bits, int n_plots, int rows, int cols,
 // memory, no barriers.  Out-of-image rows and words are zeroed and the last
 // word masked after every step (out-of-image = background for erode and
 // dilate, detector.cpp:359-362, 393-410).
-constexpr int kRegRows = 32;
+constexpr int kRegRows = 16;
 constexpr int kRegHalo = 8;  // >= 6: the largest vertical reach (3x3 close + open + 3x1 line)
 constexpr int kRegNR = kRegRows + 2 * kRegHalo;
 constexpr int kRegOwn = 30;  // owned words per warp
