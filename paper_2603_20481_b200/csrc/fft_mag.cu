@@ -204,10 +204,13 @@ struct StageIssue {
 };
 
 // Store pass PASS's outputs into smem (padded), then load pass PASS+1's
-// inputs, real parts then imaginary parts through one N-double buffer (half
-// the shared memory of a complex exchange).  Barriers are the group's named
-// barrier, so the two row groups of a CTA never wait on each other.
-template <int LOGN, int PASS>
+// inputs.  CX = false: real parts then imaginary parts through one N-double
+// buffer (half the shared memory of a complex exchange, 4 barriers).  CX =
+// true: whole complex values, 16-byte STS/LDS, 2 barriers (the padding keeps
+// both the pass-0 strided stores and the lane-contiguous loads conflict-free).
+// Barriers are the group's named barrier, so the row groups of a CTA never
+// wait on each other.
+template <int LOGN, int PASS, bool CX>
 __device__ __forceinline__ void exchange(cd* v, int j, double* buf, int bar_id, const StageIssue& nxt) {
     using PL = FftPlan<LOGN>;
     constexpr int R = PL::radix(PASS);
@@ -215,40 +218,64 @@ __device__ __forceinline__ void exchange(cd* v, int j, double* buf, int bar_id, 
     constexpr int U = PL::P / R;
     constexpr int R2 = PL::radix(PASS + 1);
     constexpr int U2 = PL::P / R2;
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
+    if constexpr (CX) {
+        double2* cbuf = reinterpret_cast<double2*>(buf);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int b = j + PL::TPR * u;
             const int k = b % NS;
             const int base = (b - k) * R + k;
 #pragma unroll
-            for (int r = 0; r < R; ++r) buf[pad_idx(base + r * NS)] = half ? v[u * R + r].im : v[u * R + r].re;
+            for (int r = 0; r < R; ++r) cbuf[pad_idx(base + r * NS)] = make_double2(v[u * R + r].re, v[u * R + r].im);
         }
         group_sync(bar_id, PL::NT);
-        if (PASS == 0 && half == 0) nxt();
+        if (PASS == 0) nxt();
 #pragma unroll
         for (int u = 0; u < U2; ++u) {
             const int b = j + PL::TPR * u;
 #pragma unroll
             for (int r = 0; r < R2; ++r) {
-                const double x = buf[pad_idx(b + r * (PL::N / R2))];
-                if (half) v[u * R2 + r].im = x;
-                else v[u * R2 + r].re = x;
+                const double2 x = cbuf[pad_idx(b + r * (PL::N / R2))];
+                v[u * R2 + r] = {x.x, x.y};
             }
         }
         group_sync(bar_id, PL::NT);
+    } else {
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int b = j + PL::TPR * u;
+                const int k = b % NS;
+                const int base = (b - k) * R + k;
+#pragma unroll
+                for (int r = 0; r < R; ++r) buf[pad_idx(base + r * NS)] = half ? v[u * R + r].im : v[u * R + r].re;
+            }
+            group_sync(bar_id, PL::NT);
+            if (PASS == 0 && half == 0) nxt();
+#pragma unroll
+            for (int u = 0; u < U2; ++u) {
+                const int b = j + PL::TPR * u;
+#pragma unroll
+                for (int r = 0; r < R2; ++r) {
+                    const double x = buf[pad_idx(b + r * (PL::N / R2))];
+                    if (half) v[u * R2 + r].im = x;
+                    else v[u * R2 + r].re = x;
+                }
+            }
+            group_sync(bar_id, PL::NT);
+        }
     }
 }
 
-template <int LOGN, int PASS, bool TWS>
+template <int LOGN, int PASS, bool TWS, bool CX>
 __device__ __forceinline__ void passes_from(cd* v, int j, const double2* tw, double* buf, int bar_id,
                                             const StageIssue& nxt) {
     using PL = FftPlan<LOGN>;
     run_pass<LOGN, PASS, TWS>(v, j, tw);
     if constexpr (PASS + 1 < PL::NP) {
-        exchange<LOGN, PASS>(v, j, buf, bar_id, nxt);
-        passes_from<LOGN, PASS + 1, TWS>(v, j, tw, buf, bar_id, nxt);
+        exchange<LOGN, PASS, CX>(v, j, buf, bar_id, nxt);
+        passes_from<LOGN, PASS + 1, TWS, CX>(v, j, tw, buf, bar_id, nxt);
     }
 }
 
@@ -323,21 +350,28 @@ struct FftArgs {
 // CTA = GROUPS independent row groups of NT threads.  Each group owns one plot
 // (PSD mode) or a strided set of row iterations, its own exchange buffer, TMA
 // stage, mbarrier and named barrier.  One-row-per-iteration shapes (N >= 4096)
-// keep the per-column PSD accumulators in shared memory (freeing 32 registers
-// for butterfly ILP) and read the pass twiddles through L1; multi-row shapes
-// (N <= 2048) accumulate in registers and share an smem copy of the twiddles.
+// exchange whole complex values (CX) and keep the per-column PSD accumulators
+// in tensor memory (TMEM, otherwise idle here): shared memory holds only the
+// exchange buffer and the IQ stage, registers stay free for butterfly ILP,
+// and the pass twiddles come through L1.  Multi-row shapes (N <= 2048)
+// accumulate in registers and share an smem copy of the twiddles.
 template <int LOGN>
 struct K1Shape {
     using PL = FftPlan<LOGN>;
     static constexpr int GROUPS = LOGN >= 13 ? 1 : 2;
     static constexpr bool TW_SMEM = PL::G > 1;
-    static constexpr bool ACC_SMEM = PL::G == 1;
-    static constexpr int XW = 1;  // doubles per exchange element (re and im go in turn)
+    static constexpr bool CX = PL::G == 1;
+    static constexpr bool ACC_TMEM = PL::G == 1;
+    static constexpr int XW = CX ? 2 : 1;  // doubles per exchange element
     static constexpr int THREADS = PL::NT * GROUPS;
+    static constexpr int WARPS = THREADS / 32;
+    // TMEM: warp w uses lanes 32*(w%4).., columns 32*(w/4) .. +31 (16 doubles)
+    static constexpr int TMEM_COLS = WARPS <= 4 ? 32 : WARPS <= 8 ? 64 : WARPS <= 16 ? 128 : 256;
+    static_assert(!ACC_TMEM || PL::P == 16, "one 32-column TMEM slot holds 16 double accumulators");
     __host__ __device__ static constexpr size_t tw_bytes() { return TW_SMEM ? sizeof(double2) * (PL::tw_size() > 0 ? PL::tw_size() : 1) : 0; }
     __host__ __device__ static constexpr size_t group_bytes(int sample_bytes) {
         return sizeof(double) * XW * PL::G * PL::SROW + static_cast<size_t>(sample_bytes) * PL::G * PL::N +
-               (PL::G > 1 ? sizeof(float) * PL::G * PL::N : 0) + (ACC_SMEM ? sizeof(double) * PL::N : 0);
+               (PL::G > 1 ? sizeof(float) * PL::G * PL::N : 0);
     }
     __host__ __device__ static constexpr size_t smem(int sample_bytes) { return tw_bytes() + GROUPS * group_bytes(sample_bytes); }
 };
@@ -370,7 +404,6 @@ fft_mag_kernel(FftArgs a) {
     double* xbuf = reinterpret_cast<double*>(gbase);                                   // G * SROW
     unsigned char* stage = gbase + sizeof(double) * KS::XW * G * PL::SROW;             // G*N samples
     float* magbuf = reinterpret_cast<float*>(stage + SAMPLE_BYTES * G * N);           // G*N (G > 1)
-    double* sacc = reinterpret_cast<double*>(stage + SAMPLE_BYTES * G * N);           // N (ACC_SMEM)
     double* mybuf = xbuf + KS::XW * g * PL::SROW;
     uint64_t* bar = &bars[gi];
 
@@ -403,20 +436,34 @@ fft_mag_kernel(FftArgs a) {
         mbar_init(bar, 1);
         fence_mbar_init();
     }
-    __syncthreads();  // twiddle copy + mbarrier init visible to all groups
+    // PSD accumulators in TMEM: this thread's 16 columns k(i) are 16 doubles =
+    // 32 consecutive 32-bit TMEM columns of its lane
+    __shared__ uint32_t tmem_slot;
+    const int wid = static_cast<int>(threadIdx.x) >> 5;
+    if constexpr (PSD && KS::ACC_TMEM) {
+        if (wid == 0) tmem_alloc<KS::TMEM_COLS>(&tmem_slot);
+        tmem_fence_before();
+    }
+    __syncthreads();  // twiddle copy + mbarrier init (+ TMEM address) visible to all groups
+    uint32_t taddr = 0;
+    if constexpr (PSD && KS::ACC_TMEM) {
+        tmem_fence_after();
+        taddr = tmem_slot + (static_cast<uint32_t>(32 * (wid & 3)) << 16) + static_cast<uint32_t>(32 * (wid >> 2));
+        uint32_t z[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) z[i] = 0u;  // +0.0 in both halves of every double
+        tmem_st32(taddr, z);
+    }
     if (lt == 0 && it_begin < it_end) {
         StageIssue first{stage, nullptr, 0u, bar, true, true};
         chunk(it_begin, &first.src, &first.bytes);
         first();
     }
 
-    constexpr int NACC = (PSD && !KS::ACC_SMEM) ? (G == 1 ? PL::P : (N >= PL::NT ? N / PL::NT : 1)) : 1;
+    constexpr int NACC = (PSD && !KS::ACC_TMEM) ? (G == 1 ? PL::P : (N >= PL::NT ? N / PL::NT : 1)) : 1;
     double acc[NACC];
 #pragma unroll
     for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
-    if constexpr (PSD && KS::ACC_SMEM) {
-        for (int c = lt; c < N; c += PL::NT) sacc[c] = 0.0;  // each column is owned by one thread
-    }
 
     constexpr int RL = PL::radix(PL::NP - 1);
     constexpr int NSL = PL::ns(PL::NP - 1);
@@ -464,7 +511,7 @@ fft_mag_kernel(FftArgs a) {
             group_sync(bar_id, PL::NT);
             nxt();
         }
-        passes_from<LOGN, 0, KS::TW_SMEM>(v, j, tw, mybuf, bar_id, nxt);
+        passes_from<LOGN, 0, KS::TW_SMEM, KS::CX>(v, j, tw, mybuf, bar_id, nxt);
 
         // epilogue: outputs of the last pass, index q = b + r*NS_last
         float m[PL::P];
@@ -478,14 +525,22 @@ fft_mag_kernel(FftArgs a) {
                     const int q = j + PL::TPR * u + r * NSL;
                     const int k = (q + N / 2) & (N - 1);
                     if (valid && out) out[k] = m[u * RL + r];
-                    if constexpr (PSD) {
-                        if (valid) {
-                            const double md = static_cast<double>(m[u * RL + r]);
-                            if constexpr (KS::ACC_SMEM) sacc[k] = __fma_rn(md, md, sacc[k]);  // column k is this thread's
-                            else acc[u * RL + r] = __fma_rn(md, md, acc[u * RL + r]);
-                        }
-                    }
                 }
+            }
+            if constexpr (PSD) {
+                // G == 1: every row of the iteration space is valid (warp-uniform)
+                uint32_t t[32];
+                tmem_wait_st();  // the previous row's update has landed
+                tmem_ld32(taddr, t);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < PL::P; ++i) {
+                    const double md = static_cast<double>(m[i]);
+                    const double s = __fma_rn(md, md, __hiloint2double(static_cast<int>(t[2 * i + 1]), static_cast<int>(t[2 * i])));
+                    t[2 * i] = static_cast<uint32_t>(__double2loint(s));
+                    t[2 * i + 1] = static_cast<uint32_t>(__double2hiint(s));
+                }
+                tmem_st32(taddr, t);
             }
         } else {
             // stage magnitudes so stores are row-contiguous and PSD runs in row order
@@ -529,13 +584,19 @@ fft_mag_kernel(FftArgs a) {
             const double inv_rows = __ddiv_rn(1.0, static_cast<double>(a.rows_per_plot));
             float* psd = a.psd + plot * N;
             if constexpr (G == 1) {
+                uint32_t t[32];
+                tmem_wait_st();
+                tmem_ld32(taddr, t);
+                tmem_wait_ld();
 #pragma unroll
                 for (int u = 0; u < UL; ++u)
 #pragma unroll
                     for (int r = 0; r < RL; ++r) {
+                        const int i = u * RL + r;
                         const int q = j + PL::TPR * u + r * NSL;
                         const int k = (q + N / 2) & (N - 1);
-                        psd[k] = __double2float_rn(__dmul_rn(KS::ACC_SMEM ? sacc[k] : acc[u * RL + r], inv_rows));
+                        const double sum = __hiloint2double(static_cast<int>(t[2 * i + 1]), static_cast<int>(t[2 * i]));
+                        psd[k] = __double2float_rn(__dmul_rn(sum, inv_rows));
                     }
             } else {
 #pragma unroll
@@ -544,6 +605,13 @@ fft_mag_kernel(FftArgs a) {
                     if (c < N) psd[c] = __double2float_rn(__dmul_rn(acc[i], inv_rows));
                 }
             }
+        }
+        if constexpr (KS::ACC_TMEM) {
+            tmem_wait_st();
+            tmem_fence_before();
+            __syncthreads();  // every warp is done with its columns
+            tmem_fence_after();
+            if (wid == 0) tmem_dealloc<KS::TMEM_COLS>(tmem_slot);
         }
     }
 }
