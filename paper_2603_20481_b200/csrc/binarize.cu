@@ -28,64 +28,109 @@ constexpr int kHistStride = 257;  // padded so column l, bin b hits bank (l + b)
 
 // bin_of (detector.cpp:36-39): trunc(fl(fl(v - lo) * scale)) clamped to 255.
 // y >= 0 here, so trunc = floor, taken as the low mantissa bits of
-// fl_rd(y + 2^23) -- an FP32 add instead of an F2I on the XU pipe.  NaN (only
-// from infinite input, undefined behaviour in the reference) goes to bin 0.
+// fl_rd(y + 2^23) -- an FP32 add instead of an F2I on the XU pipe.  The
+// unsigned clamp also sends NaN / +inf (only from non-finite input, undefined
+// behaviour in the reference) to bin 255, in bounds.
 __device__ __forceinline__ int bin_index(float v, float lo, float scale) {
     const float y = __fmul_rn(__fsub_rn(v, lo), scale);
-    const int b = __float_as_int(__fadd_rd(y, 8388608.0f)) - 0x4B000000;
-    return y == y ? (b > 255 ? 255 : b) : 0;
+    return static_cast<int>(min(static_cast<uint32_t>(__float_as_int(__fadd_rd(y, 8388608.0f))) - 0x4B000000u, 255u));
+}
+
+__device__ __forceinline__ double rcp_newton(double p) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(p));
+#pragma unroll
+    for (int k = 0; k < 2; ++k) r = __fma_rn(r, __fma_rn(-p, r, 1.0), r);
+    return r;
 }
 
 // otsu_split (detector.cpp:43-67) for one column, one warp: lane owns bins
-// 8*lane .. 8*lane+7 (hq).  Integer prefix sums, exact double variances,
-// first maximum.  Returns the split index.
+// 8*lane .. 8*lane+7 (hq).  Counts and bin-weighted sums are integers below
+// 2^53, so their prefix sums are exact in double, in any order.
+//
+// The reference evaluates var_i = ((w0*w1)*(mu0-mu1))*(mu0-mu1) with two
+// divides per split.  Here every split first gets a cheap estimate of the
+// exact rational it rounds, X_i = D^2 / (w0 w1), D = sum0*w1 - sum1*w0
+// (exact in double: |D| < 2^50), with a Newton reciprocal (rel. err. < 2^-38).
+// Rounding analysis of the reference's expression: |var_i - X_i| <= w0 w1
+// 2^-34.4 + 2^-52 X_i (mu's <= 255 carry 2^-53 relative error, the difference
+// at most 3*255 ulps of 2^-53, two rounded products).  So every split whose
+// var_i equals the maximum has estimate >= M - tol with M the largest
+// estimate and tol = M 2^-30 + total^2 2^-34; only those candidates (nearly
+// always one) run the reference's exact divides, and the first maximum among
+// them is the reference's split.  Empty bins i > 0 repeat bin i-1's
+// (w0, sum0), so they can never be the first maximum and are skipped.
 __device__ __forceinline__ int otsu_split_warp(const uint32_t* hq, int lane) {
-    unsigned long long cnt[8], wsum[8];
-    unsigned long long lc = 0, ls = 0;
+    double cnt[8], wsum[8];
+    double lc = 0.0, ls = 0.0;
     uint32_t nz = 0;  // bins whose count is non-zero (or bin 0)
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const int bin = lane * 8 + q;
-        lc += hq[q];
-        ls += static_cast<unsigned long long>(bin) * hq[q];
+        const double h = static_cast<double>(hq[q]);
+        lc = __dadd_rn(lc, h);
+        ls = __fma_rn(static_cast<double>(bin), h, ls);
         cnt[q] = lc;
         wsum[q] = ls;
         nz |= (hq[q] != 0u || bin == 0) ? (1u << q) : 0u;
     }
     // exclusive prefix over lanes of (lc, ls)
-    unsigned long long pc = lc, ps = ls;
+    double pc = lc, ps = ls;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long tc = __shfl_up_sync(0xffffffffu, pc, o);
-        const unsigned long long ts = __shfl_up_sync(0xffffffffu, ps, o);
+        const double tc = __shfl_up_sync(0xffffffffu, pc, o);
+        const double ts = __shfl_up_sync(0xffffffffu, ps, o);
         if (lane >= o) {
-            pc += tc;
-            ps += ts;
+            pc = __dadd_rn(pc, tc);
+            ps = __dadd_rn(ps, ts);
         }
     }
-    const unsigned long long total = __shfl_sync(0xffffffffu, pc, 31);
-    const double sum_all = static_cast<double>(__shfl_sync(0xffffffffu, ps, 31));
-    pc -= lc;
-    ps -= ls;
+    const double total = __shfl_sync(0xffffffffu, pc, 31);
+    const double sum_all = __shfl_sync(0xffffffffu, ps, 31);
+    pc = __dsub_rn(pc, lc);
+    ps = __dsub_rn(ps, ls);
+
+    // estimates
+    double est[8];
+    double m = -1.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const double w0 = __dadd_rn(pc, cnt[q]);
+        const double w1 = __dsub_rn(total, w0);
+        double e = ((nz >> q) & 1u) ? 0.0 : -1.0;
+        if (((nz >> q) & 1u) && w0 > 0.0 && w1 > 0.0) {
+            const double s0 = __dadd_rn(ps, wsum[q]);
+            const double s1 = __dsub_rn(sum_all, s0);
+            const double d = __fma_rn(s0, w1, -__dmul_rn(s1, w0));
+            const double p = __dmul_rn(w0, w1);
+            e = __dmul_rn(__dmul_rn(d, d), rcp_newton(p));
+        }
+        est[q] = e;
+        m = fmax(m, e);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const double floor_v = m - (m * 0x1p-30 + total * total * 0x1p-34);
+
     double best_v = -1.0;
     int best_i = 0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-        const unsigned long long w0 = pc + cnt[q];
-        const unsigned long long w1 = total - w0;
-        // an empty bin i > 0 repeats bin i-1's (w0, sum0), hence its variance:
-        // it can never be the first maximum, so skip its divides
-        double var = ((nz >> q) & 1u) ? 0.0 : -1.0;
-        if (((nz >> q) & 1u) && w0 > 0 && w1 > 0) {
-            const double sum0 = static_cast<double>(ps + wsum[q]);
-            const double mu0 = __ddiv_rn(sum0, static_cast<double>(w0));
-            const double mu1 = __ddiv_rn(__dsub_rn(sum_all, sum0), static_cast<double>(w1));
-            const double d = __dsub_rn(mu0, mu1);
-            var = __dmul_rn(__dmul_rn(__dmul_rn(static_cast<double>(w0), static_cast<double>(w1)), d), d);
-        }
-        if (var > best_v) {
-            best_v = var;
-            best_i = lane * 8 + q;
+        if (est[q] >= floor_v && est[q] >= 0.0) {
+            const double w0 = __dadd_rn(pc, cnt[q]);
+            const double w1 = __dsub_rn(total, w0);
+            double var = 0.0;
+            if (w0 > 0.0 && w1 > 0.0) {
+                const double sum0 = __dadd_rn(ps, wsum[q]);
+                const double mu0 = __ddiv_rn(sum0, w0);
+                const double mu1 = __ddiv_rn(__dsub_rn(sum_all, sum0), w1);
+                const double d = __dsub_rn(mu0, mu1);
+                var = __dmul_rn(__dmul_rn(__dmul_rn(w0, w1), d), d);
+            }
+            if (var > best_v) {
+                best_v = var;
+                best_i = lane * 8 + q;
+            }
         }
     }
     // first maximum across lanes (ties -> lowest split index)
@@ -409,13 +454,13 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
         uint32_t* h = hist + c * kHistStride;
         constexpr int RS = kBinThreads / kTileCols;  // row stride
         int r = tid >> 3;
-        // 4 rows per step: the loads and bin math of a step are independent
-        for (; r + 3 * RS < rows; r += 4 * RS) {
-            int b[4];
+        // 8 rows per step: the loads and bin math of a step are independent
+        for (; r + 7 * RS < rows; r += 8 * RS) {
+            int b[8];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) b[q] = bin_index(bt_vals[(r + q * RS) * kTileCols + c], clo, csc);
+            for (int q = 0; q < 8; ++q) b[q] = bin_index(bt_vals[(r + q * RS) * kTileCols + c], clo, csc);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) atomicAdd(h + b[q], 1u);
+            for (int q = 0; q < 8; ++q) atomicAdd(h + b[q], 1u);
         }
         for (; r < rows; r += RS) atomicAdd(h + bin_index(bt_vals[r * kTileCols + c], clo, csc), 1u);
     }

@@ -95,6 +95,58 @@ def test_otsu_exact(ss, ref):
             assert np.float32(got[1]).view(np.uint32) == np.float32(exp[1]).view(np.uint32), trial
 
 
+def test_otsu_ties_and_flat_objectives(ss, ref):
+    """The device evaluates the reference's exact divides only for splits whose
+    cheap estimate is within a proven bound of the maximum (binarize.cu,
+    otsu_split_warp): histograms with exact ties, symmetric and near-flat
+    objectives, lone outliers and tall columns must still give the
+    reference's first maximum."""
+    rng = np.random.default_rng(4141)
+    cases = []
+    for a in (1, 2, 3, 7, 50, 400):
+        for b in (1, 2, 5, 50, 300):
+            # symmetric 4-level columns: mirrored splits tie exactly
+            cases.append(np.repeat(np.float32([0, 1, 2, 3]), [a, b, b, a]))
+            cases.append(np.repeat(np.float32([0, 85, 170, 255]), [a, b, b, a]))
+    for n in (2, 3, 10, 999, 5000, 12288):
+        cases.append(np.r_[np.zeros(n - 1), [1.0]].astype(np.float32))   # lone outlier
+        cases.append(np.r_[[0.0], np.ones(n - 1)].astype(np.float32))
+        cases.append(np.linspace(0, 1, n, dtype=np.float32))               # flat-ish objective
+        cases.append((np.arange(n) % 2).astype(np.float32))                # two equal classes
+    for _ in range(150):
+        n = int(rng.integers(2, 12289))
+        k = int(rng.integers(2, 9))
+        levels = np.sort(rng.choice(256, size=k, replace=False)).astype(np.float32)
+        if rng.random() < 0.5:
+            levels[0], levels[-1] = 0, 255
+        counts = rng.multinomial(n, np.ones(k) / k)
+        v = np.repeat(levels, counts)
+        if v.max() > v.min():
+            cases.append(rng.permutation(v).astype(np.float32))
+    for _ in range(60):  # wide rayleigh columns like the C5 plots
+        n = int(rng.integers(100, 12289))
+        cases.append(np.abs(rng.normal(size=n) + 1j * rng.normal(size=n)).astype(np.float32) * 37.0)
+    for i, v in enumerate(cases):
+        got, exp = ss.otsu_threshold(v), ref.otsu_threshold(v)
+        assert got[0] == exp[0], i
+        if exp[0]:
+            assert np.float32(got[1]).view(np.uint32) == np.float32(exp[1]).view(np.uint32), i
+    # the same columns through the batched tile kernel (the detect path): lifted
+    # by 2^10 (exact, keeps every tie) over unit-Rayleigh noise columns so the
+    # PSD prune keeps them active
+    rows = 2441
+    cols = [np.resize(rng.permutation(c), rows) for c in cases[:256]]
+    noise = [np.abs(rng.normal(size=rows) + 1j * rng.normal(size=rows)) for _ in range(256)]
+    tf = np.empty((rows, 512), np.float32)
+    tf[:, 0::2] = np.stack(cols, axis=1) * np.float32(1024.0)
+    tf[:, 1::2] = np.stack(noise, axis=1)
+    cfg = ss.DetectorConfig(psd_margin_db=0.0, min_component_area=1)
+    got = ss.detect(tf, cfg)
+    exp = ref.detect(tf, margin_db=0.0, min_area=1)
+    assert np.array_equal(got.active_columns, exp["active"])
+    assert np.array_equal(got.bin_boxes, exp["bin_boxes"])
+
+
 def test_binarize_exact(ss, ref):
     rng = np.random.default_rng(47)
     assert not ss.binarize(random_plot(rng, 12, 10), []).any()
