@@ -377,7 +377,6 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     // ---- sweep A: two threads per row, one float4 (4 columns) each; fminf /
     // fmaxf equal std::min / std::max here (NaN is never taken by either, and
     // the sign of a zero extreme never reaches an output)
-    const int c = tid & 7;
     {
         const int hh = tid & 1;
         float lo4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
@@ -448,21 +447,42 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     }
     __syncthreads();
 
-    // ---- sweep B: histograms from shared memory
-    if (c_use[c]) {
-        const float clo = c_lo[c], csc = c_scale[c];
-        uint32_t* h = hist + c * kHistStride;
-        constexpr int RS = kBinThreads / kTileCols;  // row stride
-        int r = tid >> 3;
-        // 8 rows per step: the loads and bin math of a step are independent
-        for (; r + 7 * RS < rows; r += 8 * RS) {
-            int b[8];
+    // ---- sweep B: histograms from shared memory.  Two threads per row, one
+    // float4 (4 columns) each, as in sweep A: one LDS.128 per 4 values and
+    // the per-column constants in registers.  Branch-free: a column that is
+    // not binarised (inactive or constant) still counts into its own
+    // histogram (bin_index stays in [0, 255] for any input), which Otsu then
+    // ignores
+    {
+        const int hh = tid & 1;
+        float clo[4], csc[4];
+        uint32_t* hc[4];
+        bool any = false;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) b[q] = bin_index(bt_vals[(r + q * RS) * kTileCols + c], clo, csc);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) atomicAdd(h + b[q], 1u);
+        for (int q = 0; q < 4; ++q) {
+            const int cc = 4 * hh + q;
+            clo[q] = c_lo[cc];
+            csc[q] = c_scale[cc];
+            hc[q] = hist + cc * kHistStride;
+            any |= c_use[cc] != 0;
         }
-        for (; r < rows; r += RS) atomicAdd(h + bin_index(bt_vals[r * kTileCols + c], clo, csc), 1u);
+        if (any) {
+            constexpr int RS = kBinThreads / 2;  // row stride
+            int r = tid >> 1;
+            for (; r + RS < rows; r += 2 * RS) {
+                const float4 x0 = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols + 4 * hh);
+                const float4 x1 = *reinterpret_cast<const float4*>(bt_vals + (r + RS) * kTileCols + 4 * hh);
+                const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+                for (int q = 0; q < 8; ++q) atomicAdd(hc[q & 3] + bin_index(xv[q], clo[q & 3], csc[q & 3]), 1u);
+            }
+            if (r < rows) {
+                const float4 x0 = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols + 4 * hh);
+                const float xv[4] = {x0.x, x0.y, x0.z, x0.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) atomicAdd(hc[q] + bin_index(xv[q], clo[q], csc[q]), 1u);
+            }
+        }
     }
     __syncthreads();
 
