@@ -17,6 +17,8 @@
 #include "internal.h"
 
 #include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 namespace cg = cooperative_groups;
 
@@ -315,21 +317,27 @@ cudaError_t binarize_launch(const BinarizeLaunch& L, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // binarize_tile_kernel: the batch path for plots of <= kTileMaxRows rows.
 // One CTA per (plot, 8-column group): the group's T x 8 values (32 bytes per
-// row) are pulled into shared memory once with cp.async (LDGSTS, 16-byte,
-// L1-bypassing; the whole column block in flight at once), and sweeps A/B/C
-// run from shared memory -- one HBM read of the active columns in total.
+// row) are pulled into shared memory once by TMA (a 3-D tensor map over the
+// TF batch, one 8 x 256-row box per mbarrier, all boxes in flight at once,
+// issued by one thread), and sweeps A/B/C run from shared memory -- one HBM
+// read of the active columns in total; sweep A consumes each box as it lands.
 // The output byte (8 mask bits) lands in the bit-packed mask word in place
 // (little-endian: byte g of word w = columns 32w + 8g .. +7).
 constexpr int kTileCols = 8;
 constexpr int kTileMaxRows = 6144;
+constexpr int kBox = 256;  // rows per TMA box (the box-dimension limit)
+static_assert(kTileMaxRows % kBox == 0, "whole boxes");
 
 namespace ssb {
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+// TMA tile load of box (8 columns x kBox rows x 1 plot) at (c0, r0, p) of the
+// [plots][rows][cols] fp32 TF tensor, completion counted on `bar`
+__device__ __forceinline__ void tma_load_box(void* dst, const CUtensorMap* map, int c0, int r0, int p, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(p), "r"(smem_u32(bar))
+        : "memory");
 }
 
 // NSPLIT = 2: a 2-CTA cluster shares one column group, each CTA holding half
@@ -337,8 +345,9 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // column extremes and histograms are combined through distributed shared
 // memory, and both CTAs run the same Otsu on the summed histograms.
 template <int NSPLIT>
-__global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaunch a) {
-    extern __shared__ __align__(16) float bt_vals[];      // (rows / NSPLIT) x 8
+__global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaunch a, const __grid_constant__ CUtensorMap tmap) {
+    extern __shared__ __align__(128) float bt_vals[];     // (rows / NSPLIT, rounded up to kBox) x 8
+    __shared__ __align__(8) uint64_t box_bar[kTileMaxRows / kBox];
     __shared__ uint32_t hist[kTileCols * kHistStride];
     __shared__ float s_lo[kBinWarps][kTileCols], s_hi[kBinWarps][kTileCols];
     __shared__ float part_lo[kTileCols], part_hi[kTileCols];
@@ -364,15 +373,19 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
         for (int r = tid; r < rows; r += kBinThreads) plane[4 * r] = 0;
         return;
     }
-    // ---- load the block (2 x 16 B per row)
-    const float* src = a.tf + (static_cast<long long>(p) * rows_all + rbase) * cols + col0;
-    for (int e = tid; e < 2 * rows; e += kBinThreads) {
-        const int r = e >> 1, h = e & 1;
-        cp_async16(bt_vals + r * kTileCols + 4 * h, src + static_cast<long long>(r) * cols + 4 * h);
+    // ---- load the block: one TMA box per kBox rows (32 B x kBox), each on its
+    // own mbarrier, so sweep A starts on the first box while the rest land
+    const int nbox = (rows + kBox - 1) / kBox;
+    if (tid == 0) {
+        for (int b = 0; b < nbox; ++b) mbar_init(&box_bar[b], 1);
+        fence_mbar_init();
+        for (int b = 0; b < nbox; ++b) {
+            mbar_arrive_expect_tx(&box_bar[b], kBox * kTileCols * sizeof(float));
+            tma_load_box(bt_vals + b * kBox * kTileCols, &tmap, col0, rbase + b * kBox, p, &box_bar[b]);
+        }
     }
     for (int i = tid; i < kTileCols * kHistStride; i += kBinThreads) hist[i] = 0;
-    cp_async_wait_all();
-    __syncthreads();
+    __syncthreads();  // mbarrier init visible
 
     // ---- sweep A: two threads per row, one float4 (4 columns) each; fminf /
     // fmaxf equal std::min / std::max here (NaN is never taken by either, and
@@ -381,12 +394,16 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
         const int hh = tid & 1;
         float lo4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
         float hi4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-        for (int r = tid >> 1; r < rows; r += kBinThreads / 2) {
-            const float4 x = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols + 4 * hh);
-            lo4[0] = fminf(lo4[0], x.x); hi4[0] = fmaxf(hi4[0], x.x);
-            lo4[1] = fminf(lo4[1], x.y); hi4[1] = fmaxf(hi4[1], x.y);
-            lo4[2] = fminf(lo4[2], x.z); hi4[2] = fmaxf(hi4[2], x.z);
-            lo4[3] = fminf(lo4[3], x.w); hi4[3] = fmaxf(hi4[3], x.w);
+        for (int b = 0; b < nbox; ++b) {
+            mbar_wait(&box_bar[b], 0);
+            const int rend = min(rows, (b + 1) * kBox);
+            for (int r = b * kBox + (tid >> 1); r < rend; r += kBinThreads / 2) {
+                const float4 x = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols + 4 * hh);
+                lo4[0] = fminf(lo4[0], x.x); hi4[0] = fmaxf(hi4[0], x.x);
+                lo4[1] = fminf(lo4[1], x.y); hi4[1] = fmaxf(hi4[1], x.y);
+                lo4[2] = fminf(lo4[2], x.z); hi4[2] = fmaxf(hi4[2], x.z);
+                lo4[3] = fminf(lo4[3], x.w); hi4[3] = fmaxf(hi4[3], x.w);
+            }
         }
 #pragma unroll
         for (int o = 2; o < 32; o <<= 1)
@@ -535,10 +552,33 @@ constexpr int kTileSplitRows = 3264;
 
 bool binarize_tile_ok(int rows, int cols) { return cols % 32 == 0 && rows <= 2 * kTileMaxRows && rows > 0; }
 
+// The [plots][rows][cols] fp32 TF tensor as a TMA tensor map with 8 x kBox x 1
+// boxes (rows past the end of a plot read as zeros and are never used).
+static cudaError_t make_tf_map(const BinarizeLaunch& L, CUtensorMap* map) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        const cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(L.cols), static_cast<cuuint64_t>(L.rows),
+                                static_cast<cuuint64_t>(L.n_plots)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(L.cols) * sizeof(float),
+                                   static_cast<cuuint64_t>(L.rows) * L.cols * sizeof(float)};
+    const cuuint32_t box[3] = {kTileCols, kBox, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(L.tf), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 cudaError_t binarize_tile_launch(const BinarizeLaunch& L, cudaStream_t st) {
     const int split = L.rows > kTileSplitRows ? 2 : 1;
     const int rows_cta = (L.rows + split - 1) / split;
-    const size_t smem = sizeof(float) * kTileCols * static_cast<size_t>(rows_cta);
+    const size_t smem = sizeof(float) * kTileCols * static_cast<size_t>((rows_cta + kBox - 1) / kBox * kBox);
     static bool attr_set[2] = {false, false};
     if (!attr_set[split - 1]) {
         cudaError_t e = split == 1 ? cudaFuncSetAttribute(binarize_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -548,9 +588,12 @@ cudaError_t binarize_tile_launch(const BinarizeLaunch& L, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         attr_set[split - 1] = true;
     }
+    CUtensorMap map;
+    const cudaError_t me = make_tf_map(L, &map);
+    if (me != cudaSuccess) return me;
     if (split == 1) {
         dim3 grid(L.cols / kTileCols, L.n_plots);
-        binarize_tile_kernel<1><<<grid, kBinThreads, smem, st>>>(L);
+        binarize_tile_kernel<1><<<grid, kBinThreads, smem, st>>>(L, map);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg = {};
@@ -565,7 +608,7 @@ cudaError_t binarize_tile_launch(const BinarizeLaunch& L, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, binarize_tile_kernel<2>, L);
+    return cudaLaunchKernelEx(&cfg, binarize_tile_kernel<2>, L, map);
 }
 
 } // namespace ssb
