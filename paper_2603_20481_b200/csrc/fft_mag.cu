@@ -139,12 +139,49 @@ struct FftPlan {
 
 __device__ __forceinline__ int pad_idx(int i) { return i + (i >> 4); }
 
-// Twiddle + butterflies of pass p on register data already holding this
-// pass's inputs: butterfly b_u = j + TPR*u owns v[u*R .. u*R+R-1].
+// SSFFT-2 twiddles of pass PASS for this thread's butterflies b_u = j + TPR*u:
+// w1 from the table, higher powers by a fixed product tree -- one table load
+// per butterfly instead of R-1 (the loads, not the multiplies, were the cost:
+// DESIGN.md §4).  w[u*R + r] = w1^r (r >= 1).
 template <int LOGN, int PASS, bool TWS>
-__device__ __forceinline__ void run_pass(cd* v, int j, const double2* __restrict__ tw) {
+__device__ __forceinline__ void pass_twiddles(int j, const double2* __restrict__ tw, cd* w) {
     // tw points at the CTA's shared-memory copy of the pass tables (plain
-    // loads -> LDS.128) or, for N = 8192, at the global table
+    // loads -> LDS.128) or, for N >= 4096, at the global table (L1)
+    using PL = FftPlan<LOGN>;
+    constexpr int R = PL::radix(PASS);
+    constexpr int NS = PL::ns(PASS);
+    constexpr int U = PL::P / R;
+    if constexpr (NS > 1) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int b = j + PL::TPR * u;
+            const int k = b % NS;
+            const double2* t = tw + PL::tw_off(PASS) + k;
+            const double2 w1t = TWS ? t[0] : __ldg(t);
+            cd* x = w + u * R;
+            x[1] = cd{w1t.x, w1t.y};
+            if constexpr (R > 2) x[2] = c_mul(x[1], x[1]);
+            if constexpr (R > 3) x[3] = c_mul(x[2], x[1]);
+            if constexpr (R > 4) {
+                x[4] = c_mul(x[2], x[2]);
+                x[5] = c_mul(x[4], x[1]);
+                x[6] = c_mul(x[4], x[2]);
+                x[7] = c_mul(x[4], x[3]);
+            }
+            if constexpr (R > 8) {
+                x[8] = c_mul(x[4], x[4]);
+#pragma unroll
+                for (int q = 9; q < 16; ++q) x[q] = c_mul(x[8], x[q - 8]);
+            }
+        }
+    }
+}
+
+// Twiddle + butterflies of pass p on register data already holding this
+// pass's inputs: butterfly b_u = j + TPR*u owns v[u*R .. u*R+R-1]; w from
+// pass_twiddles.
+template <int LOGN, int PASS>
+__device__ __forceinline__ void run_pass(cd* v, const cd* w) {
     using PL = FftPlan<LOGN>;
     constexpr int R = PL::radix(PASS);
     constexpr int NS = PL::ns(PASS);
@@ -152,30 +189,8 @@ __device__ __forceinline__ void run_pass(cd* v, int j, const double2* __restrict
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         if constexpr (NS > 1) {
-            const int b = j + PL::TPR * u;
-            const int k = b % NS;
-            const double2* t = tw + PL::tw_off(PASS) + k;
-            // SSFFT-2: w1 from the table, higher powers by a fixed product
-            // tree -- one table load per butterfly instead of R-1 (the loads,
-            // not the multiplies, were the cost: DESIGN.md §4)
-            const double2 w1t = TWS ? t[0] : __ldg(t);
-            cd w[16];
-            w[1] = cd{w1t.x, w1t.y};
-            if constexpr (R > 2) w[2] = c_mul(w[1], w[1]);
-            if constexpr (R > 3) w[3] = c_mul(w[2], w[1]);
-            if constexpr (R > 4) {
-                w[4] = c_mul(w[2], w[2]);
-                w[5] = c_mul(w[4], w[1]);
-                w[6] = c_mul(w[4], w[2]);
-                w[7] = c_mul(w[4], w[3]);
-            }
-            if constexpr (R > 8) {
-                w[8] = c_mul(w[4], w[4]);
 #pragma unroll
-                for (int q = 9; q < 16; ++q) w[q] = c_mul(w[8], w[q - 8]);
-            }
-#pragma unroll
-            for (int r = 1; r < R; ++r) v[u * R + r] = c_mul(v[u * R + r], w[r]);
+            for (int r = 1; r < R; ++r) v[u * R + r] = c_mul(v[u * R + r], w[u * R + r]);
         }
         dft_r<R>(v + u * R);
     }
@@ -210,8 +225,9 @@ struct StageIssue {
 // both the pass-0 strided stores and the lane-contiguous loads conflict-free).
 // Barriers are the group's named barrier, so the row groups of a CTA never
 // wait on each other.
-template <int LOGN, int PASS, bool CX>
-__device__ __forceinline__ void exchange(cd* v, int j, double* buf, int bar_id, const StageIssue& nxt) {
+template <int LOGN, int PASS, bool CX, bool TWS>
+__device__ __forceinline__ void exchange(cd* v, int j, double* buf, int bar_id, const StageIssue& nxt,
+                                         const double2* tw, cd* wn) {
     using PL = FftPlan<LOGN>;
     constexpr int R = PL::radix(PASS);
     constexpr int NS = PL::ns(PASS);
@@ -228,6 +244,9 @@ __device__ __forceinline__ void exchange(cd* v, int j, double* buf, int bar_id, 
 #pragma unroll
             for (int r = 0; r < R; ++r) cbuf[pad_idx(base + r * NS)] = make_double2(v[u * R + r].re, v[u * R + r].im);
         }
+        // the data registers are free until the loads: the next pass's
+        // twiddle tree fills the wait for the slowest warp of the group
+        pass_twiddles<LOGN, PASS + 1, TWS>(j, tw, wn);
         group_sync(bar_id, PL::NT);
         if (PASS == 0) nxt();
 #pragma unroll
@@ -265,17 +284,19 @@ __device__ __forceinline__ void exchange(cd* v, int j, double* buf, int bar_id, 
             }
             group_sync(bar_id, PL::NT);
         }
+        pass_twiddles<LOGN, PASS + 1, TWS>(j, tw, wn);
     }
 }
 
 template <int LOGN, int PASS, bool TWS, bool CX>
 __device__ __forceinline__ void passes_from(cd* v, int j, const double2* tw, double* buf, int bar_id,
-                                            const StageIssue& nxt) {
+                                            const StageIssue& nxt, const cd* w) {
     using PL = FftPlan<LOGN>;
-    run_pass<LOGN, PASS, TWS>(v, j, tw);
+    run_pass<LOGN, PASS>(v, w);
     if constexpr (PASS + 1 < PL::NP) {
-        exchange<LOGN, PASS, CX>(v, j, buf, bar_id, nxt);
-        passes_from<LOGN, PASS + 1, TWS, CX>(v, j, tw, buf, bar_id, nxt);
+        cd wn[16];
+        exchange<LOGN, PASS, CX, TWS>(v, j, buf, bar_id, nxt, tw, wn);
+        passes_from<LOGN, PASS + 1, TWS, CX>(v, j, tw, buf, bar_id, nxt, wn);
     }
 }
 
@@ -511,7 +532,8 @@ fft_mag_kernel(FftArgs a) {
             group_sync(bar_id, PL::NT);
             nxt();
         }
-        passes_from<LOGN, 0, KS::TW_SMEM, KS::CX>(v, j, tw, mybuf, bar_id, nxt);
+        cd w0[16];  // pass 0 has no twiddles (Ns = 1)
+        passes_from<LOGN, 0, KS::TW_SMEM, KS::CX>(v, j, tw, mybuf, bar_id, nxt, w0);
 
         // epilogue: outputs of the last pass, index q = b + r*NS_last
         float m[PL::P];
