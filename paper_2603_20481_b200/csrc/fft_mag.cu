@@ -493,7 +493,7 @@ fft_mag_kernel(FftArgs a) {
     for (long long it = it_begin; it < it_end; it += it_step) {
         const long long r0 = row_base + it * G;
         const long long row = r0 + g;
-        const bool valid = row < row_limit;
+        const bool valid = G == 1 || row < row_limit;  // G == 1: the iteration space is exactly the rows
 
         mbar_wait(bar, phase);
         phase ^= 1;
