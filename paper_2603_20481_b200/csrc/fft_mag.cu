@@ -311,9 +311,10 @@ __device__ __forceinline__ double rsqrt_seed(double x) {
 // step in double gives sqrt(q) within 2^12.6 double ulps; when that estimate
 // is more than 2^16 ulps from a float rounding midpoint (low 29 mantissa bits
 // vs 2^28), rounding it to float equals rounding the correctly rounded double
-// sqrt (no midpoint lies between them).  Otherwise (p ~ 2^-12) and for q outside
-// [2^-120, 2^120], the IEEE __dsqrt_rn + F2F.  *fbits gets the float's bits;
-// returns true on the fast path (result a normal float).
+// sqrt (no midpoint lies between them); the rounding itself is one
+// F2F.F32.F64 (conversion unit, off the FP64 pipe).  A normal float result
+// also proves q far from the seed's flush range and from overflow.  Otherwise
+// (p ~ 2^-12, or zero / subnormal / huge magnitudes) the IEEE __dsqrt_rn + F2F.
 // Magnitudes of the thread's P outputs, branch-free on the fast path; lanes
 // flagged in the warp-uniform slow pass redo theirs with __dsqrt_rn.
 // SH: the transform ran on inputs scaled by 2^SH (int16 IQ without its exact
@@ -329,20 +330,20 @@ __device__ __forceinline__ void mags(const cd* v, float* m) {
         const double y = rsqrt_seed(q);
         const double s0 = __dmul_rn(q, y);
         const double d = __fma_rn(-s0, s0, q);
-        // y/2 by an exponent decrement and the range / midpoint checks and the
-        // final float rounding on the integer pipe: the FP64 pipe keeps only
-        // the 5 arithmetic ops (F2F.F32.F64 runs at 14/clk/SM, tools/pipe_probe)
+        // y/2 by an exponent decrement (integer pipe): the FP64 pipe keeps only
+        // the 5 arithmetic ops
         const double h = __hiloint2double(__double2hiint(y) - (1 << 20), __double2loint(y));
         const double s1 = __fma_rn(d, h, s0);
         const uint32_t hi = static_cast<uint32_t>(__double2hiint(s1));
         const uint32_t lo = static_cast<uint32_t>(__double2loint(s1));
-        const int dist = static_cast<int>(lo & 0x1FFFFFFFu) - (1 << 28);
-        const uint32_t qe = static_cast<uint32_t>(__double2hiint(q)) >> 20;  // q >= 0: biased exponent
-        const bool ok = (qe - (1023u - 120u + 2u * SH)) <= 240u && (dist > 65536 || dist < -65536);
-        // s1 in [2^-60, 2^60]: float exponent = double exponent - 896, mantissa
-        // = top 23 bits, +1 ulp when the dropped 29 bits exceed half (no ties here)
-        const uint32_t fb = ((hi - ((896u + SH) << 20)) << 3) | (lo >> 29);
-        m[i] = __uint_as_float(fb + (dist > 0 ? 1u : 0u));
+        // float rounding by F2F.F32.F64 (the conversion unit); 2^-SH as an
+        // exponent decrement first.  Fast path valid when the result is a
+        // normal float (q far from the rsqrt seed's flush range, no overflow)
+        // and s1 is > 2^16 ulps from a float rounding midpoint
+        const uint32_t mid = (lo & 0x1FFFFFFFu) + (65536u - (1u << 28));  // > 131072: |dist| > 65536
+        const float mf = __double2float_rn(SH ? __hiloint2double(static_cast<int>(hi - (SH << 20)), static_cast<int>(lo)) : s1);
+        const bool ok = (__float_as_uint(mf) - 0x00800000u) < (0x7f800000u - 0x00800000u) && mid > 131072u;
+        m[i] = mf;
         slow |= ok ? 0u : (1u << i);
     }
     if (__any_sync(0xffffffffu, slow != 0)) {
