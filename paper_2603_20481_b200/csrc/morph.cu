@@ -108,11 +108,23 @@ struct RegBand {
             x[i] = erode ? (v & left & right) : (v | left | right);
         }
     }
-    // one erosion / dilation: 3x3 (vert then horiz), 3x1 (vert), 1x3 (horiz)
+    // one erosion / dilation: 3x3 (vert then horiz), 3x1 (vert), 1x3 (horiz);
+    // CLIP = false for bands with every row and word inside the image
+    template <bool CLIP>
     __device__ __forceinline__ void step(bool erode, bool v, bool h) {
         if (v) vert(erode);
         if (h) horiz(erode);
-        clip();
+        if (CLIP) clip();
+    }
+    template <bool CLIP>
+    __device__ __forceinline__ void chain(bool along_time) {
+        if (CLIP) clip();
+        step<CLIP>(false, true, true);  // close 3x3: dilate, erode
+        step<CLIP>(true, true, true);
+        step<CLIP>(true, true, true);   // open 3x3: erode, dilate
+        step<CLIP>(false, true, true);
+        step<CLIP>(true, along_time, !along_time);  // open with the line element
+        step<CLIP>(false, along_time, !along_time);
     }
 };
 
@@ -136,13 +148,10 @@ __global__ void __launch_bounds__(128) consolidate_kernel(const uint32_t* __rest
     const uint32_t* src = in + (static_cast<long long>(p) * W + (wvalid ? gw : 0)) * rows + row0;
 #pragma unroll
     for (int i = 0; i < kRegNR; ++i) t.x[i] = (wvalid && i >= t.lo && i < t.hi) ? __ldg(src + i) : 0u;
-    t.clip();
-    t.step(false, true, true);  // close 3x3: dilate, erode
-    t.step(true, true, true);
-    t.step(true, true, true);   // open 3x3: erode, dilate
-    t.step(false, true, true);
-    t.step(true, along_time, !along_time);  // open with the line element
-    t.step(false, along_time, !along_time);
+    // interior bands (most of a plot) skip the out-of-image clipping entirely
+    const bool interior = t.lo == 0 && t.hi == kRegNR && t.wmask == 0xffffffffu;
+    if (__all_sync(0xffffffffu, interior)) t.chain<false>(along_time);
+    else t.chain<true>(along_time);
     if (!wvalid || lane == 0 || lane == 31) return;
     uint32_t* dst = out + (static_cast<long long>(p) * W + gw) * rows + r0;
     const int nrow = min(kRegRows, rows - r0);
