@@ -538,6 +538,14 @@ fft_mag_kernel(FftArgs a) {
 
         // epilogue: outputs of the last pass, index q = b + r*NS_last
         float m[PL::P];
+        // G == 1 PSD: the TMEM load of this thread's column sums is issued
+        // before the magnitudes, so its latency overlaps them (measured:
+        // -1 % vs after the stores)
+        uint32_t t[32];
+        if constexpr (G == 1 && PSD) {
+            tmem_wait_st();  // the previous row's update has landed
+            tmem_ld32(taddr, t);
+        }
         mags<PL::P, FMT == 1 ? 15 : 0>(v, m);
         if constexpr (G == 1) {
             float* out = a.tf ? a.tf + row * N : nullptr;
@@ -552,9 +560,6 @@ fft_mag_kernel(FftArgs a) {
             }
             if constexpr (PSD) {
                 // G == 1: every row of the iteration space is valid (warp-uniform)
-                uint32_t t[32];
-                tmem_wait_st();  // the previous row's update has landed
-                tmem_ld32(taddr, t);
                 tmem_wait_ld();
 #pragma unroll
                 for (int i = 0; i < PL::P; ++i) {
