@@ -246,6 +246,7 @@ int claim_bank(ss_engine* e, uint64_t w, std::unique_lock<std::mutex>& lk) {
             return -1;
         }
         e->released.wait(lk);
+        if (e->finished) return -1;  // finish() / abort while waiting: drop the rows
     }
 }
 
@@ -506,6 +507,7 @@ ss_status ss_engine_finish(ss_engine* e) {
             if (b.state == BankState::Filling) b.state = BankState::Free;  // partial tail window
     }
     e->ready.notify_all();
+    e->released.notify_all();  // a push blocked on a held bank (reader gone) returns
     return SS_OK;
 }
 

@@ -130,7 +130,7 @@ RunReport run(frontend::ChunkSource& source, const frontend::FrontendConfig& fc,
     rc.validate();
     const int F = fc.n_fft, T = fc.plot_rows;
     const double deadline = rc.deadline_s > 0.0 ? rc.deadline_s : fc.plot_span_s();
-    constexpr int kCap = 4096;  // boxes kept per window
+    constexpr int kCap = 16384;  // boxes kept per window
 
     ss_engine_cfg ec{};
     ec.n_fft = F;

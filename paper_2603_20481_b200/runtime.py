@@ -46,7 +46,7 @@ class RuntimeConfig:
     chunk_queue_capacity: int = 0
     deadline_s: float = 0.0
     n_banks: int = 2
-    box_capacity: int = 1024
+    box_capacity: int = 16384
 
     def validate(self):
         if self.n_compute_workers < 1 or self.n_sensing_workers < 1:
@@ -321,6 +321,7 @@ def run(source, frontend_config: FrontendConfig, detector_config: DetectorConfig
     th = threading.Thread(target=ingest, daemon=True)
     th.start()
     records = []
+    ok = False
     try:
         if G == 1:
             while (got := eng.poll(-1)) is not None:
@@ -341,7 +342,19 @@ def run(source, frontend_config: FrontendConfig, detector_config: DetectorConfig
                     records.append(got[0])
                     if on_detections is not None:
                         on_detections(got[0], got[1])
+        ok = True
     finally:
+        if not ok:
+            # the manager failed (handler error, capacity): end the stream so a
+            # push blocked on a held bank returns, and drain what is in flight
+            # (runtime.cpp:466-478 rethrows after joining the workers)
+            for e_ in engines:
+                try:
+                    e_.finish()
+                    while e_.poll(-1) is not None:
+                        pass
+                except Exception:  # noqa: BLE001
+                    pass
         th.join()
     if errors:
         raise Error(f"engine aborted, {errors[0]}")

@@ -166,6 +166,28 @@ def test_run_report_and_handler(ss, ref):
         assert np.array_equal(seen[w][:, :2], d.boxes[:, :2])
 
 
+def test_run_aborts_cleanly_on_manager_error(ref):
+    """A failing detection handler (or a window over the box capacity) must end
+    run() with the error, not deadlock: the unpaced ingest thread is then
+    blocked on a bank only the (gone) reader would release.  runtime.cpp:466-478
+    rethrows worker failures after joining."""
+    iq = _stream(ref, 3 * T)
+
+    def handler(r, b):
+        if r.plot_index == 1:
+            raise RuntimeError("handler failed")
+
+    t0 = time.perf_counter()
+    with pytest.raises(RuntimeError, match="handler failed"):
+        rt.run(rt.MemorySource(iq, F, total_chunks=40 * T, block=97), rt.FrontendConfig(FS, F, T),
+               on_detections=handler)
+    # capacity below the window's box count: the engine reports it, run() returns the error
+    with pytest.raises(rt.Error, match="capacity"):
+        rt.run(rt.MemorySource(iq, F, total_chunks=40 * T, block=97), rt.FrontendConfig(FS, F, T),
+               runtime_config=rt.RuntimeConfig(box_capacity=1))
+    assert time.perf_counter() - t0 < 120
+
+
 def test_int16_engine(ss, ref):
     iq = _stream(ref, 2 * T)
     v = np.clip(iq.view(np.float32) * np.float32(2.0 ** -6) * np.float32(32768.0), -32768, 32767)
