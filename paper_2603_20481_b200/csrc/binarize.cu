@@ -370,7 +370,8 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     uint8_t* plane = a.mask_bytes + ((static_cast<long long>(p) * W + (grp >> 2)) * rows_all + rbase) * 4 + (grp & 3);
     const int col0 = grp * kTileCols;
     if (abyte == 0) {  // both CTAs of a cluster see the same byte and leave together
-        for (int r = tid; r < rows; r += kBinThreads) plane[4 * r] = 0;
+        if (!a.skip_empty)
+            for (int r = tid; r < rows; r += kBinThreads) plane[4 * r] = 0;
         return;
     }
     // ---- load the block: one TMA box per kBox rows (32 B x kBox), each on its

@@ -333,13 +333,18 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
     B.cols = cols;
     B.active_bits = abits;
     const bool tile = ssb::binarize_tile_ok(rows, cols);
-    if (tile) B.mask_bytes = reinterpret_cast<uint8_t*>(m0);  // the bit mask, written bytewise
-    else B.mask_bits = m0;
+    if (tile) {
+        B.mask_bytes = reinterpret_cast<uint8_t*>(m0);  // the bit mask, written bytewise
+        B.skip_empty = true;  // empty column groups stay unwritten; K5 reads them as background
+    } else {
+        B.mask_bits = m0;
+    }
     tmark(ctx, 3, 0);
     SS_CK(ctx, ssb::binarize_launch(B, ctx->stream));
     tmark(ctx, 3, 1);
     tmark(ctx, 4, 0);
-    SS_CK(ctx, ssb::consolidate_bits_launch(m0, n_plots, rows, cols, cfg.one_d_opening_along_time != 0, m1, ctx->stream));
+    SS_CK(ctx, ssb::consolidate_bits_launch(m0, n_plots, rows, cols, cfg.one_d_opening_along_time != 0, m1, ctx->stream,
+                                            tile ? abits : nullptr));
     tmark(ctx, 4, 1);
     ctx->launches += 3;
     const long long cap = out_dev.box_capacity > 0 ? out_dev.box_capacity : 0;

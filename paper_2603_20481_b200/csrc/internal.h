@@ -79,6 +79,7 @@ struct BinarizeLaunch {
     const uint32_t* active_bits = nullptr;  // n_plots x W
     uint32_t* mask_bits = nullptr;      // n_plots x W x rows word-major bits (bit mode) or null
     uint8_t* mask_bytes = nullptr;     // tile path: the word-major bit mask as bytes (byte k of word w = columns 32w+8k..+7) or null
+    bool skip_empty = false;           // tile path: groups with no active column write nothing (K5 masks them)
     uint8_t* mask_u8 = nullptr;         // rows x cols (u8 mode, columns [c0,c1)) or null
     int c0 = 0, c1 = 0;                 // u8 mode column range
     float* col_thr = nullptr;           // optional n_plots x cols thresholds (+inf inactive)
@@ -95,8 +96,11 @@ cudaError_t unpack_launch(const uint32_t* bits, int n_plots, int rows, int cols,
                           cudaStream_t st);
 // close 3x3 -> open 3x3 -> open 1x3 (3x1 if along_time), bit-packed, fused in
 // registers.  in / out: word-major bit masks [p][ceil(cols/32)][rows].
+// active_bits (optional, [p][W]): bytes of `in` whose 8-column group has no
+// active column are read as background (the tile K4 leaves them unwritten).
 cudaError_t consolidate_bits_launch(const uint32_t* in, int n_plots, int rows,
-                                    int cols, bool along_time, uint32_t* out, cudaStream_t st);
+                                    int cols, bool along_time, uint32_t* out, cudaStream_t st,
+                                    const uint32_t* active_bits = nullptr);
 // Generic single-plot u8 morphology of columns [c0, c1) (stage API): op 0 erode,
 // 1 dilate, 2 open, 3 close; tmp: rows x cols scratch.
 cudaError_t morph_u8_launch(const uint8_t* src, int rows, int cols, int op, int se_rows, int se_cols,

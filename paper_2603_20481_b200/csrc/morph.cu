@@ -131,7 +131,8 @@ struct RegBand {
 // in/out: word-major bits [p][W][rows].  One warp per (row band, word band).
 __global__ void __launch_bounds__(128) consolidate_kernel(const uint32_t* __restrict__ in, int rows, int cols,
                                                           int wbands, long long bands, bool along_time,
-                                                          uint32_t* __restrict__ out) {
+                                                          uint32_t* __restrict__ out,
+                                                          const uint32_t* __restrict__ active_bits) {
     const int W = (cols + 31) / 32;
     const int lane = threadIdx.x & 31;
     const long long gwarp = blockIdx.x * 4LL + (threadIdx.x >> 5);
@@ -145,9 +146,15 @@ __global__ void __launch_bounds__(128) consolidate_kernel(const uint32_t* __rest
     t.lo = max(0, -row0);
     t.hi = min(kRegNR, rows - row0);
     t.wmask = !wvalid ? 0u : ((gw == W - 1 && (cols & 31)) ? ((1u << (cols & 31)) - 1u) : 0xffffffffu);
+    uint32_t keep = 0xffffffffu;  // bytes K4 wrote (groups with an active column)
+    if (active_bits && wvalid) {
+        const uint32_t ab = __ldg(active_bits + static_cast<long long>(p) * W + gw);
+        keep = ((ab & 0xffu) ? 0xffu : 0u) | ((ab & 0xff00u) ? 0xff00u : 0u) | ((ab & 0xff0000u) ? 0xff0000u : 0u) |
+               ((ab & 0xff000000u) ? 0xff000000u : 0u);
+    }
     const uint32_t* src = in + (static_cast<long long>(p) * W + (wvalid ? gw : 0)) * rows + row0;
 #pragma unroll
-    for (int i = 0; i < kRegNR; ++i) t.x[i] = (wvalid && i >= t.lo && i < t.hi) ? __ldg(src + i) : 0u;
+    for (int i = 0; i < kRegNR; ++i) t.x[i] = (wvalid && i >= t.lo && i < t.hi) ? (__ldg(src + i) & keep) : 0u;
     // interior bands (most of a plot) skip the out-of-image clipping entirely
     const bool interior = t.lo == 0 && t.hi == kRegNR && t.wmask == 0xffffffffu;
     if (__all_sync(0xffffffffu, interior)) t.chain<false>(along_time);
@@ -161,13 +168,13 @@ __global__ void __launch_bounds__(128) consolidate_kernel(const uint32_t* __rest
 }
 
 cudaError_t consolidate_bits_launch(const uint32_t* in, int n_plots, int rows, int cols, bool along_time,
-                                    uint32_t* out, cudaStream_t st) {
+                                    uint32_t* out, cudaStream_t st, const uint32_t* active_bits) {
     if (n_plots <= 0 || rows <= 0 || cols <= 0) return cudaSuccess;
     const int W = (cols + 31) / 32;
     const int wbands = (W + kRegOwn - 1) / kRegOwn;
     const long long bands = static_cast<long long>((rows + kRegRows - 1) / kRegRows) * wbands;
     dim3 grid(static_cast<unsigned>((bands + 3) / 4), n_plots);
-    consolidate_kernel<<<grid, 128, 0, st>>>(in, rows, cols, wbands, bands, along_time, out);
+    consolidate_kernel<<<grid, 128, 0, st>>>(in, rows, cols, wbands, bands, along_time, out, active_bits);
     return cudaGetLastError();
 }
 
