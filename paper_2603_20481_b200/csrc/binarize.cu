@@ -505,9 +505,12 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     __syncthreads();
 
     if constexpr (NSPLIT > 1) cg::this_cluster().sync();  // every partial histogram complete
-    // ---- Otsu: warp w handles column w
-    if (warp < kTileCols && c_use[warp]) {
-        const int cc = warp;
+    // ---- Otsu: warp w handles column w; in a cluster the CTAs split the
+    // columns (rank r: columns r*8/NSPLIT ..) and publish each threshold to
+    // every CTA's c_thr through DSMEM before the final cluster barrier
+    constexpr int OW = kTileCols / NSPLIT;  // Otsu warps per CTA
+    if (warp < OW && c_use[warp + OW * rank]) {
+        const int cc = warp + OW * rank;
         uint32_t hq[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) hq[q] = hist[cc * kHistStride + lane * 8 + q];
@@ -524,11 +527,17 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
         if (lane == 0) {
             const double lod = static_cast<double>(c_lo[cc]);
             const double e = __ddiv_rn(__dmul_rn(static_cast<double>(best_i) + 1.0, c_span[cc]), 256.0);
-            c_thr[cc] = __double2float_rn(__dadd_rn(lod, e));
+            const float t = __double2float_rn(__dadd_rn(lod, e));
+            c_thr[cc] = t;
+            if constexpr (NSPLIT > 1) {
+                cg::cluster_group cl = cg::this_cluster();
+                for (int o = 0; o < NSPLIT; ++o)
+                    if (o != rank) *cl.map_shared_rank(&c_thr[cc], o) = t;
+            }
         }
     }
     __syncthreads();
-    // no CTA may leave while a partner still reads its histogram
+    // every threshold published; no CTA may leave while a partner still reads its histogram
     if constexpr (NSPLIT > 1) cg::this_cluster().sync();
     if (a.col_thr && tid < kTileCols && col0 + tid < cols && rank == 0)
         a.col_thr[static_cast<long long>(p) * cols + col0 + tid] = c_thr[tid];
