@@ -454,8 +454,8 @@ def run_stream(args):
     fc = rt.FrontendConfig(FS, P_F, P_T)
     windows = max(args.steps, 1) * args.stream_windows
     # warm-up pass (allocations, pinned copies, clocks)
-    rt.run(rt.MemorySource(iq, P_F, total_chunks=args.warmup * P_T, block=256), fc)
-    src = rt.MemorySource(iq, P_F, total_chunks=windows * P_T, block=256)
+    rt.run(rt.MemorySource(iq, P_F, total_chunks=args.warmup * P_T, block=args.stream_block), fc)
+    src = rt.MemorySource(iq, P_F, total_chunks=windows * P_T, block=args.stream_block)
     with Clocks(local) as clk:
         rep = rt.run(src, fc)
         wall = rep.wall_time_s  # first push -> last record (the engine's setup is not in it)
@@ -586,6 +586,8 @@ def main():
                          "stream: the real-time engine at config P (latency + plots/s)")
     ap.add_argument("--stream-windows", type=int, default=200, help="stream mode: windows per timed step")
     ap.add_argument("--stream-windows5", type=int, default=20, help="stream5 mode: windows per timed step")
+    ap.add_argument("--stream-block", type=int, default=1000,
+                    help="stream mode: chunks per MemorySource block (one engine push each) in the unpaced run")
     ap.add_argument("--stream-paced-s", type=float, default=3.0, help="stream mode: seconds of paced real-time input")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
