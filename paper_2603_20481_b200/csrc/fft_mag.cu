@@ -13,15 +13,18 @@
 // The oracle's FFTW shim (oracle/fftw_shim.c) implements the same spec on the
 // CPU, so TF plots are bit-identical.
 //
-// Layout / schedule (B200): 256 threads (512 for N = 8192) per CTA, 16 complex
-// doubles per thread in registers; G = 256/(N/16) rows per CTA iteration.
-// The next iteration's raw IQ rows (contiguous, G*N samples) are fetched by
-// one TMA 1-D bulk copy into a shared stage buffer behind an mbarrier while
-// the current rows are transformed; the two inter-pass exchanges go through a
-// padded shared buffer (idx + idx/16: conflict-free 16-byte accesses).  In
-// PSD mode one CTA owns one whole plot and walks its rows in order, so the
-// per-column sum of x^2 runs in the reference's exact row order in registers
-// (acc = fma(x, x, acc): x^2 is exact, fusion is bit-neutral).
+// Layout / schedule (B200): row groups of 256 threads (512 for N = 8192), two
+// per CTA for N <= 4096, 16 complex doubles per thread in registers;
+// G = 256/(N/16) rows per group iteration.  The next iteration's raw IQ rows
+// (contiguous, G*N samples) are fetched by one TMA 1-D bulk copy into the
+// group's shared stage behind an mbarrier while the current rows transform;
+// the inter-pass exchanges go through a padded shared buffer (idx + idx/16:
+// conflict-free), whole complex values for N >= 4096 with the next pass's
+// twiddle tree computed in the barrier wait.  In PSD mode a group owns one
+// whole plot and walks its rows in order, so the per-column sum of x^2 runs in
+// the reference's exact row order (acc = fma(x, x, acc): x^2 is exact, fusion
+// is bit-neutral) -- in registers for N <= 2048, in tensor memory (TMEM,
+// tcgen05.ld/st) for N >= 4096.
 #include "common.cuh"
 #include "internal.h"
 
