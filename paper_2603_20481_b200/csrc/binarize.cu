@@ -589,15 +589,13 @@ cudaError_t binarize_tile_launch(const BinarizeLaunch& L, cudaStream_t st) {
     const int split = L.rows > kTileSplitRows ? 2 : 1;
     const int rows_cta = (L.rows + split - 1) / split;
     const size_t smem = sizeof(float) * kTileCols * static_cast<size_t>((rows_cta + kBox - 1) / kBox * kBox);
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[split - 1]) {
-        cudaError_t e = split == 1 ? cudaFuncSetAttribute(binarize_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                          kTileCols * kTileMaxRows * static_cast<int>(sizeof(float)))
-                                   : cudaFuncSetAttribute(binarize_tile_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                          kTileCols * kTileMaxRows * static_cast<int>(sizeof(float)));
-        if (e != cudaSuccess) return e;
-        attr_set[split - 1] = true;
-    }
+    static std::atomic<unsigned long long> attr_set[2];
+    const cudaError_t ae = set_attr_once(attr_set[split - 1], [&] {
+        const int lim = kTileCols * kTileMaxRows * static_cast<int>(sizeof(float));
+        return split == 1 ? cudaFuncSetAttribute(binarize_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim)
+                          : cudaFuncSetAttribute(binarize_tile_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    });
+    if (ae != cudaSuccess) return ae;
     CUtensorMap map;
     const cudaError_t me = make_tf_map(L, &map);
     if (me != cudaSuccess) return me;

@@ -7,6 +7,7 @@
 // (DESIGN.md §5 lists the contracted sites of the reference build).
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -129,6 +130,21 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
         "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
         "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
         : "memory");
+}
+
+// Kernel attributes (e.g. the dynamic shared-memory limit) belong to the
+// function's instance on one device: set once per device and function.  `done`
+// holds one bit per device ordinal; races only repeat the (idempotent) call.
+template <class F>
+inline cudaError_t set_attr_once(std::atomic<unsigned long long>& done, F&& set) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = set();
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+    return e;
 }
 
 // ------------------------------------------------------------ misc helpers

@@ -679,15 +679,11 @@ static void build_tw(std::vector<double2>& out) {
 
 template <int LOGN, int FMT, bool PSD, bool WIN>
 static cudaError_t ensure_smem_attr() {
-    static bool attr_done = false;  // per instantiation
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(fft_mag_kernel<LOGN, FMT, PSD, WIN>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(K1Shape<LOGN>::smem(FMT == 0 ? 8 : 4)));
-        if (e != cudaSuccess) return e;
-        attr_done = true;
-    }
-    return cudaSuccess;
+    static std::atomic<unsigned long long> attr_done;  // per instantiation, one bit per device
+    return set_attr_once(attr_done, [] {
+        return cudaFuncSetAttribute(fft_mag_kernel<LOGN, FMT, PSD, WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(K1Shape<LOGN>::smem(FMT == 0 ? 8 : 4)));
+    });
 }
 
 // plots the fused-PSD grid processes concurrently per SM (one plot per row group)
