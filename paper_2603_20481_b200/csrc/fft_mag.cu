@@ -71,6 +71,8 @@ __device__ __forceinline__ void dft8(cd* v) {
 }
 
 // 4x4 decomposition; y[n1*4+k2] after the first DFT4 layer.
+__device__ __forceinline__ void dft16_tail(cd* y, cd* v);
+
 __device__ __forceinline__ void dft16(cd* v) {
     cd y[16];
 #pragma unroll
@@ -80,6 +82,28 @@ __device__ __forceinline__ void dft16(cd* v) {
 #pragma unroll
         for (int k2 = 0; k2 < 4; ++k2) y[n1 * 4 + k2] = t[k2];
     }
+    dft16_tail(y, v);
+}
+
+// The first DFT4 layer of a DFT16 on integer samples (int16 IQ): every sum is
+// an integer below 2^17, exact in int32 as in double, so this layer leaves the
+// FP64 pipe; y[n1*4+k2] as dft16 forms it.
+__device__ __forceinline__ void dft16_layer1_int(const int* re, const int* im, cd* y) {
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) {
+        const int t0r = re[n1] + re[n1 + 8], t0i = im[n1] + im[n1 + 8];
+        const int t1r = re[n1] - re[n1 + 8], t1i = im[n1] - im[n1 + 8];
+        const int t2r = re[n1 + 4] + re[n1 + 12], t2i = im[n1 + 4] + im[n1 + 12];
+        const int t3r = re[n1 + 4] - re[n1 + 12], t3i = im[n1 + 4] - im[n1 + 12];
+        y[n1 * 4 + 0] = {static_cast<double>(t0r + t2r), static_cast<double>(t0i + t2i)};
+        y[n1 * 4 + 2] = {static_cast<double>(t0r - t2r), static_cast<double>(t0i - t2i)};
+        y[n1 * 4 + 1] = {static_cast<double>(t1r + t3i), static_cast<double>(t1i - t3r)};
+        y[n1 * 4 + 3] = {static_cast<double>(t1r - t3i), static_cast<double>(t1i + t3r)};
+    }
+}
+
+// internal W16 twiddles + second DFT4 layer: y -> v (natural order)
+__device__ __forceinline__ void dft16_tail(cd* y, cd* v) {
     const cd w1 = {kC1, -kS1};
     const cd w3 = {kS1, -kC1};
     const cd w9 = {-kC1, kS1};
@@ -291,11 +315,20 @@ __device__ __forceinline__ void exchange(cd* v, int j, double* buf, int bar_id, 
     }
 }
 
-template <int LOGN, int PASS, bool TWS, bool CX>
+// Y0: pass 0's inputs are already through the first DFT4 layer (int16 path)
+template <int LOGN, int PASS, bool TWS, bool CX, bool Y0 = false>
 __device__ __forceinline__ void passes_from(cd* v, int j, const double2* tw, double* buf, int bar_id,
                                             const StageIssue& nxt, const cd* w) {
     using PL = FftPlan<LOGN>;
-    run_pass<LOGN, PASS>(v, w);
+    if constexpr (Y0) {
+        static_assert(PASS == 0 && PL::radix(0) == 16 && PL::P == 16, "Y0: one radix-16 butterfly in pass 0");
+        cd y[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) y[i] = v[i];
+        dft16_tail(y, v);
+    } else {
+        run_pass<LOGN, PASS>(v, w);
+    }
     if constexpr (PASS + 1 < PL::NP) {
         cd wn[16];
         exchange<LOGN, PASS, CX, TWS>(v, j, buf, bar_id, nxt, tw, wn);
@@ -504,7 +537,19 @@ fft_mag_kernel(FftArgs a) {
 
         // pass-0 inputs from the stage
         cd v[16];
-        {
+        // int16 IQ, no window: pass 0's first DFT4 layer in integer arithmetic
+        constexpr bool INT_L1 = FMT == 1 && !WIN && PL::radix(0) == 16 && PL::P == 16;
+        if constexpr (INT_L1) {
+            int re[16], im[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const int sidx = g * N + j + r * (N / 16);
+                const short2 x = valid ? reinterpret_cast<const short2*>(stage)[sidx] : make_short2(0, 0);
+                re[r] = x.x;
+                im[r] = x.y;
+            }
+            dft16_layer1_int(re, im, v);  // v holds y
+        } else {
             constexpr int R0 = PL::radix(0);
             constexpr int U0 = PL::P / R0;
 #pragma unroll
@@ -537,7 +582,7 @@ fft_mag_kernel(FftArgs a) {
             nxt();
         }
         cd w0[16];  // pass 0 has no twiddles (Ns = 1)
-        passes_from<LOGN, 0, KS::TW_SMEM, KS::CX>(v, j, tw, mybuf, bar_id, nxt, w0);
+        passes_from<LOGN, 0, KS::TW_SMEM, KS::CX, INT_L1>(v, j, tw, mybuf, bar_id, nxt, w0);
 
         // epilogue: outputs of the last pass, index q = b + r*NS_last
         float m[PL::P];
