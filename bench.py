@@ -412,7 +412,10 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": "k1_fft_mag_psd", "achieved": achieved, "peak": hbm_peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                          "alg_bytes_per_capture": wl.alg_bytes,
-                         "fp64_tflops": B * wl.alg_flop64 / (k1_ms / 1e3) / 1e12, "fp64_peak_tflops": FP64_PEAK_TFLOPS},
+                         "fp64_tflops": B * wl.alg_flop64 / (k1_ms / 1e3) / 1e12, "fp64_peak_tflops": FP64_PEAK_TFLOPS,
+                         "fp64_frac": B * wl.alg_flop64 / (k1_ms / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
+                         "note": "K1 is bounded by FP64 pipe + issue slots at 16 warps/SM as much as by HBM "
+                                 "(DESIGN.md §4): both fractions are given, against measured peaks"},
             "e2e": {"value": e2e_val, "unit": "frames/s", "h2d_bytes_per_step": wl.samples(Be) * wl.sb if Be else 0,
                     "d2h_bytes_per_step": d2h, "captures_per_step": Be},
             "gpu_launches": launches,
