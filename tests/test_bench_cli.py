@@ -1,10 +1,13 @@
-"""bench.py contract checks that run without a GPU: the reference arm
-(`--impl reference`, the reference's own CPU path through oracle/_ref) prints
-one JSON line with the keys the driver reads."""
+"""bench.py contract checks: the reference arm (`--impl reference`, the
+reference's own CPU path through oracle/_ref, no GPU needed) and, on a GPU,
+the default arm on a small batch each print one JSON line with the keys the
+driver reads."""
 import json
 import subprocess
 import sys
 from pathlib import Path
+
+import pytest
 
 ROOT = Path(__file__).resolve().parent.parent
 
@@ -25,3 +28,26 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert "workload" in d["config"]
+
+
+
+@pytest.mark.gpu
+def test_bench_json_line_gpu():
+    """The default arm on a small batch: the keys the driver and the judge read
+    (roofline with traffic, e2e with copy bytes, gpu_launches, clocks)."""
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--steps", "1", "--warmup", "3", "--batch", "8",
+                        "--distinct", "2", "--e2e-batch", "2", "--no-cpu"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["value"] > 0 and d["gpu_launches"] > 0 and d["warmup"] >= 3
+    rf = d["roofline"]
+    assert rf["bound"] == "hbm" and rf["unit"] == "GB/s" and 0 < rf["frac"] < 1 and rf["peak"] > 0
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
