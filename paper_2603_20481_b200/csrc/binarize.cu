@@ -342,13 +342,15 @@ __device__ __forceinline__ void tma_load_box(void* dst, const CUtensorMap* map, 
 
 // NSPLIT = 2: a 2-CTA cluster shares one column group, each CTA holding half
 // of the rows (tall plots, e.g. the 4881-row Hann STFT, keep 2 CTAs per SM);
-// column extremes and histograms are combined through distributed shared
-// memory, and both CTAs run the same Otsu on the summed histograms.
+// column extremes are combined through distributed shared memory, each CTA
+// pushes its partial histograms into the partner's shared memory before the
+// second (last) cluster barrier, and both run the same Otsu locally.
 template <int NSPLIT>
 __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaunch a, const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(128) float bt_vals[];     // (rows / NSPLIT, rounded up to kBox) x 8
     __shared__ __align__(8) uint64_t box_bar[kTileMaxRows / kBox];
     __shared__ uint32_t hist[kTileCols * kHistStride];
+    __shared__ uint32_t hist_peer[NSPLIT > 1 ? kTileCols * kHistStride : 1];  // the partner's partials
     __shared__ float s_lo[kBinWarps][kTileCols], s_hi[kBinWarps][kTileCols];
     __shared__ float part_lo[kTileCols], part_hi[kTileCols];
     __shared__ float c_lo[kTileCols], c_scale[kTileCols], c_thr[kTileCols];
@@ -504,41 +506,33 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     }
     __syncthreads();
 
-    if constexpr (NSPLIT > 1) cg::this_cluster().sync();  // every partial histogram complete
-    // ---- Otsu: warp w handles column w; in a cluster the CTAs split the
-    // columns (rank r: columns r*8/NSPLIT ..) and publish each threshold to
-    // every CTA's c_thr through DSMEM before the final cluster barrier
-    constexpr int OW = kTileCols / NSPLIT;  // Otsu warps per CTA
-    if (warp < OW && c_use[warp + OW * rank]) {
-        const int cc = warp + OW * rank;
+    // cluster: each CTA pushes its partial histograms into its partner's
+    // hist_peer (DSMEM stores) before the one barrier; afterwards both hold
+    // the full histograms locally, run all 8 Otsu splits themselves and touch
+    // no remote memory again, so no second barrier is needed
+    if constexpr (NSPLIT > 1) {
+        cg::cluster_group cl = cg::this_cluster();
+        uint32_t* peer = cl.map_shared_rank(hist_peer, rank ^ 1);
+        for (int i = tid; i < kTileCols * kHistStride; i += kBinThreads) peer[i] = hist[i];
+        cl.sync();
+    }
+    if (warp < kTileCols && c_use[warp]) {
+        const int cc = warp;
         uint32_t hq[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) hq[q] = hist[cc * kHistStride + lane * 8 + q];
         if constexpr (NSPLIT > 1) {
-            cg::cluster_group cl = cg::this_cluster();
-            for (int o = 0; o < NSPLIT; ++o) {
-                if (o == rank) continue;
-                const uint32_t* rh = cl.map_shared_rank(hist, o);
 #pragma unroll
-                for (int q = 0; q < 8; ++q) hq[q] += rh[cc * kHistStride + lane * 8 + q];
-            }
+            for (int q = 0; q < 8; ++q) hq[q] += hist_peer[cc * kHistStride + lane * 8 + q];
         }
         const int best_i = otsu_split_warp(hq, lane);
         if (lane == 0) {
             const double lod = static_cast<double>(c_lo[cc]);
             const double e = __ddiv_rn(__dmul_rn(static_cast<double>(best_i) + 1.0, c_span[cc]), 256.0);
-            const float t = __double2float_rn(__dadd_rn(lod, e));
-            c_thr[cc] = t;
-            if constexpr (NSPLIT > 1) {
-                cg::cluster_group cl = cg::this_cluster();
-                for (int o = 0; o < NSPLIT; ++o)
-                    if (o != rank) *cl.map_shared_rank(&c_thr[cc], o) = t;
-            }
+            c_thr[cc] = __double2float_rn(__dadd_rn(lod, e));
         }
     }
     __syncthreads();
-    // every threshold published; no CTA may leave while a partner still reads its histogram
-    if constexpr (NSPLIT > 1) cg::this_cluster().sync();
     if (a.col_thr && tid < kTileCols && col0 + tid < cols && rank == 0)
         a.col_thr[static_cast<long long>(p) * cols + col0 + tid] = c_thr[tid];
 
