@@ -342,17 +342,18 @@ __device__ __forceinline__ void tma_load_box(void* dst, const CUtensorMap* map, 
 
 // NSPLIT = 2: a 2-CTA cluster shares one column group, each CTA holding half
 // of the rows (tall plots, e.g. the 4881-row Hann STFT, keep 2 CTAs per SM);
-// column extremes are combined through distributed shared memory, each CTA
+// column extremes are pushed into the partner (DSMEM stores), each CTA
 // pushes its partial histograms into the partner's shared memory before the
 // second (last) cluster barrier, and both run the same Otsu locally.
 template <int NSPLIT>
 __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaunch a, const __grid_constant__ CUtensorMap tmap) {
+    static_assert(NSPLIT == 1 || NSPLIT == 2, "pairs: the partner is rank ^ 1");
     extern __shared__ __align__(128) float bt_vals[];     // (rows / NSPLIT, rounded up to kBox) x 8
     __shared__ __align__(8) uint64_t box_bar[kTileMaxRows / kBox];
     __shared__ uint32_t hist[kTileCols * kHistStride];
     __shared__ uint32_t hist_peer[NSPLIT > 1 ? kTileCols * kHistStride : 1];  // the partner's partials
     __shared__ float s_lo[kBinWarps][kTileCols], s_hi[kBinWarps][kTileCols];
-    __shared__ float part_lo[kTileCols], part_hi[kTileCols];
+    __shared__ float part_lo[kTileCols], part_hi[kTileCols], peer_lo[kTileCols], peer_hi[kTileCols];
     __shared__ float c_lo[kTileCols], c_scale[kTileCols], c_thr[kTileCols];
     __shared__ double c_span[kTileCols];
     __shared__ int c_use[kTileCols];
@@ -433,6 +434,11 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
             }
             part_lo[tid] = l;
             part_hi[tid] = h;
+            // push into the partner too (peer slot): after the barrier both
+            // read only local shared memory
+            cg::cluster_group cl = cg::this_cluster();
+            *cl.map_shared_rank(&peer_lo[tid], rank ^ 1) = l;
+            *cl.map_shared_rank(&peer_hi[tid], rank ^ 1) = h;
         }
         cg::this_cluster().sync();
     }
@@ -440,14 +446,8 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
         float l, h;
         if constexpr (NSPLIT > 1) {
             // min / max are order-free: every CTA of the cluster derives the same extremes
-            cg::cluster_group cl = cg::this_cluster();
-            l = part_lo[tid];
-            h = part_hi[tid];
-            for (int q = 0; q < NSPLIT; ++q) {
-                if (q == rank) continue;
-                l = fminf(l, *cl.map_shared_rank(&part_lo[tid], q));
-                h = fmaxf(h, *cl.map_shared_rank(&part_hi[tid], q));
-            }
+            l = fminf(part_lo[tid], peer_lo[tid]);
+            h = fmaxf(part_hi[tid], peer_hi[tid]);
         } else {
             l = s_lo[0][tid];
             h = s_hi[0][tid];
