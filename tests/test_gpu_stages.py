@@ -134,17 +134,19 @@ def test_otsu_ties_and_flat_objectives(ss, ref):
     # the same columns through the batched tile kernel (the detect path): lifted
     # by 2^10 (exact, keeps every tie) over unit-Rayleigh noise columns so the
     # PSD prune keeps them active
-    rows = 2441
-    cols = [np.resize(rng.permutation(c), rows) for c in cases[:256]]
-    noise = [np.abs(rng.normal(size=rows) + 1j * rng.normal(size=rows)) for _ in range(256)]
-    tf = np.empty((rows, 512), np.float32)
-    tf[:, 0::2] = np.stack(cols, axis=1) * np.float32(1024.0)
-    tf[:, 1::2] = np.stack(noise, axis=1)
-    cfg = ss.DetectorConfig(psd_margin_db=0.0, min_component_area=1)
-    got = ss.detect(tf, cfg)
-    exp = ref.detect(tf, margin_db=0.0, min_area=1)
-    assert np.array_equal(got.active_columns, exp["active"])
-    assert np.array_equal(got.bin_boxes, exp["bin_boxes"])
+    # 2441 rows: one CTA per column group; 4881 rows: the 2-CTA cluster form
+    # (extremes and partial histograms pushed between the CTAs)
+    for rows in (2441, 4881):
+        cols = [np.resize(rng.permutation(c), rows) for c in cases[:256]]
+        noise = [np.abs(rng.normal(size=rows) + 1j * rng.normal(size=rows)) for _ in range(256)]
+        tf = np.empty((rows, 512), np.float32)
+        tf[:, 0::2] = np.stack(cols, axis=1) * np.float32(1024.0)
+        tf[:, 1::2] = np.stack(noise, axis=1)
+        cfg = ss.DetectorConfig(psd_margin_db=0.0, min_component_area=1)
+        got = ss.detect(tf, cfg)
+        exp = ref.detect(tf, margin_db=0.0, min_area=1)
+        assert np.array_equal(got.active_columns, exp["active"]), rows
+        assert np.array_equal(got.bin_boxes, exp["bin_boxes"]), rows
 
 
 def test_binarize_exact(ss, ref):
