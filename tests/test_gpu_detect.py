@@ -197,7 +197,8 @@ def test_host_input_pipeline_matches_device(ss, hop, window, rows):
     torch.cuda.synchronize()
 
 
-@pytest.mark.parametrize("n_fft,rows", [(8192, 60), (32, 700), (64, 1), (2048, 3), (1024, 6200), (512, 3265), (256, 12289)])
+@pytest.mark.parametrize("n_fft,rows", [(8192, 60), (32, 700), (64, 1), (2048, 3), (1024, 6200), (512, 3264), (512, 3265),
+                                         (256, 12288), (256, 12289)])
 def test_size_edges(ss, ref, n_fft, rows):
     """Extreme geometries through the fused pipeline vs the reference: the largest
     device FFT, the smallest F the default window accepts, single-row plots,
