@@ -244,3 +244,62 @@ def test_large_fft_detect(ss, ref, n_fft, rows):
     exp_tf = ref.make_plots(x, 1e6, n_fft, rows)
     for p, det in enumerate(dets):
         _check(det, ref.detect(exp_tf[p], start_seq=p * rows, fs=1e6), tf[p], exp_tf[p])
+
+
+def _k2_ms(ss):
+    """Stage-timer reading of K2 (the separate PSD kernel): zero when K1 fused it."""
+    import ctypes as C
+    ctx = ss.Context.get(0)
+    st = (C.c_double * 8)()
+    ctx.lib.ss_stage_times(ctx.h, st)
+    return st[1]
+
+
+@pytest.mark.parametrize("n_fft,rows,P,fmt", [(4096, 12, 296, 0), (4096, 12, 296, 1), (8192, 6, 148, 0),
+                                              (1024, 8, 592, 0)])
+def test_fused_full_wave(ss, ref, n_fft, rows, P, fmt):
+    """Batches that fill whole waves of plot slots take K1's fused-PSD form (one
+    plot per row group, row-order column sums -- in TMEM for N >= 4096; the
+    int16 form's first DFT4 layer in integer arithmetic) and the bench's
+    K4 -> K6 chain: every plot vs the reference, bit for bit."""
+    rng = np.random.default_rng(n_fft * 7 + P + fmt)
+    n = P * rows * n_fft
+    x = (rng.normal(size=n) + 1j * rng.normal(size=n)).astype(np.complex64)
+    t = np.arange(n)
+    x += (6 * np.exp(2j * np.pi * 0.23 * t) * ((t // (rows * n_fft)) % 3 == 0)).astype(np.complex64)
+    fs = 1e6
+    ctx = ss.Context.get(0)
+    ctx.lib.ss_enable_stage_timing(ctx.h, 1)  # resets the stage timers
+    try:
+        if fmt == 1:
+            v = np.clip(x.view(np.float32) * np.float32(2048.0), -32768, 32767)
+            q = np.rint(v).astype(np.int16)
+            dets, tf = ss.sense(q, fs, n_fft, rows, fmt=1, return_tf=True, box_capacity=4096)
+            x = (q.astype(np.float32) * np.float32(1 / 32768)).view(np.complex64)
+        else:
+            dets, tf = ss.sense(x, fs, n_fft, rows, return_tf=True, box_capacity=4096)
+        assert _k2_ms(ss) == 0.0, "batch did not take the fused-PSD K1"
+    finally:
+        ctx.lib.ss_enable_stage_timing(ctx.h, 0)
+    exp_tf = ref.make_plots(x, fs, n_fft, rows)
+    assert len(dets) == len(exp_tf) == P
+    for p, det in enumerate(dets):
+        _check(det, ref.detect(exp_tf[p], start_seq=p * rows, fs=fs), tf[p], exp_tf[p])
+
+
+def test_fused_full_wave_hann(ss, ora):
+    """Config 5 as written on a full wave (296 plots): the fused K1 with the
+    window, vs the oracle's STFT restatement."""
+    n_fft, hop, rows, P, fs = 4096, 2048, 6, 296, 100e6
+    rng = np.random.default_rng(2961)
+    n = P * rows * hop + n_fft - hop
+    iq = (rng.normal(size=n) + 1j * rng.normal(size=n)).astype(np.complex64)
+    dets, tf = ss.sense(iq, fs, n_fft, rows, hop=hop, window=1, return_tf=True, first_seq=0, box_capacity=4096)
+    exp_tf = ora.stft_plot(iq, n_fft, hop, 1, P * rows).reshape(P, rows, n_fft)
+    assert len(dets) == P
+    for p in range(0, P, 37):
+        assert np.array_equal(tf[p].view(np.uint32), exp_tf[p].view(np.uint32)), p
+        exp = ora.detect(exp_tf[p], start_seq=p * rows, fs=fs)
+        assert np.array_equal(dets[p].psd.raw.view(np.uint32), exp["raw"].view(np.uint32)), p
+        assert np.array_equal(dets[p].active_columns, exp["active"]), p
+        assert np.array_equal(dets[p].bin_boxes, exp["bin_boxes"]), p
