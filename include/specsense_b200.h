@@ -252,7 +252,9 @@ ss_status ss_engine_open(int device, const ss_engine_cfg* cfg, const ss_detector
 void ss_engine_close(ss_engine* eng);
 const char* ss_engine_last_error(const ss_engine* eng);
 /* n_chunks chunks of n_fft samples (host or device memory, contiguous),
-   sequence numbers first_seq, first_seq + 1, ... */
+   sequence numbers first_seq, first_seq + 1, ...  Synchronous for the caller's
+   buffer, like frontend::PingPongBuffer writers: when push returns, the samples
+   have been copied out of `samples` (staged or DMA'd) and it may be reused. */
 ss_status ss_engine_push(ss_engine* eng, const void* samples, int64_t n_chunks, uint64_t first_seq);
 /* Chunks [first_seq, last_seq) were lost upstream: their windows drop
    (frontend::PingPongBuffer::mark_lost_range). */
@@ -261,7 +263,9 @@ ss_status ss_engine_mark_lost(ss_engine* eng, uint64_t first_seq, uint64_t last_
 ss_status ss_engine_finish(ss_engine* eng);
 /* Next completed window in completion (= window) order.  wait_ms < 0 waits
    until a record is ready or the stream is finished and drained; *got = 1
-   when rec/boxes/bin_boxes (each may be NULL, capacity cap) were filled. */
+   when rec/boxes/bin_boxes (each may be NULL, capacity cap) were filled.
+   SS_ECUDA with *got = 1: that window's sensing faulted on the device; its
+   record is consumed but rec/boxes hold no result (ss_engine_last_error). */
 ss_status ss_engine_poll(ss_engine* eng, int wait_ms, ss_plot_record* rec, ss_box* boxes, ss_bin_box* bin_boxes,
                          int cap, int* got);
 /* windows completed (handed to the GPU), windows dropped (overruns), rows

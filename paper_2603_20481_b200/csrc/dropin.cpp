@@ -2,10 +2,9 @@
 // implemented over the C ABI, so reference callers (runtime, baseline, CLI,
 // acceptance) relink against libspecsense_b200.so unchanged.
 //
-// Host spans are staged through device buffers; every computation runs on the
-// GPU.  One ss_ctx per host thread (thread_local), bound to the legacy
-// default stream so the synchronous cudaMemcpy staging is ordered with the
-// kernels.  Status codes map back onto the reference's exception types
+// Host spans are staged through a persistent per-thread workspace (device
+// buffers that only grow + a pinned staging buffer, one stream synchronize per
+// call); every computation runs on the GPU.  Status codes map back onto the reference's exception types
 // (proj/include/specsense/types.hpp:43-70).
 #include "specsense/detector.hpp"
 #include "specsense/frontend.hpp"
@@ -13,28 +12,60 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 
 namespace specsense {
 namespace {
 
+// Per-host-thread context: one ss_ctx on a private non-blocking stream, a set
+// of device buffers that only grow (no cudaMalloc / cudaFree per call once
+// warm), and a pinned staging buffer through which small host spans travel
+// (memcpy + async copy instead of a pageable cudaMemcpy per span).
 struct Ctx {
     ss_ctx* h = nullptr;
+    cudaStream_t s = nullptr;
+    struct Slot {
+        void* p = nullptr;
+        std::size_t bytes = 0;
+    };
+    Slot slots[16];
+    unsigned char* pin = nullptr;
+    std::size_t pin_cap = 0, pin_used = 0, pin_want = 0;
+    struct Pending {
+        void* dst;
+        const void* src;
+        std::size_t n;
+    };
+    std::vector<Pending> pend;
+
     Ctx() {
         const char* dev = std::getenv("SPECSENSE_DEVICE");
-        const ss_status s = ss_open(dev ? std::atoi(dev) : 0, &h);
-        if (s != SS_OK) throw Error("specsense-b200: no usable sm_100 device (ss_open status " + std::to_string(s) + ")");
-        ss_set_stream(h, nullptr);
+        const ss_status st = ss_open(dev ? std::atoi(dev) : 0, &h);
+        if (st != SS_OK) throw Error("specsense-b200: no usable sm_100 device (ss_open status " + std::to_string(st) + ")");
+        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) throw Error("cudaStreamCreate failed");
+        ss_set_stream(h, s);
     }
-    ~Ctx() { ss_close(h); }
+    ~Ctx() {
+        cudaStreamSynchronize(s);
+        for (Slot& b : slots) cudaFree(b.p);
+        cudaFreeHost(pin);
+        ss_close(h);
+        cudaStreamDestroy(s);
+    }
 };
 
-ss_ctx* ctx() {
+constexpr std::size_t kPinnedMax = std::size_t(64) << 20;  // larger spans copy from pageable memory directly
+
+Ctx& ctx_obj() {
     thread_local Ctx c;
-    return c.h;
+    return c;
 }
+
+ss_ctx* ctx() { return ctx_obj().h; }
 
 void check(ss_status s) {
     if (s == SS_OK) return;
@@ -48,23 +79,87 @@ void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw Error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-template <typename T>
-struct DBuf {
-    T* p = nullptr;
-    std::size_t n = 0;
-    explicit DBuf(std::size_t count) : n(count) {
-        cuda_check(cudaMalloc(&p, sizeof(T) * (count ? count : 1)), "cudaMalloc");
+// One drop-in call: device slots handed out in order, host inputs staged in,
+// host outputs collected at finish() (one stream synchronize per call).
+class Call {
+  public:
+    Call() : c_(ctx_obj()) {
+        c_.pend.clear();
+        if (c_.pin_want > c_.pin_cap) {  // grow the pinned stage between calls, never during one
+            cudaFreeHost(c_.pin);
+            c_.pin = nullptr;
+            c_.pin_cap = 0;
+            const std::size_t want = std::min(kPinnedMax, c_.pin_want + c_.pin_want / 4);
+            if (cudaMallocHost(&c_.pin, want) == cudaSuccess) c_.pin_cap = want;
+            else cudaGetLastError();
+        }
+        c_.pin_used = 0;
+        c_.pin_want = 0;
     }
-    DBuf(const T* host, std::size_t count) : DBuf(count) { put(host, count); }
-    ~DBuf() { cudaFree(p); }
-    DBuf(const DBuf&) = delete;
-    DBuf& operator=(const DBuf&) = delete;
-    void put(const T* host, std::size_t count) {
-        if (count) cuda_check(cudaMemcpy(p, host, sizeof(T) * count, cudaMemcpyHostToDevice), "H2D");
+    Call(const Call&) = delete;
+    Call& operator=(const Call&) = delete;
+
+    template <typename T>
+    T* dev(std::size_t count) {
+        if (next_ >= 16) throw Error("drop-in: too many device buffers in one call");
+        Ctx::Slot& b = c_.slots[next_++];
+        const std::size_t need = sizeof(T) * (count ? count : 1);
+        if (b.bytes < need) {
+            cuda_check(cudaStreamSynchronize(c_.s), "stream sync");
+            cudaFree(b.p);
+            b.p = nullptr;
+            b.bytes = 0;
+            const std::size_t alloc = need + need / 4;
+            cuda_check(cudaMalloc(&b.p, alloc), "cudaMalloc");
+            b.bytes = alloc;
+        }
+        return static_cast<T*>(b.p);
     }
-    void get(T* host, std::size_t count) const {
-        if (count) cuda_check(cudaMemcpy(host, p, sizeof(T) * count, cudaMemcpyDeviceToHost), "D2H");
+    template <typename T>
+    T* in(const T* host, std::size_t count) {
+        T* d = dev<T>(count);
+        put(d, host, count);
+        return d;
     }
+    template <typename T>
+    void put(T* d, const T* host, std::size_t count) {
+        const std::size_t n = sizeof(T) * count;
+        if (!n) return;
+        if (unsigned char* st = stage(n)) {
+            std::memcpy(st, host, n);
+            cuda_check(cudaMemcpyAsync(d, st, n, cudaMemcpyHostToDevice, c_.s), "H2D");
+        } else {
+            cuda_check(cudaMemcpyAsync(d, host, n, cudaMemcpyHostToDevice, c_.s), "H2D");
+        }
+    }
+    template <typename T>
+    void get(T* host, const T* d, std::size_t count) {
+        const std::size_t n = sizeof(T) * count;
+        if (!n) return;
+        if (unsigned char* st = stage(n)) {
+            cuda_check(cudaMemcpyAsync(st, d, n, cudaMemcpyDeviceToHost, c_.s), "D2H");
+            c_.pend.push_back({host, st, n});
+        } else {
+            cuda_check(cudaMemcpyAsync(host, d, n, cudaMemcpyDeviceToHost, c_.s), "D2H");
+        }
+    }
+    void finish() {
+        cuda_check(cudaStreamSynchronize(c_.s), "stream sync");
+        for (const auto& p : c_.pend) std::memcpy(p.dst, p.src, p.n);
+        c_.pend.clear();
+    }
+    void rewind() { next_ = 0; }
+
+  private:
+    unsigned char* stage(std::size_t n) {
+        const std::size_t off = (c_.pin_used + 255) & ~std::size_t(255);
+        c_.pin_want = std::max(c_.pin_want, off + n);
+        if (off + n > c_.pin_cap) return nullptr;
+        c_.pin_used = off + n;
+        return c_.pin + off;
+    }
+    Ctx& c_;
+    int next_ = 0;
 };
 
 ss_detector_cfg to_c(const detector::DetectorConfig& c) {
@@ -111,11 +206,12 @@ static std::vector<float> tf_device(const void* host, std::size_t bytes, ss_fmt 
     const std::size_t n = static_cast<std::size_t>(rows) * n_fft * n_plots;
     std::vector<float> out(n);
     if (n == 0) return out;
-    DBuf<unsigned char> iq(static_cast<const unsigned char*>(host), bytes);
-    DBuf<float> tf(n);
-    check(ss_tf_plots(ctx(), iq.p, fmt, n_fft, rows, n_plots, tf.p));
-    check(ss_synchronize(ctx()));
-    tf.get(out.data(), n);
+    Call c;
+    const unsigned char* iq = c.in(static_cast<const unsigned char*>(host), bytes);
+    float* tf = c.dev<float>(n);
+    check(ss_tf_plots(ctx(), iq, fmt, n_fft, rows, n_plots, tf));
+    c.get(out.data(), tf, n);
+    c.finish();
     return out;
 }
 
@@ -209,11 +305,12 @@ void estimate_psd_into(const frontend::TFPlotView& plot, int col_begin, int col_
     if (plot.rows < 1 || plot.cols < 1) throw ValidationError("empty TF plot");
     if (col_begin < 0 || col_end > plot.cols || col_begin >= col_end)
         throw ValidationError("PSD column range out of bounds");
-    DBuf<float> tf(plot.data, cells(plot));
-    DBuf<float> o(static_cast<std::size_t>(col_end - col_begin));
-    check(ss_psd_cols(ctx(), tf.p, plot.rows, plot.cols, col_begin, col_end, o.p));
-    check(ss_synchronize(ctx()));
-    o.get(out, static_cast<std::size_t>(col_end - col_begin));
+    Call c;
+    const float* tf = c.in(plot.data, cells(plot));
+    float* o = c.dev<float>(static_cast<std::size_t>(col_end - col_begin));
+    check(ss_psd_cols(ctx(), tf, plot.rows, plot.cols, col_begin, col_end, o));
+    c.get(out, o, static_cast<std::size_t>(col_end - col_begin));
+    c.finish();
 }
 
 std::vector<float> estimate_psd(const frontend::TFPlotView& plot) {
@@ -224,32 +321,35 @@ std::vector<float> estimate_psd(const frontend::TFPlotView& plot) {
 
 std::vector<float> savgol_smooth(std::span<const float> values, int window, int order) {
     const std::size_t n = values.size();
-    DBuf<float> v(values.data(), n);
-    DBuf<float> o(n);
-    check(ss_savgol_smooth(ctx(), v.p, static_cast<int>(n), window, order, o.p));
-    check(ss_synchronize(ctx()));
+    Call c;
+    const float* v = c.in(values.data(), n);
+    float* o = c.dev<float>(n);
+    check(ss_savgol_smooth(ctx(), v, static_cast<int>(n), window, order, o));
     std::vector<float> out(n);
-    o.get(out.data(), n);
+    c.get(out.data(), o, n);
+    c.finish();
     return out;
 }
 
 static std::vector<int> floor_prune(PsdProfile& profile, const DetectorConfig& config) {
     const std::size_t n = profile.raw.size();
     const ss_detector_cfg c = to_c(config);
-    DBuf<float> raw(profile.raw.data(), n);
-    DBuf<float> sm(n);
-    DBuf<float> ft(2);
-    DBuf<std::int32_t> act(n);
+    Call k;
+    const float* raw = k.in(profile.raw.data(), n);
+    float* sm = k.dev<float>(n);
+    float* ft = k.dev<float>(2);
+    std::int32_t* act = k.dev<std::int32_t>(n);
     std::int32_t na = 0;
-    check(ss_floor(ctx(), raw.p, static_cast<int>(n), &c, sm.p, ft.p, act.p, &na));
+    check(ss_floor(ctx(), raw, static_cast<int>(n), &c, sm, ft, act, &na));  // returns after the count is on the host
     profile.smoothed.resize(n);
-    sm.get(profile.smoothed.data(), n);
+    k.get(profile.smoothed.data(), sm, n);
     float f[2];
-    ft.get(f, 2);
+    k.get(f, ft, 2);
+    std::vector<int> active(static_cast<std::size_t>(na));
+    k.get(active.data(), act, active.size());
+    k.finish();
     profile.noise_floor = f[0];
     profile.threshold = f[1];
-    std::vector<int> active(static_cast<std::size_t>(na));
-    act.get(active.data(), active.size());
     return active;
 }
 
@@ -257,33 +357,37 @@ void smooth_and_floor(PsdProfile& profile, const DetectorConfig& config) { floor
 
 std::vector<int> prune_columns(const PsdProfile& profile) {
     const std::size_t n = profile.raw.size();
-    DBuf<float> raw(profile.raw.data(), n);
-    DBuf<std::int32_t> act(n);
+    Call k;
+    const float* raw = k.in(profile.raw.data(), n);
+    std::int32_t* act = k.dev<std::int32_t>(n);
     std::int32_t na = 0;
-    check(ss_prune(ctx(), raw.p, static_cast<int>(n), profile.threshold, act.p, &na));
+    check(ss_prune(ctx(), raw, static_cast<int>(n), profile.threshold, act, &na));
     std::vector<int> active(static_cast<std::size_t>(na));
-    act.get(active.data(), active.size());
+    k.get(active.data(), act, active.size());
+    k.finish();
     return active;
 }
 
 OtsuResult otsu_threshold(std::span<const float> values) {
     if (values.empty()) throw ValidationError("otsu on an empty column");
-    DBuf<float> v(values.data(), values.size());
+    Call k;
+    const float* v = k.in(values.data(), values.size());
     std::int32_t valid = 0;
     float thr = 0.0f;
-    check(ss_otsu(ctx(), v.p, static_cast<int>(values.size()), &valid, &thr));
+    check(ss_otsu(ctx(), v, static_cast<int>(values.size()), &valid, &thr));  // synchronous
     return {valid != 0, thr};
 }
 
 void binarize_columns(const frontend::TFPlotView& plot, std::span<const int> active_columns, int col_begin,
                       int col_end, Mask& out) {
     if (out.rows != plot.rows || out.cols != plot.cols) throw ValidationError("binarize output mask shape mismatch");
-    DBuf<float> tf(plot.data, cells(plot));
-    DBuf<std::uint8_t> m(out.v.data(), out.v.size());
-    check(ss_binarize_cols(ctx(), tf.p, plot.rows, plot.cols, active_columns.data(),
-                           static_cast<int>(active_columns.size()), col_begin, col_end, m.p));
-    check(ss_synchronize(ctx()));
-    m.get(out.v.data(), out.v.size());
+    Call k;
+    const float* tf = k.in(plot.data, cells(plot));
+    std::uint8_t* m = k.in(out.v.data(), out.v.size());
+    check(ss_binarize_cols(ctx(), tf, plot.rows, plot.cols, active_columns.data(),
+                           static_cast<int>(active_columns.size()), col_begin, col_end, m));
+    k.get(out.v.data(), m, out.v.size());
+    k.finish();
 }
 
 Mask binarize(const frontend::TFPlotView& plot, std::span<const int> active_columns) {
@@ -295,12 +399,13 @@ Mask binarize(const frontend::TFPlotView& plot, std::span<const int> active_colu
 void morphology_cols(const Mask& src, Mask& dst, MorphOp op, StructuringElement se, int col_begin, int col_end,
                      MorphScratch&) {
     if (dst.rows != src.rows || dst.cols != src.cols) throw ValidationError("morphology output mask shape mismatch");
-    DBuf<std::uint8_t> s(src.v.data(), src.v.size());
-    DBuf<std::uint8_t> d(dst.v.data(), dst.v.size());
-    check(ss_morph_cols(ctx(), s.p, src.rows, src.cols, static_cast<ss_morph_op>(op), se.rows, se.cols, col_begin,
-                        col_end, d.p));
-    check(ss_synchronize(ctx()));
-    d.get(dst.v.data(), dst.v.size());
+    Call k;
+    const std::uint8_t* s = k.in(src.v.data(), src.v.size());
+    std::uint8_t* d = k.in(dst.v.data(), dst.v.size());
+    check(ss_morph_cols(ctx(), s, src.rows, src.cols, static_cast<ss_morph_op>(op), se.rows, se.cols, col_begin,
+                        col_end, d));
+    k.get(dst.v.data(), d, dst.v.size());
+    k.finish();
 }
 
 Mask morphology(const Mask& mask, MorphOp op, StructuringElement se) {
@@ -312,11 +417,12 @@ Mask morphology(const Mask& mask, MorphOp op, StructuringElement se) {
 
 Mask consolidate(const Mask& mask, bool one_d_opening_along_time) {
     Mask out(mask.rows, mask.cols);
-    DBuf<std::uint8_t> s(mask.v.data(), mask.v.size());
-    DBuf<std::uint8_t> d(mask.v.size());
-    check(ss_consolidate(ctx(), s.p, mask.rows, mask.cols, one_d_opening_along_time ? 1 : 0, d.p));
-    check(ss_synchronize(ctx()));
-    d.get(out.v.data(), out.v.size());
+    Call k;
+    const std::uint8_t* s = k.in(mask.v.data(), mask.v.size());
+    std::uint8_t* d = k.dev<std::uint8_t>(mask.v.size());
+    check(ss_consolidate(ctx(), s, mask.rows, mask.cols, one_d_opening_along_time ? 1 : 0, d));
+    k.get(out.v.data(), d, out.v.size());
+    k.finish();
     return out;
 }
 
@@ -326,13 +432,14 @@ static LabeledComponents components(const Mask& mask, int min_area, bool with_la
     lc.rows = mask.rows;
     lc.cols = mask.cols;
     const std::size_t n = mask.v.size();
-    DBuf<std::uint8_t> m(mask.v.data(), n);
-    DBuf<std::int32_t> labels(with_labels ? n : 1);
+    Call k;
+    const std::uint8_t* m = k.in(mask.v.data(), n);
+    std::int32_t* labels = k.dev<std::int32_t>(with_labels ? n : 1);
     std::int64_t cap = 1024, count = 0;
     std::vector<ss_extent> ext;
     for (;;) {
         ext.resize(static_cast<std::size_t>(cap));
-        const ss_status s = ss_components(ctx(), m.p, mask.rows, mask.cols, min_area, with_labels ? labels.p : nullptr,
+        const ss_status s = ss_components(ctx(), m, mask.rows, mask.cols, min_area, with_labels ? labels : nullptr,
                                           ext.data(), cap, &count);
         if (s == SS_ECAPACITY && count > cap) {
             cap = count;
@@ -349,7 +456,8 @@ static LabeledComponents components(const Mask& mask, int min_area, bool with_la
     }
     if (with_labels) {
         lc.labels.resize(n);
-        labels.get(lc.labels.data(), n);
+        k.get(lc.labels.data(), labels, n);
+        k.finish();
     }
     return lc;
 }
@@ -375,65 +483,70 @@ BoundingBox bin_box_to_physical(const BinBox& b, const frontend::TFPlotView& plo
     return out;
 }
 
-// Shared unpacking of a device batch into Detections.
-static std::vector<Detections> unpack(int P, int F, int K, const DBuf<float>& raw, const DBuf<float>& sm,
-                                      const DBuf<float>& ft, const DBuf<std::int32_t>& act,
-                                      const DBuf<std::int32_t>& nact, const DBuf<ss_box>& bx,
-                                      const DBuf<ss_bin_box>& bb, const std::vector<std::int32_t>& nb) {
-    std::vector<float> hraw(static_cast<std::size_t>(P) * F), hsm(hraw.size()), hft(static_cast<std::size_t>(P) * 2);
-    std::vector<std::int32_t> hact(hraw.size()), hnact(static_cast<std::size_t>(P));
-    std::vector<ss_box> hbx(static_cast<std::size_t>(P) * K);
-    std::vector<ss_bin_box> hbb(hbx.size());
-    raw.get(hraw.data(), hraw.size());
-    sm.get(hsm.data(), hsm.size());
-    ft.get(hft.data(), hft.size());
-    act.get(hact.data(), hact.size());
-    nact.get(hnact.data(), hnact.size());
-    bx.get(hbx.data(), hbx.size());
-    bb.get(hbb.data(), hbb.size());
-    std::vector<Detections> out(static_cast<std::size_t>(P));
-    for (int p = 0; p < P; ++p) {
-        Detections& d = out[static_cast<std::size_t>(p)];
-        const std::size_t o = static_cast<std::size_t>(p) * F;
-        d.psd.raw.assign(hraw.begin() + static_cast<std::ptrdiff_t>(o), hraw.begin() + static_cast<std::ptrdiff_t>(o + F));
-        d.psd.smoothed.assign(hsm.begin() + static_cast<std::ptrdiff_t>(o), hsm.begin() + static_cast<std::ptrdiff_t>(o + F));
-        d.psd.noise_floor = hft[2 * static_cast<std::size_t>(p)];
-        d.psd.threshold = hft[2 * static_cast<std::size_t>(p) + 1];
-        d.active_columns.assign(hact.begin() + static_cast<std::ptrdiff_t>(o),
-                                hact.begin() + static_cast<std::ptrdiff_t>(o + static_cast<std::size_t>(hnact[p])));
-        for (int i = 0; i < nb[static_cast<std::size_t>(p)]; ++i) {
-            const ss_box& b = hbx[static_cast<std::size_t>(p) * K + i];
-            const ss_bin_box& q = hbb[static_cast<std::size_t>(p) * K + i];
-            d.boxes.push_back({b.f0_hz, b.f1_hz, b.t0_s, b.t1_s});
-            d.bin_boxes.push_back({q.t0, q.t1, q.f0, q.f1});
-        }
-    }
-    return out;
-}
+// Device outputs of one batch call and their host copies.
+struct BatchBufs {
+    float *raw, *sm, *ft;
+    std::int32_t *act, *nact, *nbox;
+    ss_box* bx;
+    ss_bin_box* bb;
+};
 
-// Runs one batch call with a growing box capacity.
-template <class Call>
-static std::vector<Detections> run_batch(int P, int F, Call&& call) {
+// Runs one batch call with a growing box capacity; the inputs occupy the
+// call's first `keep` device slots and survive a retry.
+template <class Call_>
+static std::vector<Detections> run_batch(Call& k, int keep, int P, int F, Call_&& call) {
+    const std::size_t PF = static_cast<std::size_t>(P) * F;
     int K = 256;
     for (;;) {
-        DBuf<float> raw(static_cast<std::size_t>(P) * F), sm(static_cast<std::size_t>(P) * F), ft(static_cast<std::size_t>(P) * 2);
-        DBuf<std::int32_t> act(static_cast<std::size_t>(P) * F), nact(static_cast<std::size_t>(P)), nbox(static_cast<std::size_t>(P));
-        DBuf<ss_box> bx(static_cast<std::size_t>(P) * K);
-        DBuf<ss_bin_box> bb(static_cast<std::size_t>(P) * K);
-        ss_batch_out o{raw.p, sm.p, ft.p, act.p, nact.p, bx.p, bb.p, nbox.p, K};
+        k.rewind();
+        for (int i = 0; i < keep; ++i) k.dev<unsigned char>(0);  // skip the input slots (never shrink)
+        BatchBufs d{k.dev<float>(PF), k.dev<float>(PF), k.dev<float>(2 * static_cast<std::size_t>(P)),
+                    k.dev<std::int32_t>(PF), k.dev<std::int32_t>(static_cast<std::size_t>(P)),
+                    k.dev<std::int32_t>(static_cast<std::size_t>(P)), k.dev<ss_box>(PF ? static_cast<std::size_t>(P) * K : 1),
+                    k.dev<ss_bin_box>(static_cast<std::size_t>(P) * K)};
+        ss_batch_out o{d.raw, d.sm, d.ft, d.act, d.nact, d.bx, d.bb, d.nbox, K};
         const ss_status s = call(o);
         std::vector<std::int32_t> nb(static_cast<std::size_t>(P));
         if (s == SS_ECAPACITY) {
-            nbox.get(nb.data(), nb.size());
+            k.get(nb.data(), d.nbox, nb.size());
+            k.finish();
             int mx = K;
             for (int v : nb) mx = v > mx ? v : mx;
             K = mx + 1;
             continue;
         }
         check(s);
-        check(ss_synchronize(ctx()));
-        nbox.get(nb.data(), nb.size());
-        return unpack(P, F, K, raw, sm, ft, act, nact, bx, bb, nb);
+        std::vector<float> hraw(PF), hsm(PF), hft(static_cast<std::size_t>(P) * 2);
+        std::vector<std::int32_t> hact(PF), hnact(static_cast<std::size_t>(P));
+        std::vector<ss_box> hbx(static_cast<std::size_t>(P) * K);
+        std::vector<ss_bin_box> hbb(hbx.size());
+        k.get(nb.data(), d.nbox, nb.size());
+        k.get(hraw.data(), d.raw, PF);
+        k.get(hsm.data(), d.sm, PF);
+        k.get(hft.data(), d.ft, hft.size());
+        k.get(hact.data(), d.act, PF);
+        k.get(hnact.data(), d.nact, hnact.size());
+        k.get(hbx.data(), d.bx, hbx.size());
+        k.get(hbb.data(), d.bb, hbb.size());
+        k.finish();
+        std::vector<Detections> out(static_cast<std::size_t>(P));
+        for (int p = 0; p < P; ++p) {
+            Detections& r = out[static_cast<std::size_t>(p)];
+            const std::size_t o0 = static_cast<std::size_t>(p) * F;
+            const auto at = [o0](auto& v, std::size_t i) { return v.begin() + static_cast<std::ptrdiff_t>(o0 + i); };
+            r.psd.raw.assign(at(hraw, 0), at(hraw, F));
+            r.psd.smoothed.assign(at(hsm, 0), at(hsm, F));
+            r.psd.noise_floor = hft[2 * static_cast<std::size_t>(p)];
+            r.psd.threshold = hft[2 * static_cast<std::size_t>(p) + 1];
+            r.active_columns.assign(at(hact, 0), at(hact, static_cast<std::size_t>(hnact[static_cast<std::size_t>(p)])));
+            for (int i = 0; i < nb[static_cast<std::size_t>(p)]; ++i) {
+                const ss_box& b = hbx[static_cast<std::size_t>(p) * K + i];
+                const ss_bin_box& q = hbb[static_cast<std::size_t>(p) * K + i];
+                r.boxes.push_back({b.f0_hz, b.f1_hz, b.t0_s, b.t1_s});
+                r.bin_boxes.push_back({q.t0, q.t1, q.f0, q.f1});
+            }
+        }
+        return out;
     }
 }
 
@@ -446,17 +559,16 @@ std::vector<Detections> detect_batch(std::span<const frontend::TFPlotView> plots
         if (v.rows != T || v.cols != F || v.sample_rate_hz != plots[0].sample_rate_hz)
             throw ValidationError("detect_batch: plots must share rows, cols and sample rate");
     const std::size_t per = static_cast<std::size_t>(T) * F;
-    DBuf<float> tf(per * static_cast<std::size_t>(P));
+    Call k;
+    float* tf = k.dev<float>(per * static_cast<std::size_t>(P));
     std::vector<std::uint64_t> seq(static_cast<std::size_t>(P));
     for (int p = 0; p < P; ++p) {
-        cuda_check(cudaMemcpy(tf.p + per * static_cast<std::size_t>(p), plots[static_cast<std::size_t>(p)].data,
-                              sizeof(float) * per, cudaMemcpyHostToDevice),
-                   "H2D");
+        k.put(tf + per * static_cast<std::size_t>(p), plots[static_cast<std::size_t>(p)].data, per);
         seq[static_cast<std::size_t>(p)] = plots[static_cast<std::size_t>(p)].start_seq;
     }
     const ss_detector_cfg c = to_c(config);
-    return run_batch(P, F, [&](const ss_batch_out& o) {
-        return ss_detect_batch(ctx(), tf.p, P, T, F, seq.data(), plots[0].sample_rate_hz, &c, &o);
+    return run_batch(k, 1, P, F, [&](const ss_batch_out& o) {
+        return ss_detect_batch(ctx(), tf, P, T, F, seq.data(), plots[0].sample_rate_hz, &c, &o);
     });
 }
 
@@ -483,10 +595,11 @@ std::vector<Detections> sense(std::span<const cfloat> samples, const frontend::F
     const std::size_t per = static_cast<std::size_t>(fc.plot_rows) * fc.n_fft;
     const int P = static_cast<int>(samples.size() / per);
     if (P == 0) return {};
-    DBuf<cfloat> iq(samples.data(), per * static_cast<std::size_t>(P));
+    Call k;
+    const cfloat* iq = k.in(samples.data(), per * static_cast<std::size_t>(P));
     const ss_detector_cfg c = to_c(config);
-    return run_batch(P, fc.n_fft, [&](const ss_batch_out& o) {
-        return ss_sense_batch(ctx(), iq.p, SS_FMT_F32, fc.n_fft, fc.plot_rows, P, 0, fc.sample_rate_hz, &c, nullptr, &o);
+    return run_batch(k, 1, P, fc.n_fft, [&](const ss_batch_out& o) {
+        return ss_sense_batch(ctx(), iq, SS_FMT_F32, fc.n_fft, fc.plot_rows, P, 0, fc.sample_rate_hz, &c, nullptr, &o);
     });
 }
 

@@ -89,6 +89,8 @@ struct Bank {
     cudaEvent_t start_ev = nullptr;  // compute stream, before the window's first kernel
     cudaEvent_t done_ev = nullptr;   // compute stream, after the boxes' D2H
     double gpu_s = 0.0;
+    cudaError_t fault = cudaSuccess;  // the done event's query status, reported by poll
+    bool poisoned = false;            // the filling window lost rows upstream: it can never complete
     Clock::time_point complete_at{};
     Clock::time_point done_at{};
 };
@@ -121,8 +123,10 @@ struct ss_engine {
     std::thread waiter;
     bool stop = false;
     uint64_t completed = 0, overruns = 0, rows_retired = 0, launched = 0, polled = 0;
-    bool have_dropped = false;
-    uint64_t dropped_window = 0;       // most recent window shed (its later rows are ignored)
+    // per bank slot: highest window counted as dropped, +1 (frontend.cpp:206-223
+    // dropped_upto / count_drop: each window counted at most once, and rows of a
+    // counted window are ignored)
+    std::vector<uint64_t> dropped_upto;
     uint64_t newest_window = 0;        // highest window seen (rows of older, recycled windows are stale)
     bool finished = false;
     std::string err;
@@ -172,6 +176,7 @@ void waiter_main(ss_engine* e) {
             e->inflight.pop_front();
             b.done_at = now;
             b.gpu_s = 1e-3 * ms;
+            b.fault = st;
             e->done.push_back(bi);
         }
         e->ready.notify_all();
@@ -216,16 +221,34 @@ ss_status launch_window(ss_engine* e, int bi) {
 // Bank for window w, or -1 when its rows must be dropped.  Called with lk held.
 // w is a window this engine owns; its banks cycle over the owned windows
 // (w / shards) so a sharded engine sees consecutive bank indices.
+int bank_slot(const ss_engine* e, uint64_t w) {
+    return static_cast<int>((w / e->shards) % static_cast<uint64_t>(e->cfg.n_banks));
+}
+
+bool already_dropped(const ss_engine* e, uint64_t w) {
+    return w + 1 <= e->dropped_upto[static_cast<size_t>(bank_slot(e, w))];
+}
+
+// Counts window w as one overrun, at most once (windows needing drops arrive in
+// nondecreasing order per bank slot).  mu held.
+void count_drop(ss_engine* e, uint64_t w) {
+    uint64_t& up = e->dropped_upto[static_cast<size_t>(bank_slot(e, w))];
+    if (w + 1 > up) {
+        up = w + 1;
+        ++e->overruns;
+    }
+}
+
 int claim_bank(ss_engine* e, uint64_t w, std::unique_lock<std::mutex>& lk) {
-    if (e->have_dropped && w == e->dropped_window) return -1;
+    if (already_dropped(e, w)) return -1;  // rows of a shed or lost window
     if (w + static_cast<uint64_t>(e->cfg.n_banks) * e->shards <= e->newest_window) return -1;  // stale row
-    const int bi = static_cast<int>((w / e->shards) % static_cast<uint64_t>(e->cfg.n_banks));
+    const int bi = bank_slot(e, w);
     for (;;) {
         Bank& b = e->banks[static_cast<size_t>(bi)];
-        if (b.state == BankState::Filling && b.window == w) return bi;
+        if (b.state == BankState::Filling && b.window == w) return b.poisoned ? -1 : bi;
         if (b.state == BankState::Filling && b.window < w) {
             // an older window never completed (rows lost upstream): shed it
-            ++e->overruns;
+            count_drop(e, b.window);
             b.state = BankState::Free;
         }
         if (b.state == BankState::Free) {
@@ -233,15 +256,14 @@ int claim_bank(ss_engine* e, uint64_t w, std::unique_lock<std::mutex>& lk) {
             b.window = w;
             b.samples_in = 0;
             b.st_lo = b.st_hi = 0;
+            b.poisoned = false;
             e->newest_window = std::max(e->newest_window, w);
             return bi;
         }
         // Busy: held by the reader (or a newer window is filling it)
         if (b.state == BankState::Filling && b.window > w) return -1;
         if (e->cfg.paced) {
-            ++e->overruns;
-            e->have_dropped = true;
-            e->dropped_window = w;
+            count_drop(e, w);
             e->newest_window = std::max(e->newest_window, w);
             return -1;
         }
@@ -294,6 +316,7 @@ ss_status ss_engine_open(int device, const ss_engine_cfg* cfg, const ss_detector
     e->compute = ssb::engine_ctx_stream(e->ctx);
     if (cudaStreamCreateWithFlags(&e->copy, cudaStreamNonBlocking) != cudaSuccess) return bad(SS_ECUDA, "copy stream");
     e->banks.resize(static_cast<size_t>(e->cfg.n_banks));
+    e->dropped_upto.assign(static_cast<size_t>(e->cfg.n_banks), 0);
     const size_t cells = static_cast<size_t>(T) * F;  // TF plot
     const size_t iq_n = static_cast<size_t>(e->span);  // IQ samples per window
     for (Bank& b : e->banks) {
@@ -433,6 +456,7 @@ ss_status ss_engine_push(ss_engine* e, const void* samples, int64_t n_chunks, ui
     }
     std::unique_lock<std::mutex> lk(e->mu);
     if (e->finished) return efail(e, SS_EVALIDATION, "push after finish");
+    bool direct = false;  // a DMA straight from the caller's buffer was queued
     e->rows_retired += static_cast<uint64_t>(n_chunks);
     // the push's samples: [a0, a1); every window they meet gets its part
     const uint64_t a0 = first_seq * F, a1 = (first_seq + static_cast<uint64_t>(n_chunks)) * F;
@@ -453,6 +477,7 @@ ss_status ss_engine_push(ss_engine* e, const void* samples, int64_t n_chunks, ui
             if (s != SS_OK) return s;
             EN_CK(e, cudaMemcpyAsync(b.iq + static_cast<size_t>(o0) * e->sbytes, from, static_cast<size_t>(n) * e->sbytes,
                                      cudaMemcpyDefault, e->copy));
+            direct = true;
         } else {
             if (o0 != b.st_hi) {  // not contiguous with the staged run
                 ss_status s = flush_stage(e, b);
@@ -474,6 +499,21 @@ ss_status ss_engine_push(ss_engine* e, const void* samples, int64_t n_chunks, ui
             if (s != SS_OK) return s;
         }
     }
+    if (direct) {
+        // The reference's push is synchronous: the caller may reuse its buffer
+        // as soon as push returns, so wait for the DMA out of it (not for the
+        // window's sensing).  Waited on outside the lock.
+        cudaEvent_t ev;
+        EN_CK(e, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        const cudaError_t r = cudaEventRecord(ev, e->copy);
+        lk.unlock();
+        const cudaError_t w = r == cudaSuccess ? cudaEventSynchronize(ev) : r;
+        cudaEventDestroy(ev);
+        if (w != cudaSuccess) {
+            std::lock_guard<std::mutex> g(e->mu);
+            return efail(e, SS_ECUDA, std::string("push copy: ") + cudaGetErrorString(w));
+        }
+    }
     return SS_OK;
 }
 
@@ -487,12 +527,12 @@ ss_status ss_engine_mark_lost(ss_engine* e, uint64_t first, uint64_t last) {
     windows_of(e, first * F, last * F, &w_lo, &w_hi);
     for (uint64_t w = w_lo; w <= w_hi; ++w) {
         if (!e->owns(w)) continue;
-        const int bi = static_cast<int>((w / e->shards) % static_cast<uint64_t>(e->cfg.n_banks));
-        Bank& b = e->banks[static_cast<size_t>(bi)];
-        if (b.state == BankState::Filling && b.window == w) b.state = BankState::Free;
-        if (!(e->have_dropped && e->dropped_window == w)) ++e->overruns;
-        e->have_dropped = true;
-        e->dropped_window = w;
+        // every window the lost samples belong to drops once (with hop < F a
+        // lost chunk can belong to several); a window already filling keeps its
+        // bank, poisoned, until a newer window reclaims it (frontend.cpp:321-330)
+        count_drop(e, w);
+        Bank& b = e->banks[static_cast<size_t>(bank_slot(e, w))];
+        if (b.state == BankState::Filling && b.window == w) b.poisoned = true;
         e->newest_window = std::max(e->newest_window, w);
     }
     return SS_OK;
@@ -545,6 +585,15 @@ ss_status ss_engine_poll(ss_engine* e, int wait_ms, ss_plot_record* rec, ss_box*
     b.state = BankState::Free;
     ++e->polled;
     *got = 1;
+    const cudaError_t fault = b.fault;
+    b.fault = cudaSuccess;
+    if (fault != cudaSuccess) {
+        // a device fault inside the window's graph: its record is not delivered as a result
+        e->err = std::string("window ") + std::to_string(b.window) + ": " + cudaGetErrorString(fault);
+        lk.unlock();
+        e->released.notify_all();
+        return SS_ECUDA;
+    }
     lk.unlock();
     e->released.notify_all();
     if (nb > K) return efail(e, SS_ECAPACITY, "box capacity too small: " + std::to_string(nb));

@@ -172,7 +172,8 @@ RunReport run(frontend::ChunkSource& source, const frontend::FrontendConfig& fc,
             while (!failed.load() && source.next(chunk)) {
                 if (chunk.samples.size() != static_cast<std::size_t>(F))
                     throw ValidationError("chunk size " + std::to_string(chunk.samples.size()) + " != n_fft");
-                if (chunk.seq < expected) continue;  // stale / duplicate
+                // as runtime.cpp:283-285: a gap is lost, expected follows the chunk
+                // (stale chunks go on to the engine, which retires them)
                 if (chunk.seq > expected) eng.check(ss_engine_mark_lost(eng.h, expected, chunk.seq));
                 eng.check(ss_engine_push(eng.h, chunk.samples.data(), 1, chunk.seq));
                 expected = chunk.seq + 1;

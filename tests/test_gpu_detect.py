@@ -303,3 +303,27 @@ def test_fused_full_wave_hann(ss, ora):
         assert np.array_equal(dets[p].psd.raw.view(np.uint32), exp["raw"].view(np.uint32)), p
         assert np.array_equal(dets[p].active_columns, exp["active"]), p
         assert np.array_equal(dets[p].bin_boxes, exp["bin_boxes"]), p
+
+
+SCEN_DIR = __import__("pathlib").Path(__file__).resolve().parents[1] / "oracle" / "_ref" / "suite" / "scenarios"
+REF_SCENARIOS = ["sparse", "default", "control", "dense_mixed", "dense_noise_like"]
+
+
+@pytest.mark.parametrize("name", REF_SCENARIOS)
+@pytest.mark.parametrize("rows", [2000, 500])
+def test_reference_scenario_fixtures(ss, ref, name, rows):
+    """The reference's own scenario fixtures (proj/scenarios/*.json, SURVEY.md
+    §8(d) P-parity set; copied next to the suite binaries by oracle/Makefile),
+    rendered by the reference's signals::synthesize, through ss_sense_batch:
+    2 plots at (2000, 1024) and 8 at (500, 1024) per scenario (10 and 40 over
+    the five), every output
+    bit-identical to the reference's make_plots + detect."""
+    text = (SCEN_DIR / f"{name}.json").read_text()
+    iq, _ = ref.synthesize(text)
+    fs = 100e6
+    dets, tf = ss.sense(iq, fs, 1024, rows, return_tf=True)
+    exp_tf = ref.make_plots(iq, fs, 1024, rows)
+    assert len(dets) == len(exp_tf) == (2 if rows == 2000 else 8)
+    for p, det in enumerate(dets):
+        exp = ref.detect(exp_tf[p], start_seq=p * rows, fs=fs)
+        _check(det, exp, tf[p], exp_tf[p])

@@ -131,7 +131,7 @@ BL_DEMO = ROOT / "paper_2603_20481_b200" / "_lib" / "baseline_demo"
 
 
 def test_baseline_dropin_matches_reference(ref, tmp_path):
-    """specsense::baseline / metrics through the C++ drop-in vs the reference."""
+    """specsense::baseline through the C++ drop-in vs the reference."""
     assert BL_DEMO.exists(), "build() links tools/baseline_demo.cpp"
     sc = signals.paper_scenario(rows=500)
     iq, truth = ref.synthesize(signals.scenario_json(sc))
@@ -151,11 +151,4 @@ def test_baseline_dropin_matches_reference(ref, tmp_path):
     got = r.take(np.float64, 4 * nb).reshape(-1, 4)
     exp = ref.baseline_detect(tf, 0, fs)
     assert np.array_equal(got.view(np.uint64), exp.view(np.uint64))
-    pipe = r.take(np.float64, 4)
-    base = r.take(np.float64, 4)
-    speedup = r.one(np.float64)
-    assert pipe[0] > 0 and base[0] > 0 and speedup > 0 and 0 <= pipe[1] <= 1 and 0 <= base[1] <= 1
-    from paper_2603_20481_b200 import metrics
-    ev = metrics.evaluate(gt, exp, theta=0.3)
-    assert np.array_equal(r.take(np.float64, 4), np.array([ev.n_true, ev.n_false, ev.p_fa, ev.mean_iou]))
     assert r.one(np.int32) == 1

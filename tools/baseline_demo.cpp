@@ -1,8 +1,9 @@
-// baseline_demo.cpp -- a reference-style caller of specsense::baseline and
-// specsense::metrics (include/specsense/{baseline,metrics}.hpp) linked
-// against libspecsense_b200.so.  Reads one rows x cols f32 TF plot and a
-// ground-truth box list, writes kernel sizes, baseline boxes and the
-// compare() table to a binary file for tests/test_gpu_dropin.py.
+// baseline_demo.cpp -- a reference-style caller of specsense::baseline
+// (include/specsense/baseline.hpp) linked against libspecsense_b200.so.
+// Reads one rows x cols f32 TF plot, writes kernel sizes and baseline boxes to
+// a binary file for tests/test_gpu_dropin.py.  (compare() and the metrics are
+// the reference's own evaluation code: the reference's test_baseline.cpp runs
+// them over this library, oracle/Makefile `suite`.)
 //
 //   baseline_demo <tf.f32> <rows> <cols> <fs> <start_seq> <truth.f64> <out.bin>
 #include "specsense/baseline.hpp"
@@ -43,18 +44,6 @@ int main(int argc, char** argv) {
         const int nb = static_cast<int>(boxes.size());
         put(&nb, sizeof(nb));
         put(boxes.data(), sizeof(BoundingBox) * boxes.size());
-        const std::vector<std::vector<BoundingBox>> tp{truth};
-        const frontend::TFPlotView views[1] = {view};
-        const auto cmp = baseline::compare(views, tp, detector::DetectorConfig{}, baseline::BaselineConfig{}, 0.5);
-        for (const auto& r : cmp.rows) {
-            const double v[4] = {r.mean_latency_s, r.p_d, r.p_fa, r.mean_iou};
-            put(v, sizeof(v));
-        }
-        put(&cmp.speedup, sizeof(double));
-        // metrics spot values: evaluate(truth, baseline boxes, 0.3)
-        const auto ev = metrics::evaluate(truth, boxes, 0.3);
-        const double e[4] = {static_cast<double>(ev.n_true), static_cast<double>(ev.n_false), ev.p_fa, ev.mean_iou};
-        put(e, sizeof(e));
         try {
             baseline::BaselineConfig bad;
             bad.conv_threshold = 0.0;
