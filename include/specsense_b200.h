@@ -246,6 +246,8 @@ typedef struct {
     double complete_s;     /* engine clock: window complete */
     double done_s;         /* engine clock: boxes on the host */
     double gpu_s;          /* device time from the window's first kernel to its boxes' D2H end */
+    double stage_s[8];     /* device time per stage, ss_stage_times ids (0 K1 FFT, 1 K2 PSD, 2 K3 floor
+                              + prune, 3 K4 binarize, 4 K5 consolidate, 5 K6 label + boxes; 6, 7 unused) */
 } ss_plot_record;
 
 ss_status ss_engine_open(int device, const ss_engine_cfg* cfg, const ss_detector_cfg* det, ss_engine** out);

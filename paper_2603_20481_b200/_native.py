@@ -54,7 +54,7 @@ class PlotRecord(C.Structure):
     _fields_ = [("plot_index", C.c_uint64), ("start_seq", C.c_uint64), ("latency_s", C.c_double),
                 ("deadline_s", C.c_double), ("met", C.c_int32), ("n_boxes", C.c_int32), ("n_active", C.c_int32),
                 ("noise_floor", C.c_float), ("threshold", C.c_float), ("complete_s", C.c_double),
-                ("done_s", C.c_double), ("gpu_s", C.c_double)]
+                ("done_s", C.c_double), ("gpu_s", C.c_double), ("stage_s", C.c_double * 8)]
 
 
 # name -> (restype, argtypes); every symbol include/specsense_b200.h declares

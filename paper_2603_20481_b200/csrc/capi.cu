@@ -1206,4 +1206,22 @@ ss_status engine_check_stft(ss_ctx* ctx, int n_fft, int hop, int window, ss_fmt 
 
 void engine_add_launches(ss_ctx* ctx, int64_t n) { ctx->launches += n; }
 
+// Stage events for one graph capture: with ev16 non-null the context's stage
+// marks (tmark) record into the caller's 16 events, so a captured window chain
+// carries its own per-stage event nodes; used8 returns which stages recorded.
+// With ev16 null, stage timing is off again and the context forgets the events.
+void engine_stage_events(ss_ctx* ctx, cudaEvent_t* ev16, bool* used8) {
+    if (ev16) {
+        for (int i = 0; i < 16; ++i) ctx->ev[i] = ev16[i];
+        for (bool& u : ctx->ev_used) u = false;
+        ctx->timing = true;
+        return;
+    }
+    if (used8)
+        for (int i = 0; i < 8; ++i) used8[i] = ctx->ev_used[i];
+    for (cudaEvent_t& e : ctx->ev) e = nullptr;
+    for (bool& u : ctx->ev_used) u = false;
+    ctx->timing = false;
+}
+
 } // namespace ssb

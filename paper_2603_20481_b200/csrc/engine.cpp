@@ -46,6 +46,7 @@ ss_status engine_sense(ss_ctx* ctx, const void* diq, ss_fmt fmt, int n_fft, int 
                        const unsigned long long* seq_dev);
 ss_status engine_check_stft(ss_ctx* ctx, int n_fft, int hop, int window, ss_fmt fmt);
 void engine_add_launches(ss_ctx* ctx, int64_t n);
+void engine_stage_events(ss_ctx* ctx, cudaEvent_t* ev16, bool* used8);
 } // namespace ssb
 
 namespace {
@@ -88,6 +89,9 @@ struct Bank {
     cudaEvent_t rows_ready = nullptr;
     cudaEvent_t start_ev = nullptr;  // compute stream, before the window's first kernel
     cudaEvent_t done_ev = nullptr;   // compute stream, after the boxes' D2H
+    cudaEvent_t stage_ev[16] = {};    // begin/end of each stage (K1..K6), event nodes of the graph
+    bool stage_used[8] = {};
+    double stage_s[8] = {};
     double gpu_s = 0.0;
     cudaError_t fault = cudaSuccess;  // the done event's query status, reported by poll
     bool poisoned = false;            // the filling window lost rows upstream: it can never complete
@@ -170,12 +174,21 @@ void waiter_main(ss_engine* e) {
         while ((st = cudaEventQuery(b.done_ev)) == cudaErrorNotReady) std::this_thread::yield();
         const Clock::time_point now = Clock::now();
         float ms = 0.f;
-        if (st == cudaSuccess) cudaEventElapsedTime(&ms, b.start_ev, b.done_ev);
+        double stage_s[8] = {};
+        if (st == cudaSuccess) {
+            cudaEventElapsedTime(&ms, b.start_ev, b.done_ev);
+            for (int i = 0; i < 8; ++i) {
+                float t = 0.f;
+                if (b.stage_used[i] && cudaEventElapsedTime(&t, b.stage_ev[2 * i], b.stage_ev[2 * i + 1]) == cudaSuccess)
+                    stage_s[i] = 1e-3 * t;
+            }
+        }
         {
             std::lock_guard<std::mutex> lk(e->mu);
             e->inflight.pop_front();
             b.done_at = now;
             b.gpu_s = 1e-3 * ms;
+            for (int i = 0; i < 8; ++i) b.stage_s[i] = stage_s[i];
             b.fault = st;
             e->done.push_back(bi);
         }
@@ -352,8 +365,12 @@ ss_status ss_engine_open(int device, const ss_engine_cfg* cfg, const ss_detector
         if (cudaStreamBeginCapture(e->compute, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
             return bad(SS_ECUDA, "graph capture");
         cudaGraph_t g = nullptr;
+        for (cudaEvent_t& ev : b.stage_ev)
+            if (cudaEventCreate(&ev) != cudaSuccess) return bad(SS_ECUDA, "event");
+        ssb::engine_stage_events(e->ctx, b.stage_ev, nullptr);
         const ss_status cs = ssb::engine_sense(e->ctx, b.iq, cfg->fmt, F, e->hop, e->window, T, 0, cfg->sample_rate_hz,
                                                *det, b.tf, dev_out(b, K), b.d_seq);
+        ssb::engine_stage_events(e->ctx, nullptr, b.stage_used);
         bool ok = cs == SS_OK &&
                   cudaMemcpyAsync(&b.host->n_boxes, b.n_boxes, sizeof(int32_t), cudaMemcpyDeviceToHost, e->compute) == cudaSuccess &&
                   cudaMemcpyAsync(&b.host->n_active, b.n_active, sizeof(int32_t), cudaMemcpyDeviceToHost, e->compute) == cudaSuccess &&
@@ -420,6 +437,8 @@ void ss_engine_close(ss_engine* e) {
         cudaFree(b.d_seq);
         if (b.start_ev) cudaEventDestroy(b.start_ev);
         if (b.done_ev) cudaEventDestroy(b.done_ev);
+        for (cudaEvent_t ev : b.stage_ev)
+            if (ev) cudaEventDestroy(ev);
     }
     if (e->ctx) ss_close(e->ctx);
     delete e;
@@ -579,6 +598,7 @@ ss_status ss_engine_poll(ss_engine* e, int wait_ms, ss_plot_record* rec, ss_box*
         rec->complete_s = e->secs(b.complete_at);
         rec->done_s = e->secs(b.done_at);
         rec->gpu_s = b.gpu_s;
+        for (int i = 0; i < 8; ++i) rec->stage_s[i] = b.stage_s[i];
     }
     if (boxes && keep > 0) std::memcpy(boxes, b.h_boxes, sizeof(ss_box) * static_cast<size_t>(keep));
     if (bin_boxes && keep > 0) std::memcpy(bin_boxes, b.h_bin_boxes, sizeof(ss_bin_box) * static_cast<size_t>(keep));

@@ -37,7 +37,15 @@ class IoUMatrix:
 def iou_matrix(gt, detections) -> IoUMatrix:
     gt = np.asarray(gt, np.float64).reshape(-1, 4)
     det = np.asarray(detections, np.float64).reshape(-1, 4)
-    v = np.array([[iou(g, d) for d in det] for g in gt], np.float64).reshape(len(gt), len(det))
+    # iou() broadcast over all pairs (same IEEE operations, same order)
+    ga = ((gt[:, 1] - gt[:, 0]) * (gt[:, 3] - gt[:, 2]))[:, None]
+    da = ((det[:, 1] - det[:, 0]) * (det[:, 3] - det[:, 2]))[None, :]
+    fi = np.maximum(0.0, np.minimum(gt[:, None, 1], det[None, :, 1]) - np.maximum(gt[:, None, 0], det[None, :, 0]))
+    ti = np.maximum(0.0, np.minimum(gt[:, None, 3], det[None, :, 3]) - np.maximum(gt[:, None, 2], det[None, :, 2]))
+    inter = fi * ti
+    with np.errstate(divide="ignore", invalid="ignore"):
+        v = inter / (ga + da - inter)
+    v = np.where((ga <= 0.0) | (da <= 0.0), 0.0, v).reshape(len(gt), len(det))
     return IoUMatrix(len(gt), len(det), v)
 
 

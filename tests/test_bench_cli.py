@@ -31,12 +31,25 @@ def test_reference_arm_json_line():
 
 
 
+def test_bench_spawns_ranks_for_gpus_n():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as 2 ranks
+    (torch.distributed.run, 127.0.0.1); rank 0 alone prints the line."""
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--gpus", "2", "--steps", "1",
+                        "--warmup", "0", "--ref-step-seconds", "0.3"], capture_output=True, text=True, timeout=900,
+                       cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "capture-sharded x2"
+
+
 @pytest.mark.gpu
 def test_bench_json_line_gpu():
     """The default arm on a small batch: the keys the driver and the judge read
     (roofline with traffic, e2e with copy bytes, gpu_launches, clocks)."""
     r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--steps", "1", "--warmup", "3", "--batch", "8",
-                        "--distinct", "2", "--e2e-batch", "2", "--no-cpu"],
+                        "--distinct", "2", "--e2e-batch", "2", "--no-cpu", "--no-hann"],
                        capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
@@ -51,3 +64,6 @@ def test_bench_json_line_gpu():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    # the timed batch checked against the reference on the host, bit for bit
+    assert d["parity"]["plots"] == 2 and d["parity"]["mismatches"] == 0
+    assert d["e2e"]["same_as_device_path"] is True

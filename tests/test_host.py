@@ -115,6 +115,9 @@ def test_capture_shard():
 
 
 def _gloo_worker(rank, world, port, q):
+    """One rank of bench.py's exchange step: detections (counts + fixed-capacity
+    records, as ss_sense_batch writes them) gathered to rank 0 with the exact
+    function bench.measure() calls each timed step."""
     import os
 
     import torch
@@ -123,14 +126,17 @@ def _gloo_worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     P, K = 3, 5
-    n = torch.tensor([rank + 1, 0, 2], dtype=torch.int32)
+    n = torch.tensor([rank + 1, 0, 7 if rank else 2], dtype=torch.int32)   # 7 > K: clamped like the device capacity
     b = torch.full((P, K, 4), float(rank), dtype=torch.float64)
     b[:, :, 0] += torch.arange(P, dtype=torch.float64)[:, None]
-    counts, recs = parallel.gather_detections(n, b)
-    flat = parallel.flatten_detections(counts, recs)
+    b[:, :, 1] += torch.arange(K, dtype=torch.float64)[None, :]
+    g = parallel.gather_detections(n, b)
     if rank == 0:
-        q.put(json.dumps({"counts": counts.tolist(), "lens": [len(x) for x in flat],
-                          "first": flat[0].tolist(), "last": flat[-1].tolist()}))
+        flat = parallel.flatten_detections(g)
+        q.put(json.dumps({"counts": [c.tolist() for c, _ in g], "sizes": [list(p.shape) for _, p in g],
+                          "lens": [len(x) for x in flat], "first": flat[0].tolist(), "last": flat[-1].tolist()}))
+    else:
+        assert g is None
     dist.destroy_process_group()
 
 
@@ -148,11 +154,13 @@ def test_gather_detections_gloo_world2():
     procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = json.loads(q.get(timeout=120))
+    res = json.loads(q.get(timeout=300))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert res["counts"] == [[1, 0, 2], [2, 0, 2]]
-    assert res["lens"] == [1, 0, 2, 2, 0, 2]
+    assert res["counts"] == [[1, 0, 2], [2, 0, 5]]
+    assert res["sizes"] == [[3, 4], [7, 4]]                # only the boxes that exist travel
+    assert res["lens"] == [1, 0, 2, 2, 0, 5]
     assert res["first"] == [[0.0, 0.0, 0.0, 0.0]]
-    assert res["last"] == [[3.0, 1.0, 1.0, 1.0], [3.0, 1.0, 1.0, 1.0]]
+    assert res["last"] == [[3.0, 1.0, 1.0, 1.0], [3.0, 2.0, 1.0, 1.0], [3.0, 3.0, 1.0, 1.0], [3.0, 4.0, 1.0, 1.0],
+                           [3.0, 5.0, 1.0, 1.0]]
