@@ -115,7 +115,12 @@ void tmark(ss_ctx* ctx, int stage, int end) {
     if (!ctx->timing) return;
     cudaEvent_t& e = ctx->ev[2 * stage + end];
     if (!e) cudaEventCreate(&e);
-    cudaEventRecord(e, ctx->stream);
+    // under stream capture (the engine's per-bank graphs) a plain record only
+    // orders the capture; an external record becomes a timed event node
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(ctx->stream, &cap);
+    if (cap == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, ctx->stream, cudaEventRecordExternal);
+    else cudaEventRecord(e, ctx->stream);
     if (end) ctx->ev_used[stage] = true;
 }
 
