@@ -15,7 +15,7 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-CSRC = PKG / "csrc"
+CSRC = Path(os.environ.get("SSB_CSRC", PKG / "csrc"))  # override: A/B builds of patched sources
 LIB = Path(os.environ.get("SSB_BUILD_DIR", PKG / "_lib"))
 OBJ = LIB / "obj"
 SO = LIB / "libspecsense_b200.so"

@@ -148,6 +148,100 @@ __device__ __forceinline__ int otsu_split_warp(const uint32_t* hq, int lane) {
     return best_i;
 }
 
+// Tile path (<= 2 * kTileMaxRows rows per column): the same search with the
+// prefix sums in uint32.
+__device__ __forceinline__ int otsu_split_warp_u32(const uint32_t* hq, int lane) {
+    // counts and bin-weighted sums are integers below 2^32 (<= 12288 rows of
+    // one column, bins <= 255): their prefix sums are exact in uint32, in any
+    // order, and convert exactly to the doubles the reference accumulates
+    uint32_t cnt[8], wsum[8];
+    uint32_t lc = 0u, ls = 0u;
+    uint32_t nz = 0;  // bins whose count is non-zero (or bin 0)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t bin = static_cast<uint32_t>(lane * 8 + q);
+        lc += hq[q];
+        ls += bin * hq[q];
+        cnt[q] = lc;
+        wsum[q] = ls;
+        nz |= (hq[q] != 0u || bin == 0u) ? (1u << q) : 0u;
+    }
+    // exclusive prefix over lanes of (lc, ls)
+    uint32_t pcu = lc, psu = ls;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t tc = __shfl_up_sync(0xffffffffu, pcu, o);
+        const uint32_t ts = __shfl_up_sync(0xffffffffu, psu, o);
+        if (lane >= o) {
+            pcu += tc;
+            psu += ts;
+        }
+    }
+    const uint32_t total_u = __shfl_sync(0xffffffffu, pcu, 31);
+    const uint32_t sum_all_u = __shfl_sync(0xffffffffu, psu, 31);
+    pcu -= lc;
+    psu -= ls;
+    const double total = static_cast<double>(total_u);
+    const double sum_all = static_cast<double>(sum_all_u);
+
+    // estimates: D = sum0*w1 - sum1*w0 exactly in int64 (|D| < 2^37), p = w0*w1 < 2^26
+    double est[8];
+    double m = -1.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t w0 = pcu + cnt[q];
+        const uint32_t w1 = total_u - w0;
+        double e = ((nz >> q) & 1u) ? 0.0 : -1.0;
+        if (((nz >> q) & 1u) && w0 > 0u && w1 > 0u) {
+            const uint32_t s0 = psu + wsum[q];
+            const uint32_t s1 = sum_all_u - s0;
+            const long long dd = static_cast<long long>(s0) * w1 - static_cast<long long>(s1) * w0;
+            const double d = static_cast<double>(dd);
+            const double p = static_cast<double>(w0 * w1);
+            e = __dmul_rn(__dmul_rn(d, d), rcp_newton(p));
+        }
+        est[q] = e;
+        m = fmax(m, e);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const double floor_v = m - (m * 0x1p-30 + total * total * 0x1p-34);
+
+    double best_v = -1.0;
+    int best_i = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        if (est[q] >= floor_v && est[q] >= 0.0) {
+            const uint32_t w0u = pcu + cnt[q];
+            const double w0 = static_cast<double>(w0u);
+            const double w1 = static_cast<double>(total_u - w0u);
+            double var = 0.0;
+            if (w0 > 0.0 && w1 > 0.0) {
+                const double sum0 = static_cast<double>(psu + wsum[q]);
+                const double mu0 = __ddiv_rn(sum0, w0);
+                const double mu1 = __ddiv_rn(__dsub_rn(sum_all, sum0), w1);
+                const double d = __dsub_rn(mu0, mu1);
+                var = __dmul_rn(__dmul_rn(__dmul_rn(w0, w1), d), d);
+            }
+            if (var > best_v) {
+                best_v = var;
+                best_i = lane * 8 + q;
+            }
+        }
+    }
+    // first maximum across lanes (ties -> lowest split index)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best_v, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+        if (ov > best_v || (ov == best_v && oi < best_i)) {
+            best_v = ov;
+            best_i = oi;
+        }
+    }
+    return best_i;
+}
+
 __global__ void __launch_bounds__(kBinThreads) binarize_kernel(BinarizeLaunch a) {
     __shared__ uint32_t hist[32 * kHistStride];
     __shared__ float s_lo[kBinWarps][32], s_hi[kBinWarps][32];
@@ -398,16 +492,20 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
         const int hh = tid & 1;
         float lo4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
         float hi4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        // exactly two rows of each box per thread, branch-free: rows past the
+        // CTA's last row re-read that row (a repeated value changes no extreme)
+        static_assert(kBox == 2 * (kBinThreads / 2), "two rows of a box per thread");
+        const int last = rows - 1;
         for (int b = 0; b < nbox; ++b) {
             mbar_wait(&box_bar[b], 0);
-            const int rend = min(rows, (b + 1) * kBox);
-            for (int r = b * kBox + (tid >> 1); r < rend; r += kBinThreads / 2) {
-                const float4 x = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols + 4 * hh);
-                lo4[0] = fminf(lo4[0], x.x); hi4[0] = fmaxf(hi4[0], x.x);
-                lo4[1] = fminf(lo4[1], x.y); hi4[1] = fmaxf(hi4[1], x.y);
-                lo4[2] = fminf(lo4[2], x.z); hi4[2] = fmaxf(hi4[2], x.z);
-                lo4[3] = fminf(lo4[3], x.w); hi4[3] = fmaxf(hi4[3], x.w);
-            }
+            const int r0 = min(b * kBox + (tid >> 1), last);
+            const int r1 = min(b * kBox + kBinThreads / 2 + (tid >> 1), last);
+            const float4 x = *reinterpret_cast<const float4*>(bt_vals + r0 * kTileCols + 4 * hh);
+            const float4 y = *reinterpret_cast<const float4*>(bt_vals + r1 * kTileCols + 4 * hh);
+            lo4[0] = fminf(lo4[0], fminf(x.x, y.x)); hi4[0] = fmaxf(hi4[0], fmaxf(x.x, y.x));
+            lo4[1] = fminf(lo4[1], fminf(x.y, y.y)); hi4[1] = fmaxf(hi4[1], fmaxf(x.y, y.y));
+            lo4[2] = fminf(lo4[2], fminf(x.z, y.z)); hi4[2] = fmaxf(hi4[2], fmaxf(x.z, y.z));
+            lo4[3] = fminf(lo4[3], fminf(x.w, y.w)); hi4[3] = fmaxf(hi4[3], fmaxf(x.w, y.w));
         }
 #pragma unroll
         for (int o = 2; o < 32; o <<= 1)
@@ -525,7 +623,7 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
 #pragma unroll
             for (int q = 0; q < 8; ++q) hq[q] += hist_peer[cc * kHistStride + lane * 8 + q];
         }
-        const int best_i = otsu_split_warp(hq, lane);
+        const int best_i = otsu_split_warp_u32(hq, lane);
         if (lane == 0) {
             const double lod = static_cast<double>(c_lo[cc]);
             const double e = __ddiv_rn(__dmul_rn(static_cast<double>(best_i) + 1.0, c_span[cc]), 256.0);

@@ -1,7 +1,7 @@
 // capi.cu -- the extern "C" boundary (include/specsense_b200.h): context,
 // device workspace, argument validation with the reference's error
 // semantics, and the fused batch pipelines that chain K1..K6 on one stream.
-#include "../../include/specsense_b200.h"
+#include "specsense_b200.h"
 #include "internal.h"
 #include "baseline_host.h"
 

@@ -64,22 +64,25 @@ cudaError_t unpack_launch(const uint32_t* bits, int n_plots, int rows, int cols,
 }
 
 // ------------------------------------------------------------- fused chain
-// Register-resident form: a warp owns a band of kRegRows (16) output rows x 30
-// mask words.  Lane l holds word (band*30 + l - 1) for kRegNR = kRegRows +
-// 2*kRegHalo consecutive rows in registers; lanes 0 and 31 are halo words.
-// Vertical erode/dilate is register-to-register (rows i-1, i, i+1 of the same
-// lane), horizontal is shift/carry with the neighbouring lanes' words
-// (__shfl_up/down).  The six steps move information at most 6 rows and 6
-// columns, so the halo rows / words absorb the invalid band: no shared
-// memory, no barriers.  Out-of-image rows and words are zeroed and the last
-// word masked after every step (out-of-image = background for erode and
-// dilate, detector.cpp:359-362, 393-410).
-constexpr int kRegRows = 16;
-constexpr int kRegHalo = 8;  // >= 6: the largest vertical reach (3x3 close + open + 3x1 line)
-constexpr int kRegNR = kRegRows + 2 * kRegHalo;
-constexpr int kRegOwn = 30;  // owned words per warp
+// Register-resident form: a warp owns a band of 16 output rows x 30 mask
+// words.  Lane l holds word (band*30 + l - 1) for kRegNR = 16 + 2*HALO
+// consecutive rows in registers; lanes 0 and 31 are halo words.  Vertical
+// erode/dilate is register-to-register (rows i-1, i, i+1 of the same lane),
+// horizontal is a funnel shift with the neighbouring lanes' words
+// (__shfl_up/down).  Each step moves information at most one row / column,
+// so HALO rows (the chain's vertical reach: 4 for close3x3 + open3x3 + the
+// 1x3 line, 6 with the 3x1 line) and one halo word per side (horizontal
+// reach <= 6 columns) absorb the invalid margin: no shared memory, no
+// barriers.  Out-of-image rows and words are zeroed and the last word masked
+// after every step (out-of-image = background for erode and dilate,
+// detector.cpp:359-362, 393-410).
+constexpr int kRegOwnRows = 16;  // 16 owned rows beat 24 (0.634 vs 0.718 ms per C5r step: occupancy)
+constexpr int kRegOwn = 30;      // owned words per warp
 
+template <int HALO>
 struct RegBand {
+    static constexpr int OWN = kRegOwnRows;
+    static constexpr int kRegNR = OWN + 2 * HALO;
     uint32_t x[kRegNR];
     int lo, hi;        // buffer rows [lo, hi) lie inside the image
     uint32_t wmask;    // 0 outside the image's words; last word: valid columns only
@@ -103,8 +106,8 @@ struct RegBand {
             const uint32_t v = x[i];
             const uint32_t prev = __shfl_up_sync(0xffffffffu, v, 1);    // word w-1 (lane 0: its own, halo)
             const uint32_t next = __shfl_down_sync(0xffffffffu, v, 1);  // word w+1 (lane 31: its own, halo)
-            const uint32_t left = (v << 1) | (prev >> 31);
-            const uint32_t right = (v >> 1) | (next << 31);
+            const uint32_t left = __funnelshift_l(prev, v, 1);          // (v << 1) | (prev >> 31)
+            const uint32_t right = __funnelshift_r(v, next, 1);         // (v >> 1) | (next << 31)
             x[i] = erode ? (v & left & right) : (v | left | right);
         }
     }
@@ -129,20 +132,23 @@ struct RegBand {
 };
 
 // in/out: word-major bits [p][W][rows].  One warp per (row band, word band).
+template <int HALO>
 __global__ void __launch_bounds__(128) consolidate_kernel(const uint32_t* __restrict__ in, int rows, int cols,
                                                           int wbands, long long bands, bool along_time,
                                                           uint32_t* __restrict__ out,
                                                           const uint32_t* __restrict__ active_bits) {
+    using RB = RegBand<HALO>;
     const int W = (cols + 31) / 32;
     const int lane = threadIdx.x & 31;
     const long long gwarp = blockIdx.x * 4LL + (threadIdx.x >> 5);
     if (gwarp >= bands) return;  // uniform per warp
     const int p = blockIdx.y;
     const int rb = static_cast<int>(gwarp / wbands), wb = static_cast<int>(gwarp % wbands);
-    const int r0 = rb * kRegRows, row0 = r0 - kRegHalo;
+    const int r0 = rb * RB::OWN, row0 = r0 - HALO;
     const int gw = wb * kRegOwn + lane - 1;
     const bool wvalid = gw >= 0 && gw < W;
-    RegBand t;
+    constexpr int kRegNR = RB::kRegNR;
+    RB t;
     t.lo = max(0, -row0);
     t.hi = min(kRegNR, rows - row0);
     t.wmask = !wvalid ? 0u : ((gw == W - 1 && (cols & 31)) ? ((1u << (cols & 31)) - 1u) : 0xffffffffu);
@@ -157,14 +163,14 @@ __global__ void __launch_bounds__(128) consolidate_kernel(const uint32_t* __rest
     for (int i = 0; i < kRegNR; ++i) t.x[i] = (wvalid && i >= t.lo && i < t.hi) ? (__ldg(src + i) & keep) : 0u;
     // interior bands (most of a plot) skip the out-of-image clipping entirely
     const bool interior = t.lo == 0 && t.hi == kRegNR && t.wmask == 0xffffffffu;
-    if (__all_sync(0xffffffffu, interior)) t.chain<false>(along_time);
-    else t.chain<true>(along_time);
+    if (__all_sync(0xffffffffu, interior)) t.template chain<false>(along_time);
+    else t.template chain<true>(along_time);
     if (!wvalid || lane == 0 || lane == 31) return;
     uint32_t* dst = out + (static_cast<long long>(p) * W + gw) * rows + r0;
-    const int nrow = min(kRegRows, rows - r0);
+    const int nrow = min(RB::OWN, rows - r0);
 #pragma unroll
-    for (int i = 0; i < kRegRows; ++i)
-        if (i < nrow) dst[i] = t.x[kRegHalo + i];
+    for (int i = 0; i < RB::OWN; ++i)
+        if (i < nrow) dst[i] = t.x[HALO + i];
 }
 
 cudaError_t consolidate_bits_launch(const uint32_t* in, int n_plots, int rows, int cols, bool along_time,
@@ -172,9 +178,14 @@ cudaError_t consolidate_bits_launch(const uint32_t* in, int n_plots, int rows, i
     if (n_plots <= 0 || rows <= 0 || cols <= 0) return cudaSuccess;
     const int W = (cols + 31) / 32;
     const int wbands = (W + kRegOwn - 1) / kRegOwn;
-    const long long bands = static_cast<long long>((rows + kRegRows - 1) / kRegRows) * wbands;
+    // vertical reach of the chain: 4 rows (1x3 line), 6 (3x1 line)
+    const int own = along_time ? RegBand<6>::OWN : RegBand<4>::OWN;
+    const long long bands = static_cast<long long>((rows + own - 1) / own) * wbands;
     dim3 grid(static_cast<unsigned>((bands + 3) / 4), n_plots);
-    consolidate_kernel<<<grid, 128, 0, st>>>(in, rows, cols, wbands, bands, along_time, out, active_bits);
+    if (along_time)
+        consolidate_kernel<6><<<grid, 128, 0, st>>>(in, rows, cols, wbands, bands, along_time, out, active_bits);
+    else
+        consolidate_kernel<4><<<grid, 128, 0, st>>>(in, rows, cols, wbands, bands, along_time, out, active_bits);
     return cudaGetLastError();
 }
 
