@@ -478,10 +478,15 @@ def measure(args, wl, B, D, steps, warmup, e2e_batch, with_gather=True):
         if ws > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # asynchronous batches (ss_set_async): step i+1's host->device copies
+        # queue behind step i without a host round trip; ss_wait checks them all
+        ctx.check(lib.ss_set_async(ctx.h, 1))
         e0.record(stream)
         for _ in range(steps):
             e2e_step()
         e1.record(stream)
+        ctx.check(lib.ss_wait(ctx.h))
+        ctx.check(lib.ss_set_async(ctx.h, 0))
         torch.cuda.synchronize()
         e2e_el = e0.elapsed_time(e1) / 1e3
         if ws > 1:

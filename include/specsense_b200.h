@@ -109,6 +109,19 @@ void ss_default_detector_cfg(ss_detector_cfg* cfg);
    default stream).  A new context uses its own non-blocking stream. */
 ss_status ss_set_stream(ss_ctx* ctx, void* stream);
 ss_status ss_synchronize(ss_ctx* ctx);
+/* Asynchronous batches.  With on != 0, ss_sense_batch, ss_stft_sense_batch and
+   ss_detect_batch return as soon as their work is queued on the context
+   stream -- no host synchronisation, so back-to-back batches overlap (outputs
+   in pinned host memory or on the device; a pageable host output makes its
+   copy, and so the call, synchronous).  The checks a synchronous call makes
+   before returning (box capacity, CCL run-pool overflow) run on the device and
+   are reported by ss_wait for every batch since the previous ss_wait:
+   SS_ECAPACITY if a plot had more boxes than box_capacity or more runs than
+   the shared pool (its results are then incomplete: re-run those batches with
+   async off, which sizes the pool exactly).  on = 0 restores synchronous calls. */
+ss_status ss_set_async(ss_ctx* ctx, int on);
+/* Wait for all queued work of the context; SS_ECAPACITY as described above. */
+ss_status ss_wait(ss_ctx* ctx);
 /* Device kernel launches issued by this context so far (instrumentation). */
 int64_t ss_launch_count(const ss_ctx* ctx);
 /* Per-stage CUDA-event timing of the batch pipelines (on the context stream):

@@ -68,6 +68,8 @@ SIGNATURES = {
     "ss_default_detector_cfg": (None, [C.POINTER(DetectorCfg)]),
     "ss_set_stream": (_I, [_P, _P]),
     "ss_synchronize": (_I, [_P]),
+    "ss_set_async": (_I, [_P, _I]),
+    "ss_wait": (_I, [_P]),
     "ss_launch_count": (C.c_int64, [_P]),
     "ss_enable_stage_timing": (_I, [_P, _I]),
     "ss_stage_times": (_I, [_P, C.POINTER(C.c_double)]),

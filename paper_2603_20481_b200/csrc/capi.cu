@@ -50,6 +50,10 @@ struct ss_ctx {
     bool exact_pool = false;
     int64_t launches = 0;
     // optional per-stage timing (CUDA events on the context stream)
+    // asynchronous batches (ss_set_async): device-side check flags
+    // {pool overflow seen, largest box count above capacity}, read by ss_wait
+    bool async = false;
+    int* async_flags = nullptr;
     bool timing = false;
     cudaEvent_t ev[2 * 8] = {};
     bool ev_used[8] = {};
@@ -225,12 +229,31 @@ bool is_device_ptr(const void* p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// async-mode checks, on the device: OR a CCL pool-overflow flag in; record
+// the largest box count above the capacity
+__global__ void note_overflow_kernel(const int* of, int* flags) {
+    if (*of) flags[0] = 1;
+}
+__global__ void note_capacity_kernel(const int* n_boxes, int n, int cap, int* flags) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        if (n_boxes[i] > cap) atomicMax(flags + 1, n_boxes[i]);
+}
+
+ss_status async_flags(ss_ctx* ctx, int** out) {
+    if (!ctx->async_flags) {
+        SS_CK(ctx, cudaMalloc(&ctx->async_flags, 2 * sizeof(int)));
+        SS_CK(ctx, cudaMemsetAsync(ctx->async_flags, 0, 2 * sizeof(int), ctx->stream));
+    }
+    *out = ctx->async_flags;
+    return SS_OK;
+}
+
 // CCL over n_plots bit masks with a pool of pool_cap runs; fills the workspace
 // pointers and launches.
 ss_status run_ccl(ss_ctx* ctx, const uint32_t* bits, int n_plots, int rows, int cols, int min_area,
                   long long pool_cap, int* n_comp, long long cap, long long* extents, int* bin_boxes,
                   double* boxes, const unsigned long long* start_seq, double fs, int32_t* labels,
-                  int* overflow_host, int time_bins = 0) {
+                  int* overflow_host, int time_bins = 0, int* overflow_acc = nullptr) {
     ssb::CclLaunch L;
     L.time_bins = time_bins;
     L.bits = bits;
@@ -279,6 +302,11 @@ ss_status run_ccl(ss_ctx* ctx, const uint32_t* bits, int n_plots, int rows, int 
     SS_CK(ctx, ssb::ccl_launch(L, ctx->stream));
     ctx->launches += 7 + (rows > 1 ? 1 : 0) + (rows > 16 ? 1 : 0) + (labels ? 1 : 0);
     if (overflow_host) SS_CK(ctx, cudaMemcpyAsync(overflow_host, of, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    if (overflow_acc) {
+        note_overflow_kernel<<<1, 1, 0, ctx->stream>>>(of, overflow_acc);
+        SS_CK(ctx, cudaGetLastError());
+        ctx->launches += 1;
+    }
     return SS_OK;
 }
 
@@ -359,6 +387,18 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
         s = run_ccl(ctx, m1, n_plots, rows, cols, cfg.min_component_area, worst_pool(rows, cols) * n_plots,
                     out_dev.n_boxes ? out_dev.n_boxes : ncomp, cap, nullptr, reinterpret_cast<int*>(out_dev.bin_boxes),
                     reinterpret_cast<double*>(out_dev.boxes), seq_dev, fs, nullptr, nullptr, time_bins);
+        tmark(ctx, 5, 1);
+        return s;
+    }
+    if (ctx->async) {  // no host round trip: the overflow check goes to ss_wait
+        int* flags = nullptr;
+        s = async_flags(ctx, &flags);
+        if (s != SS_OK) return s;
+        tmark(ctx, 5, 0);
+        s = run_ccl(ctx, m1, n_plots, rows, cols, cfg.min_component_area, default_pool(n_plots, rows, cols),
+                    out_dev.n_boxes ? out_dev.n_boxes : ncomp, cap, nullptr,
+                    reinterpret_cast<int*>(out_dev.bin_boxes), reinterpret_cast<double*>(out_dev.boxes), seq_dev, fs,
+                    nullptr, nullptr, time_bins, flags);
         tmark(ctx, 5, 1);
         return s;
     }
@@ -459,6 +499,7 @@ void ss_close(ss_ctx* ctx) {
     for (auto& kv : ctx->sg) cudaFree(kv.second);
     for (auto& kv : ctx->win) cudaFree(kv.second);
     for (auto& kv : ctx->ws) cudaFree(kv.second.p);
+    if (ctx->async_flags) cudaFree(ctx->async_flags);
     for (cudaEvent_t e : ctx->ev)
         if (e) cudaEventDestroy(e);
     for (int b = 0; b < 2; ++b) {
@@ -485,6 +526,27 @@ ss_status ss_set_stream(ss_ctx* ctx, void* stream) {
 ss_status ss_synchronize(ss_ctx* ctx) {
     if (!ctx) return SS_EVALIDATION;
     SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    return SS_OK;
+}
+
+ss_status ss_set_async(ss_ctx* ctx, int on) {
+    if (!ctx) return SS_EVALIDATION;
+    ctx->async = on != 0;
+    return SS_OK;
+}
+
+ss_status ss_wait(ss_ctx* ctx) {
+    if (!ctx) return SS_EVALIDATION;
+    int* h = ctx->pinned + 8;  // pinned words 8, 9
+    h[0] = h[1] = 0;
+    if (ctx->async_flags) {
+        SS_CK(ctx, cudaMemcpyAsync(h, ctx->async_flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        SS_CK(ctx, cudaMemsetAsync(ctx->async_flags, 0, 2 * sizeof(int), ctx->stream));
+    }
+    SS_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    tcollect(ctx);
+    if (h[0]) return fail(ctx, SS_ECAPACITY, "CCL run pool overflow in an asynchronous batch: re-run it with async off");
+    if (h[1]) return fail(ctx, SS_ECAPACITY, "box capacity too small: " + std::to_string(h[1]));
     return SS_OK;
 }
 
@@ -770,6 +832,15 @@ ss_status ss_detect_batch(ss_ctx* ctx, const float* tf, int n_plots, int rows, i
     float* praw = out->psd_raw ? out->psd_raw : psd;
     s = detect_device(ctx, tf, n_plots, rows, cols, seq, sample_rate_hz, *cfg, praw, false, *out);
     if (s != SS_OK) return s;
+    if (out->n_boxes && out->box_capacity >= 0 && ctx->async) {
+        int* flags = nullptr;
+        s = async_flags(ctx, &flags);
+        if (s != SS_OK) return s;
+        note_capacity_kernel<<<1, 256, 0, ctx->stream>>>(out->n_boxes, n_plots, out->box_capacity, flags);
+        SS_CK(ctx, cudaGetLastError());
+        ctx->launches += 1;
+        return SS_OK;
+    }
     if (out->n_boxes && out->box_capacity >= 0) {
         std::vector<int> nb(static_cast<size_t>(n_plots));
         SS_CK(ctx, cudaMemcpy(nb.data(), out->n_boxes, sizeof(int) * n_plots, cudaMemcpyDeviceToHost));
@@ -1011,6 +1082,17 @@ static ss_status sense_impl(ss_ctx* ctx, const void* iq, ss_fmt fmt, int n_fft, 
         SS_CK(ctx, cp(out->bin_boxes, dev.bin_boxes, sizeof(ss_bin_box) * n_plots * K));
         SS_CK(ctx, cp(out->n_boxes, dev.n_boxes, sizeof(int32_t) * n_plots));
         tmark(ctx, 7, 1);
+    }
+    if (ctx->async) {  // the capacity check goes to ss_wait as well
+        if (out->n_boxes) {
+            int* flags = nullptr;
+            s = async_flags(ctx, &flags);
+            if (s != SS_OK) return s;
+            note_capacity_kernel<<<1, 256, 0, ctx->stream>>>(dev.n_boxes, n_plots, K, flags);
+            SS_CK(ctx, cudaGetLastError());
+            ctx->launches += 1;
+        }
+        return SS_OK;
     }
     if (out->n_boxes) {
         std::vector<int> nb(static_cast<size_t>(n_plots));

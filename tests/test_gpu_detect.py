@@ -327,3 +327,62 @@ def test_reference_scenario_fixtures(ss, ref, name, rows):
     for p, det in enumerate(dets):
         exp = ref.detect(exp_tf[p], start_seq=p * rows, fs=fs)
         _check(det, exp, tf[p], exp_tf[p])
+
+
+def test_async_batches_match_sync(ss, ref):
+    """ss_set_async: back-to-back batches from pinned host IQ into pinned host
+    outputs queue without a host synchronisation; after ss_wait their results
+    equal the synchronous calls bit for bit, and an exceeded box capacity is
+    reported by ss_wait (not by the call)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2603_20481_b200 import _native as NAT
+    ctx = ss.Context.get(0)
+    lib = ctx.lib
+    fs, n_fft, rows, P = 100e6, 1024, 500, 4
+    iqs = []
+    for k in range(2):
+        iq, _ = ref.synthesize(signals.scenario_json(signals.paper_scenario(rows=P * rows, seed=11 + k)))
+        h = torch.from_numpy(np.ascontiguousarray(iq[: P * rows * n_fft])).pin_memory()
+        iqs.append(h)
+    cfg = ss.DetectorConfig().c()
+
+    def outs(K):
+        o = dict(raw=torch.empty((P, n_fft), dtype=torch.float32), sm=torch.empty((P, n_fft), dtype=torch.float32),
+                 ft=torch.empty((P, 2), dtype=torch.float32), act=torch.empty((P, n_fft), dtype=torch.int32),
+                 nact=torch.empty(P, dtype=torch.int32), boxes=torch.empty((P, K, 4), dtype=torch.float64),
+                 bins=torch.empty((P, K, 4), dtype=torch.int32), nb=torch.empty(P, dtype=torch.int32))
+        o = {k: v.pin_memory() for k, v in o.items()}
+        return o, NAT.BatchOut(*(C.c_void_p(v.data_ptr()) for v in o.values()), K)
+
+    def call(h, bo):
+        return lib.ss_sense_batch(ctx.h, C.c_void_p(h.data_ptr()), NAT.SS_FMT_F32, n_fft, rows, P, C.c_uint64(0),
+                                  C.c_double(fs), C.byref(cfg), None, C.byref(bo))
+
+    sync = []
+    for h in iqs:
+        o, bo = outs(1024)
+        ctx.check(call(h, bo))
+        sync.append(o)
+    ctx.check(lib.ss_set_async(ctx.h, 1))
+    try:
+        a = [outs(1024) for _ in iqs]
+        for h, (o, bo) in zip(iqs, a):
+            ctx.check(call(h, bo))         # queued, returns before the work is done
+        ctx.check(lib.ss_wait(ctx.h))
+        for (o, _), e in zip(a, sync):
+            for k in ("raw", "sm", "ft", "nact", "nb"):
+                assert torch.equal(o[k], e[k]), k
+            for p in range(P):
+                n = int(e["nb"][p])
+                assert torch.equal(o["bins"][p, :n], e["bins"][p, :n])
+                assert torch.equal(o["boxes"][p, :n].view(torch.int64), e["boxes"][p, :n].view(torch.int64))
+        # a capacity below the true box count is reported at ss_wait
+        small, bs = outs(1)
+        ctx.check(call(iqs[0], bs))
+        assert lib.ss_wait(ctx.h) == NAT.SS_ECAPACITY
+        assert lib.ss_wait(ctx.h) == NAT.SS_OK          # the flags were consumed
+    finally:
+        lib.ss_set_async(ctx.h, 0)
