@@ -203,15 +203,36 @@ __device__ __forceinline__ int otsu_split_warp_u32(const uint32_t* hq, int lane)
         est[q] = e;
         m = fmax(m, e);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    // warp maximum of the estimates, exactly, by two 32-bit REDUX steps on the
+    // bit patterns (order-preserving for the non-negative doubles; the -1
+    // placeholders map to +0, and lane 0's bin 0 always holds an estimate >= 0)
+    {
+        const unsigned long long key = m > 0.0 ? static_cast<unsigned long long>(__double_as_longlong(m)) : 0ull;
+        const uint32_t khi = static_cast<uint32_t>(key >> 32);
+        const uint32_t mhi = __reduce_max_sync(0xffffffffu, khi);
+        const uint32_t mlo = __reduce_max_sync(0xffffffffu, khi == mhi ? static_cast<uint32_t>(key) : 0u);
+        m = __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(mhi) << 32) | mlo));
+    }
     const double floor_v = m - (m * 0x1p-30 + total * total * 0x1p-34);
+
+    // the reference's split is among the candidates (estimate >= floor_v);
+    // when there is exactly one -- nearly always -- it is the split, and the
+    // exact divides and the first-maximum reduction are not needed
+    uint32_t cand = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) cand |= (est[q] >= floor_v && est[q] >= 0.0) ? (1u << q) : 0u;
+    const uint32_t n_cand = __reduce_add_sync(0xffffffffu, static_cast<uint32_t>(__popc(cand)));
+    if (n_cand == 1u) {
+        const uint32_t holders = __ballot_sync(0xffffffffu, cand != 0u);
+        const int src = __ffs(static_cast<int>(holders)) - 1;
+        return __shfl_sync(0xffffffffu, lane * 8 + __ffs(static_cast<int>(cand)) - 1, src);
+    }
 
     double best_v = -1.0;
     int best_i = 0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-        if (est[q] >= floor_v && est[q] >= 0.0) {
+        if ((cand >> q) & 1u) {
             const uint32_t w0u = pcu + cnt[q];
             const double w0 = static_cast<double>(w0u);
             const double w1 = static_cast<double>(total_u - w0u);

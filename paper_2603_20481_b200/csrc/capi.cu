@@ -271,6 +271,7 @@ ss_status run_ccl(ss_ctx* ctx, const uint32_t* bits, int n_plots, int rows, int 
     L.labels = labels;
     ssb::CclWorkspace& w = L.ws;
     SS_WS(rr, int, "ccl.row_runs", static_cast<size_t>(n_plots) * rows);
+    SS_WS(so, int2, "ccl.seg_off", static_cast<size_t>(n_plots) * rows * ssb::kCclSeg);
     SS_WS(ro, int, "ccl.row_off", static_cast<size_t>(n_plots) * (rows + 1));
     SS_WS(pb, long long, "ccl.plot_base", n_plots);
     SS_WS(pok, int, "ccl.plot_ok", n_plots);
@@ -285,6 +286,7 @@ ss_status run_ccl(ss_ctx* ctx, const uint32_t* bits, int n_plots, int rows, int 
     SS_WS(mxt, int, "ccl.max_t", pool_cap);
     SS_WS(dn, int, "ccl.dense", pool_cap);
     w.row_runs = rr;
+    w.seg_off = so;
     w.row_off = ro;
     w.plot_base = pb;
     w.plot_ok = pok;
@@ -300,7 +302,8 @@ ss_status run_ccl(ss_ctx* ctx, const uint32_t* bits, int n_plots, int rows, int 
     w.dense = dn;
     w.pool_cap = pool_cap;
     SS_CK(ctx, ssb::ccl_launch(L, ctx->stream));
-    ctx->launches += 7 + (rows > 1 ? 1 : 0) + (rows > 16 ? 1 : 0) + (labels ? 1 : 0);
+    // count, scan, plot_base, emit, union_block, [union_boundary], flatten, compact, [labels]
+    ctx->launches += 7 + (rows > 16 ? 1 : 0) + (labels ? 1 : 0);
     if (overflow_host) SS_CK(ctx, cudaMemcpyAsync(overflow_host, of, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     if (overflow_acc) {
         note_overflow_kernel<<<1, 1, 0, ctx->stream>>>(of, overflow_acc);

@@ -34,7 +34,7 @@ namespace ssb {
 // runs are counted per segment; a run's index is the number of starts before
 // its start bit in the row, its end the number of ends before its end bit,
 // so segments emit independently once their prefix counts are known.
-constexpr int kSeg = 4;
+constexpr int kSeg = kCclSeg;
 
 struct SegRange {
     int w0, w1;
@@ -50,30 +50,52 @@ __device__ __forceinline__ uint32_t seg_carry(const uint32_t* col, int rows, int
     return w0 > 0 ? (col[static_cast<long long>(w0 - 1) * rows] >> 31) : 0u;
 }
 
+// Also records each segment's exclusive start / end offsets within its row
+// (seg_off[p][r][k] = {starts, ends} before segment k), so emit_runs walks
+// the mask once.
 __global__ void __launch_bounds__(32 * kSeg) count_runs_kernel(const uint32_t* __restrict__ bits, int rows, int W,
-                                                               int* row_runs) {
-    __shared__ int cnt_s[kSeg][32];
+                                                               int* row_runs, int2* seg_off) {
+    __shared__ int st_s[kSeg][32], en_s[kSeg][32];
     const int p = blockIdx.y;
     const int lane = threadIdx.x & 31, k = threadIdx.x >> 5;
     const int r = blockIdx.x * 32 + lane;
-    int cnt = 0;
+    int ns = 0, ne = 0;
     if (r < rows) {
         const uint32_t* col = bits + static_cast<long long>(p) * W * rows + r;
         const SegRange g = seg_range(W, k);
         uint32_t carry = seg_carry(col, rows, g.w0);
-        for (int w = g.w0; w < g.w1; ++w) {
-            const uint32_t x = col[static_cast<long long>(w) * rows];
-            cnt += __popc(x & ~((x << 1) | carry));
+        int w = g.w0;
+        for (; w + 8 <= g.w1; w += 8) {  // eight word loads in flight
+            uint32_t xs[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) xs[q] = __ldg(col + static_cast<long long>(w + q) * rows);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t sh = (xs[q] << 1) | carry;
+                ns += __popc(xs[q] & ~sh);
+                ne += __popc(~xs[q] & sh);
+                carry = xs[q] >> 31;
+            }
+        }
+        for (; w < g.w1; ++w) {
+            const uint32_t x = __ldg(col + static_cast<long long>(w) * rows);
+            const uint32_t sh = (x << 1) | carry;
+            ns += __popc(x & ~sh);
+            ne += __popc(~x & sh);
             carry = x >> 31;
         }
     }
-    cnt_s[k][lane] = cnt;
+    st_s[k][lane] = ns;
+    en_s[k][lane] = ne;
     __syncthreads();
-    if (k == 0 && r < rows) {
-        int t = 0;
-#pragma unroll
-        for (int q = 0; q < kSeg; ++q) t += cnt_s[q][lane];
-        row_runs[static_cast<long long>(p) * rows + r] = t;
+    if (r < rows) {
+        int s0 = 0, e0 = 0;
+        for (int q = 0; q < k; ++q) {
+            s0 += st_s[q][lane];
+            e0 += en_s[q][lane];
+        }
+        seg_off[(static_cast<long long>(p) * rows + r) * kSeg + k] = make_int2(s0, e0);
+        if (k == kSeg - 1) row_runs[static_cast<long long>(p) * rows + r] = s0 + ns;
     }
 }
 
@@ -163,41 +185,21 @@ __global__ void __launch_bounds__(1024) plot_base_kernel(const int* row_off, int
 // ~x & (x<<1|carry)), appended at the row's offset in the pool; segment k of
 // the row writes the starts / ends that fall in its words.
 __global__ void __launch_bounds__(32 * kSeg) emit_runs_kernel(const uint32_t* __restrict__ bits, int rows, int cols,
-                                                              const int* row_off, const long long* plot_base,
-                                                              const int* plot_ok, CclWorkspace ws) {
-    __shared__ int st_s[kSeg][32], en_s[kSeg][32];
+                                                              const int* row_off, const int2* __restrict__ seg_off,
+                                                              const long long* plot_base, const int* plot_ok,
+                                                              CclWorkspace ws) {
     const int W = (cols + 31) / 32;
     const int p = blockIdx.y;
     const int lane = threadIdx.x & 31, k = threadIdx.x >> 5;
     const int r = blockIdx.x * 32 + lane;
-    const bool live = r < rows && plot_ok[p];
+    if (r >= rows || !plot_ok[p]) return;
     const uint32_t* col = bits + static_cast<long long>(p) * W * rows + r;
     const SegRange g = seg_range(W, k);
-    int ns = 0, ne = 0;
-    if (live) {
-        uint32_t carry = seg_carry(col, rows, g.w0);
-        for (int w = g.w0; w < g.w1; ++w) {
-            const uint32_t x = col[static_cast<long long>(w) * rows];
-            const uint32_t sh = (x << 1) | carry;
-            ns += __popc(x & ~sh);
-            ne += __popc(~x & sh);
-            carry = x >> 31;
-        }
-    }
-    st_s[k][lane] = ns;
-    en_s[k][lane] = ne;
-    __syncthreads();
-    if (!live) return;
-    int s0 = 0, e0 = 0;
-    for (int q = 0; q < k; ++q) {
-        s0 += st_s[q][lane];
-        e0 += en_s[q][lane];
-    }
+    const int2 so = seg_off[(static_cast<long long>(p) * rows + r) * kSeg + k];
     const long long row0 = plot_base[p] + row_off[static_cast<long long>(p) * (rows + 1) + r];
-    long long si = row0 + s0, ei = row0 + e0;
+    long long si = row0 + so.x, ei = row0 + so.y;
     uint32_t carry = seg_carry(col, rows, g.w0);
-    for (int w = g.w0; w < g.w1; ++w) {
-        const uint32_t x = col[static_cast<long long>(w) * rows];
+    auto emit_word = [&](int w, uint32_t x) {
         const uint32_t sh = (x << 1) | carry;
         uint32_t starts = x & ~sh, ends = ~x & sh;
         carry = x >> 31;
@@ -207,11 +209,6 @@ __global__ void __launch_bounds__(32 * kSeg) emit_runs_kernel(const uint32_t* __
             ws.run_begin[si] = 32 * w + bpos;
             ws.run_row[si] = r;
             ws.parent[si] = static_cast<int>(si);
-            ws.area[si] = 0ull;
-            ws.min_f[si] = INT_MAX;
-            ws.max_f[si] = -1;
-            ws.max_t[si] = -1;
-            ws.dense[si] = -1;
             ++si;
         }
         while (ends) {
@@ -219,7 +216,16 @@ __global__ void __launch_bounds__(32 * kSeg) emit_runs_kernel(const uint32_t* __
             ends &= ends - 1;
             ws.run_end[ei++] = 32 * w + bpos;
         }
+    };
+    int w = g.w0;
+    for (; w + 8 <= g.w1; w += 8) {  // eight word loads in flight
+        uint32_t xs[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) xs[q] = __ldg(col + static_cast<long long>(w + q) * rows);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) emit_word(w + q, xs[q]);
     }
+    for (; w < g.w1; ++w) emit_word(w, __ldg(col + static_cast<long long>(w) * rows));
     if (k == kSeg - 1 || g.w1 == W) {
         // a run still open after the last word reaches the last column (cols % 32 == 0)
         if (g.w1 == W && g.w0 < g.w1 && carry) ws.run_end[ei] = cols;
@@ -309,15 +315,20 @@ __device__ __forceinline__ void sm_unite(int* par, int a, int b) {
 
 // Union within blocks of kUB rows: the block's runs (contiguous in the pool)
 // are united in shared memory, then every run's parent is set to its
-// block-local root.  Blocks whose runs exceed kUCap unite in global memory.
-// Rows r0 (a block's first row) are joined to the row above by
-// union_boundary_kernel afterwards.
+// block-local root and each block-local root gets its block-local component's
+// statistics (area, max row, min / max column; area = 0 marks the other runs),
+// so the global flatten walks and updates one entry per block-local
+// component instead of one per run.  Blocks whose runs exceed kUCap unite in
+// global memory and give every run its own statistics.  Rows r0 (a block's
+// first row) are joined to the row above by union_boundary_kernel afterwards.
+// Launched for every plot, one row included (rows == 1: each run alone).
 constexpr int kUB = 16;
-constexpr int kUCap = 2048;
+constexpr int kUCap = 1024;
 
 __global__ void __launch_bounds__(256) union_block_kernel(int rows, const int* row_off, const long long* plot_base,
                                                           const int* plot_ok, CclWorkspace ws) {
     __shared__ int sb[kUCap], se[kUCap], sp[kUCap];
+    __shared__ int s_area[kUCap], s_maxt[kUCap], s_minf[kUCap], s_maxf[kUCap];
     __shared__ int roff[kUB + 1];
     const int p = blockIdx.y;
     const int r0 = blockIdx.x * kUB, r1 = min(rows, r0 + kUB);
@@ -325,9 +336,18 @@ __global__ void __launch_bounds__(256) union_block_kernel(int rows, const int* r
     const int* off = row_off + static_cast<long long>(p) * (rows + 1);
     const long long base = plot_base[p];
     const int g0 = off[r0], n = off[r1] - g0;
+    const int lane = threadIdx.x & 31;
     if (n > kUCap) {  // dense block: rows r0+1 .. r1-1 in global memory, one warp per row
         for (int r = r0 + 1 + (threadIdx.x >> 5); r < r1; r += blockDim.x >> 5)
-            unite_row_global(r, off, base, ws, threadIdx.x & 31, 32);
+            unite_row_global(r, off, base, ws, lane, 32);
+        for (int r = r0 + (threadIdx.x >> 5); r < r1; r += blockDim.x >> 5)
+            for (long long i = base + off[r] + lane; i < base + off[r + 1]; i += 32) {
+                const int b = ws.run_begin[i], e = ws.run_end[i];
+                ws.area[i] = static_cast<unsigned long long>(e - b);
+                ws.max_t[i] = r;
+                ws.min_f[i] = b;
+                ws.max_f[i] = e - 1;
+            }
         return;
     }
     const long long gb = base + g0;
@@ -335,11 +355,14 @@ __global__ void __launch_bounds__(256) union_block_kernel(int rows, const int* r
         sb[i] = ws.run_begin[gb + i];
         se[i] = ws.run_end[gb + i];
         sp[i] = i;
+        s_area[i] = 0;
+        s_maxt[i] = -1;
+        s_minf[i] = INT_MAX;
+        s_maxf[i] = -1;
     }
     for (int j = threadIdx.x; j <= r1 - r0; j += blockDim.x) roff[j] = off[r0 + j] - g0;
     __syncthreads();
     // one warp per row pair (j-1, j), lanes over row j's runs
-    const int lane = threadIdx.x & 31;
     for (int j = 1 + (threadIdx.x >> 5); j < r1 - r0; j += blockDim.x >> 5) {
         const int pb = roff[j - 1], cb = roff[j], ce = roff[j + 1];
         for (int i = cb + lane; i < ce; i += 32) {
@@ -354,10 +377,27 @@ __global__ void __launch_bounds__(256) union_block_kernel(int rows, const int* r
         }
     }
     __syncthreads();
+    // parents and block-local statistics; one warp per row (the row is the run's)
+    for (int j = threadIdx.x >> 5; j < r1 - r0; j += blockDim.x >> 5) {
+        for (int i = roff[j] + lane; i < roff[j + 1]; i += 32) {
+            int x = i;
+            while (sp[x] != x) x = sp[x];
+            ws.parent[gb + i] = static_cast<int>(gb + x);
+            atomicAdd(&s_area[x], se[i] - sb[i]);
+            atomicMax(&s_maxt[x], r0 + j);
+            atomicMin(&s_minf[x], sb[i]);
+            atomicMax(&s_maxf[x], se[i] - 1);
+        }
+    }
+    __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        int x = i;
-        while (sp[x] != x) x = sp[x];
-        ws.parent[gb + i] = static_cast<int>(gb + x);
+        const int a = s_area[i];  // > 0 exactly for the block-local roots
+        ws.area[gb + i] = static_cast<unsigned long long>(a);
+        if (a > 0) {
+            ws.max_t[gb + i] = s_maxt[i];
+            ws.min_f[gb + i] = s_minf[i];
+            ws.max_f[gb + i] = s_maxf[i];
+        }
     }
 }
 
@@ -371,6 +411,9 @@ __global__ void union_boundary_kernel(int rows, const int* row_off, const long l
     unite_row_global(r, off, plot_base[p], ws, threadIdx.x & 31, 32);
 }
 
+// Entries with statistics (area > 0: block-local roots, or every run of a
+// dense block) hook onto their global root and add their statistics to it.
+// Only those entries change; a run's component is its block-local root's.
 __global__ void flatten_kernel(int rows, const int* row_off, const long long* plot_base, const int* plot_ok,
                                CclWorkspace ws) {
     const int p = blockIdx.y;
@@ -380,13 +423,15 @@ __global__ void flatten_kernel(int rows, const int* row_off, const long long* pl
     for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < n;
          k += static_cast<long long>(gridDim.x) * blockDim.x) {
         const long long i = base + k;
+        const unsigned long long a = ws.area[i];
+        if (a == 0ull) continue;
         const int root = uf_root(ws.parent, static_cast<int>(i));
+        if (root == static_cast<int>(i)) continue;
         ws.parent[i] = root;
-        const int b = ws.run_begin[i], e = ws.run_end[i];
-        atomicAdd(ws.area + root, static_cast<unsigned long long>(e - b));
-        atomicMax(ws.max_t + root, ws.run_row[i]);
-        atomicMin(ws.min_f + root, b);
-        atomicMax(ws.max_f + root, e - 1);
+        atomicAdd(ws.area + root, a);
+        atomicMax(ws.max_t + root, ws.max_t[i]);
+        atomicMin(ws.min_f + root, ws.min_f[i]);
+        atomicMax(ws.max_f + root, ws.max_f[i]);
     }
 }
 
@@ -426,8 +471,8 @@ __global__ void compact_kernel(int rows, int cols, const int* row_off, const lon
         __syncthreads();
         const int carry = carry_s;
         const int id = carry + (w > 0 ? red[w - 1] : 0) + inc - flag;
+        if (k < n && ws.parent[i] == static_cast<int>(i)) ws.dense[i] = flag ? id : -1;  // read per root only
         if (flag) {
-            ws.dense[i] = id;
             if (id < L.cap) {
                 const long long o = static_cast<long long>(p) * L.cap + id;
                 const int min_t = ws.run_row[i], max_t = ws.max_t[i];
@@ -467,7 +512,7 @@ __global__ void labels_kernel(int rows, int cols, const int* row_off, CclWorkspa
     const long long n = row_off[rows];
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int id = ws.dense[ws.parent[i]];
+        const int id = ws.dense[uf_root(ws.parent, static_cast<int>(i))];
         if (id < 0) continue;
         int32_t* row = labels + static_cast<long long>(ws.run_row[i]) * cols;
         for (int c = ws.run_begin[i]; c < ws.run_end[i]; ++c) row[c] = id + 1;
@@ -479,12 +524,13 @@ cudaError_t ccl_launch(const CclLaunch& L, cudaStream_t st) {
     const int W = (L.cols + 31) / 32;
     const CclWorkspace& ws = L.ws;
     dim3 tgrid((L.rows + 31) / 32, L.n_plots);
-    count_runs_kernel<<<tgrid, 32 * kSeg, 0, st>>>(L.bits, L.rows, W, ws.row_runs);
+    count_runs_kernel<<<tgrid, 32 * kSeg, 0, st>>>(L.bits, L.rows, W, ws.row_runs, ws.seg_off);
     scan_rows_kernel<<<L.n_plots, 1024, 0, st>>>(ws.row_runs, L.rows, ws.row_off);
     plot_base_kernel<<<1, 1024, 0, st>>>(ws.row_off, L.n_plots, L.rows, ws.pool_cap, ws.plot_base, ws.plot_ok,
                                          ws.overflow);
-    emit_runs_kernel<<<tgrid, 32 * kSeg, 0, st>>>(L.bits, L.rows, L.cols, ws.row_off, ws.plot_base, ws.plot_ok, ws);
-    if (L.rows > 1) {
+    emit_runs_kernel<<<tgrid, 32 * kSeg, 0, st>>>(L.bits, L.rows, L.cols, ws.row_off, ws.seg_off, ws.plot_base,
+                                                  ws.plot_ok, ws);
+    {
         const int nblk = (L.rows + kUB - 1) / kUB;
         union_block_kernel<<<dim3(nblk, L.n_plots), 256, 0, st>>>(L.rows, ws.row_off, ws.plot_base, ws.plot_ok, ws);
         if (nblk > 1) {

@@ -107,8 +107,10 @@ cudaError_t morph_u8_launch(const uint8_t* src, int rows, int cols, int op, int 
                             int c0, int c1, uint8_t* tmp, uint8_t* dst, cudaStream_t st);
 
 // ---- K6 ccl.cu
+constexpr int kCclSeg = 4;  // word segments per row in the run kernels (ccl.cu)
 struct CclWorkspace {
     int* row_runs = nullptr;      // n_plots x rows: runs starting in each row
+    int2* seg_off = nullptr;      // n_plots x rows x kCclSeg: {starts, ends} before each row segment
     int* row_off = nullptr;       // n_plots x (rows + 1): exclusive prefix within the plot
     long long* plot_base = nullptr;  // n_plots: first pool index of the plot's runs
     int* plot_ok = nullptr;       // n_plots: 1 if the plot's runs fit the pool

@@ -26,6 +26,9 @@ class CyclingSource final : public frontend::ChunkSource {
         const std::size_t n = s_.size() / static_cast<std::size_t>(f_);
         const std::size_t at = static_cast<std::size_t>(seq_ % n) * static_cast<std::size_t>(f_);
         if (pace_) {
+            // the stream starts when the engine first asks for a chunk (engine
+            // set-up time is not part of the paced stream)
+            if (seq_ == 0) t0_ = std::chrono::steady_clock::now();
             const auto due = t0_ + std::chrono::duration<double>(static_cast<double>(seq_ + 1) * f_ / fs_);
             std::this_thread::sleep_until(due);
         }
