@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kBinThreads) binarize_kernel(BinarizeLaunch a)
             for (int r = warp; r < rows; r += kBinWarps)
                 if (col_out) a.mask_u8[static_cast<long long>(r) * a.cols + col] = 0;
         } else if (a.mask_bits) {
-            uint32_t* mb = a.mask_bits + (static_cast<long long>(p) * W + wd) * rows;  // word-major
+            uint32_t* mb = a.mask_bits + (static_cast<long long>(p) * W + wd) * mask_rs(rows);  // word-major
             for (int r = threadIdx.x; r < rows; r += kBinThreads) mb[r] = 0;
         }
         if (a.col_thr && threadIdx.x < 32 && in_image)
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kBinThreads) binarize_kernel(BinarizeLaunch a)
             a.mask_u8[static_cast<long long>(r) * a.cols + col] = x > thr ? 1 : 0;
         }
     } else {
-        uint32_t* mb = a.mask_bits + (static_cast<long long>(p) * W + wd) * rows;  // word-major
+        uint32_t* mb = a.mask_bits + (static_cast<long long>(p) * W + wd) * mask_rs(rows);  // word-major
         int r = warp;
         for (; r + 3 * kBinWarps < rows; r += 4 * kBinWarps) {
             float x[4];
@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     const uint32_t abyte = (a.active_bits[static_cast<long long>(p) * W + grp / 4] >> (8 * (grp & 3))) & 0xffu;
     // byte (grp & 3) of the word-major mask words (grp >> 2, r): the tile path
     // writes the packed mask K5 reads, 4 bytes apart per row
-    uint8_t* plane = a.mask_bytes + ((static_cast<long long>(p) * W + (grp >> 2)) * rows_all + rbase) * 4 + (grp & 3);
+    uint8_t* plane = a.mask_bytes + ((static_cast<long long>(p) * W + (grp >> 2)) * mask_rs(rows_all) + rbase) * 4 + (grp & 3);
     const int col0 = grp * kTileCols;
     if (abyte == 0) {  // both CTAs of a cluster see the same byte and leave together
         if (!a.skip_empty)

@@ -340,8 +340,8 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
     SS_WS(act, int, "det.active", static_cast<size_t>(n_plots) * cols);
     SS_WS(nact, int, "det.n_active", n_plots);
     SS_WS(abits, uint32_t, "det.active_bits", static_cast<size_t>(n_plots) * W);
-    SS_WS(m0, uint32_t, "det.mask0", static_cast<size_t>(n_plots) * rows * W);
-    SS_WS(m1, uint32_t, "det.mask1", static_cast<size_t>(n_plots) * rows * W);
+    SS_WS(m0, uint32_t, "det.mask0", static_cast<size_t>(n_plots) * ssb::mask_rs(rows) * W);
+    SS_WS(m1, uint32_t, "det.mask1", static_cast<size_t>(n_plots) * ssb::mask_rs(rows) * W);
     ssb::FloorLaunch F;
     F.raw = psd;
     F.n_plots = n_plots;
@@ -421,7 +421,7 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
         // alone with its exact worst-case pool
         int* nb = out_dev.n_boxes ? out_dev.n_boxes : ncomp;
         for (int p = 0; p < n_plots; ++p) {
-            const size_t mo = static_cast<size_t>(p) * rows * W;
+            const size_t mo = static_cast<size_t>(p) * ssb::mask_rs(rows) * W;
             s = run_ccl(ctx, m1 + mo, 1, rows, cols, cfg.min_component_area, worst_pool(rows, cols), nb + p, cap,
                         nullptr, out_dev.bin_boxes ? reinterpret_cast<int*>(out_dev.bin_boxes) + 4 * cap * p : nullptr,
                         out_dev.boxes ? reinterpret_cast<double*>(out_dev.boxes) + 4 * cap * p : nullptr,
@@ -780,8 +780,8 @@ ss_status ss_consolidate(ss_ctx* ctx, const uint8_t* src, int rows, int cols, in
     if (!ctx) return SS_EVALIDATION;
     if (rows < 1 || cols < 1) return fail(ctx, SS_EVALIDATION, "empty mask");
     const int W = (cols + 31) / 32;
-    SS_WS(a, uint32_t, "cons.a", static_cast<size_t>(rows) * W);
-    SS_WS(b, uint32_t, "cons.b", static_cast<size_t>(rows) * W);
+    SS_WS(a, uint32_t, "cons.a", static_cast<size_t>(ssb::mask_rs(rows)) * W);
+    SS_WS(b, uint32_t, "cons.b", static_cast<size_t>(ssb::mask_rs(rows)) * W);
     SS_CK(ctx, ssb::pack_u8_launch(src, 1, rows, cols, a, ctx->stream));
     SS_CK(ctx, ssb::consolidate_bits_launch(a, 1, rows, cols, along_time != 0, b, ctx->stream));
     SS_CK(ctx, ssb::unpack_launch(b, 1, rows, cols, dst, ctx->stream));
@@ -798,7 +798,7 @@ ss_status ss_components(ss_ctx* ctx, const uint8_t* mask, int rows, int cols, in
         return SS_OK;
     }
     const int W = (cols + 31) / 32;
-    SS_WS(bits, uint32_t, "comp.bits", static_cast<size_t>(rows) * W);
+    SS_WS(bits, uint32_t, "comp.bits", static_cast<size_t>(ssb::mask_rs(rows)) * W);
     SS_WS(ncomp, int, "comp.n", 1);
     const long long dcap = cap > 0 ? cap : 1;
     SS_WS(ext, long long, "comp.ext", static_cast<size_t>(5 * dcap));

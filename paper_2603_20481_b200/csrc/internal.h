@@ -71,6 +71,11 @@ bool savgol_weights_host(int window, int order, std::vector<double>& w);
 bool host_has_fma_avx2();
 
 // ---- K4 binarize.cu
+// Word-major bit masks [p][w][rs] keep each word's rows at a stride padded to
+// a multiple of 4 (16 bytes): row bands of 4-aligned rows load and store as
+// 128-bit vectors (K5).  Rows rows .. rs-1 are padding, never read as data.
+__host__ __device__ inline int mask_rs(int rows) { return (rows + 3) & ~3; }
+
 struct BinarizeLaunch {
     const float* tf = nullptr;          // n_plots x rows x cols
     int n_plots = 0;

@@ -24,14 +24,14 @@ __global__ void pack_u8_kernel(const uint8_t* __restrict__ m, int rows, int cols
     const long long warp_global = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
     const long long nwarps = (static_cast<long long>(gridDim.x) * blockDim.x) >> 5;
     const uint8_t* mp = m + static_cast<long long>(p) * rows * cols;
-    uint32_t* bp = bits + static_cast<long long>(p) * nwords;
+    uint32_t* bp = bits + static_cast<long long>(p) * mask_rs(rows) * W;
     for (long long wi = warp_global; wi < nwords; wi += nwarps) {
         const long long r = wi / W;
         const int w = static_cast<int>(wi % W);
         const int c = w * 32 + lane;
         const bool b = c < cols && mp[r * cols + c] != 0;
         const uint32_t word = __ballot_sync(0xffffffffu, b);
-        if (lane == 0) bp[static_cast<long long>(w) * rows + r] = word;
+        if (lane == 0) bp[static_cast<long long>(w) * mask_rs(rows) + r] = word;
     }
 }
 
@@ -46,13 +46,13 @@ __global__ void unpack_kernel(const uint32_t* __restrict__ bits, int rows, int c
     const int W = (cols + 31) / 32;
     const int p = blockIdx.y;
     const long long npx = static_cast<long long>(rows) * cols;
-    const uint32_t* bp = bits + static_cast<long long>(p) * rows * W;
+    const uint32_t* bp = bits + static_cast<long long>(p) * mask_rs(rows) * W;
     uint8_t* mp = m + static_cast<long long>(p) * npx;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < npx;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         const long long r = i / cols;
         const int c = static_cast<int>(i % cols);
-        mp[i] = (bp[static_cast<long long>(c >> 5) * rows + r] >> (c & 31)) & 1u;
+        mp[i] = (bp[static_cast<long long>(c >> 5) * mask_rs(rows) + r] >> (c & 31)) & 1u;
     }
 }
 
@@ -106,8 +106,10 @@ struct RegBand {
             const uint32_t v = x[i];
             const uint32_t prev = __shfl_up_sync(0xffffffffu, v, 1);    // word w-1 (lane 0: its own, halo)
             const uint32_t next = __shfl_down_sync(0xffffffffu, v, 1);  // word w+1 (lane 31: its own, halo)
-            const uint32_t left = __funnelshift_l(prev, v, 1);          // (v << 1) | (prev >> 31)
-            const uint32_t right = __funnelshift_r(v, next, 1);         // (v >> 1) | (next << 31)
+            // funnel shifts written as shifts: the __funnelshift intrinsics are
+            // volatile asm, which pins their order against the shuffles
+            const uint32_t left = (v << 1) | (prev >> 31);
+            const uint32_t right = (v >> 1) | (next << 31);
             x[i] = erode ? (v & left & right) : (v | left | right);
         }
     }
@@ -118,8 +120,8 @@ struct RegBand {
             const uint32_t v = x[i];
             const uint32_t prev = __shfl_up_sync(0xffffffffu, v, 1);
             const uint32_t next = __shfl_down_sync(0xffffffffu, v, 1);
-            x[i] = v & __funnelshift_l(prev, v, 1) & __funnelshift_l(prev, v, 2) & __funnelshift_r(v, next, 1) &
-                   __funnelshift_r(v, next, 2);
+            x[i] = v & ((v << 1) | (prev >> 31)) & ((v << 2) | (prev >> 30)) & ((v >> 1) | (next << 31)) &
+                   ((v >> 2) | (next << 30));
         }
     }
     // one erosion / dilation: 3x3 (vert then horiz), 3x1 (vert), 1x3 (horiz);
@@ -153,7 +155,7 @@ struct RegBand {
 
 // in/out: word-major bits [p][W][rows].  One warp per (row band, word band).
 template <int HALO>
-__global__ void __launch_bounds__(128) consolidate_kernel(const uint32_t* __restrict__ in, int rows, int cols,
+__global__ void __launch_bounds__(128, 7) consolidate_kernel(const uint32_t* __restrict__ in, int rows, int cols,
                                                           int wbands, long long bands, bool along_time,
                                                           uint32_t* __restrict__ out,
                                                           const uint32_t* __restrict__ active_bits) {
@@ -178,19 +180,42 @@ __global__ void __launch_bounds__(128) consolidate_kernel(const uint32_t* __rest
         keep = ((ab & 0xffu) ? 0xffu : 0u) | ((ab & 0xff00u) ? 0xff00u : 0u) | ((ab & 0xff0000u) ? 0xff0000u : 0u) |
                ((ab & 0xff000000u) ? 0xff000000u : 0u);
     }
-    const uint32_t* src = in + (static_cast<long long>(p) * W + (wvalid ? gw : 0)) * rows + row0;
+    const int rs = mask_rs(rows);
+    const uint32_t* src = in + (static_cast<long long>(p) * W + (wvalid ? gw : 0)) * rs + row0;
+    if (HALO % 4 == 0 && row0 >= 0 && row0 + kRegNR <= rs) {
+        // 16-byte aligned (row0 and rs are multiples of 4): 128-bit loads;
+        // rows past the image (padding) are cleared below
 #pragma unroll
-    for (int i = 0; i < kRegNR; ++i) t.x[i] = (wvalid && i >= t.lo && i < t.hi) ? (__ldg(src + i) & keep) : 0u;
+        for (int i = 0; i < kRegNR; i += 4) {
+            const uint4 q = wvalid ? __ldg(reinterpret_cast<const uint4*>(src + i)) : make_uint4(0u, 0u, 0u, 0u);
+            t.x[i] = q.x;
+            t.x[i + 1] = q.y;
+            t.x[i + 2] = q.z;
+            t.x[i + 3] = q.w;
+        }
+#pragma unroll
+        for (int i = 0; i < kRegNR; ++i) t.x[i] = (i < t.hi) ? (t.x[i] & keep) : 0u;
+    } else {
+#pragma unroll
+        for (int i = 0; i < kRegNR; ++i) t.x[i] = (wvalid && i >= t.lo && i < t.hi) ? (__ldg(src + i) & keep) : 0u;
+    }
     // interior bands (most of a plot) skip the out-of-image clipping entirely
     const bool interior = t.lo == 0 && t.hi == kRegNR && t.wmask == 0xffffffffu;
     if (__all_sync(0xffffffffu, interior)) t.template chain<false>(along_time);
     else t.template chain<true>(along_time);
     if (!wvalid || lane == 0 || lane == 31) return;
-    uint32_t* dst = out + (static_cast<long long>(p) * W + gw) * rows + r0;
-    const int nrow = min(RB::OWN, rows - r0);
+    uint32_t* dst = out + (static_cast<long long>(p) * W + gw) * rs + r0;
+    if (r0 + RB::OWN <= rs) {  // r0 is a multiple of 16: 128-bit stores (padding rows may take garbage)
 #pragma unroll
-    for (int i = 0; i < RB::OWN; ++i)
-        if (i < nrow) dst[i] = t.x[HALO + i];
+        for (int i = 0; i < RB::OWN; i += 4)
+            *reinterpret_cast<uint4*>(dst + i) = make_uint4(t.x[HALO + i], t.x[HALO + i + 1], t.x[HALO + i + 2],
+                                                            t.x[HALO + i + 3]);
+    } else {
+        const int nrow = min(RB::OWN, rows - r0);
+#pragma unroll
+        for (int i = 0; i < RB::OWN; ++i)
+            if (i < nrow) dst[i] = t.x[HALO + i];
+    }
 }
 
 cudaError_t consolidate_bits_launch(const uint32_t* in, int n_plots, int rows, int cols, bool along_time,
