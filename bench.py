@@ -54,6 +54,10 @@ class Workload:
         # K1 algorithmic bytes per plot: read its new IQ once + write the TF plot
         self.alg_bytes = self.stride * self.sb + self.rows * N_FFT * 4
         self.alg_flop64 = self.rows * 5 * N_FFT * 12                   # conventional 5 N log2 N per row
+        # FP64 warp-instructions K1 executes per row and warp (ncu source view of
+        # fft_mag_kernel<12,0,1,0>): the SSFFT-2 work itself,
+        # counted for the default (rect, fp32) kernel only
+        self.k1_fp64_instr = 824 if (name == "c5r" and window == 0) else None
 
     def samples(self, plots):
         return plots * self.stride + self.tail
@@ -515,12 +519,28 @@ def measure(args, wl, B, D, steps, warmup, e2e_batch, with_gather=True):
                         "fp64_peak_tflops": FP64_PEAK_TFLOPS,
                         "fp64_frac": B * wl.alg_flop64 / (k1_ms / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
                         "pipeline": pipeline,
+                        "fp64_executed": _fp64_executed(wl, k1_ms / B),
                         "note": "K1 is bounded by FP64 pipe + issue slots as much as by HBM (DESIGN.md §4): "
                                 "both fractions are given, against measured peaks; `pipeline` = the same "
                                 "algorithmic bytes over the whole step"}}
     del iq, tf, outs
     torch.cuda.empty_cache()
     return res
+
+
+def _fp64_executed(wl, k1_ms_per_capture):
+    """K1 against the FP64 pipe executing the instructions it actually issues:
+    rows x N/16 threads x the per-thread FP64 instruction count, at the measured
+    DFMA lane rate (FP64_PEAK_TFLOPS / 2 flops).  `frac` = that floor over the
+    measured K1 time; `hbm_frac_cap` = the HBM fraction K1 would reach at it."""
+    if wl.k1_fp64_instr is None:
+        return None
+    lane_ops = wl.rows * (N_FFT // 16) * wl.k1_fp64_instr
+    floor_us = lane_ops / (FP64_PEAK_TFLOPS * 1e12 / 2) * 1e6
+    meas_us = k1_ms_per_capture * 1e3
+    hbm_us = wl.alg_bytes / (_peaks()[0] * 1e9) * 1e6
+    return {"warp_instr_per_row_warp": wl.k1_fp64_instr, "floor_us_per_capture": floor_us,
+            "measured_us_per_capture": meas_us, "frac": floor_us / meas_us, "hbm_frac_cap": hbm_us / floor_us}
 
 
 def quality_at(wl, caps, rows, K=4096):

@@ -326,8 +326,9 @@ __device__ __forceinline__ void sm_unite(int* par, int a, int b) {
 // Launched for every plot, one row included (rows == 1: each run alone).
 constexpr int kUB = 16;  // 16 beat 32 (0.78 ms per C5r step) and 64 (1.02)
 constexpr int kUCap = 1024;
+constexpr int kUThreads = 256;  // 256 beat 128 (0.72 ms per C5r step), 64 (0.96), 32 (1.27)
 
-__global__ void __launch_bounds__(256) union_block_kernel(int rows, const int* row_off, const long long* plot_base,
+__global__ void __launch_bounds__(kUThreads) union_block_kernel(int rows, const int* row_off, const long long* plot_base,
                                                           const int* plot_ok, CclWorkspace ws) {
     __shared__ int sb[kUCap], se[kUCap], sp[kUCap];
     __shared__ int s_area[kUCap], s_maxt[kUCap], s_minf[kUCap], s_maxf[kUCap];
@@ -534,7 +535,7 @@ cudaError_t ccl_launch(const CclLaunch& L, cudaStream_t st) {
                                                   ws.plot_ok, ws);
     {
         const int nblk = (L.rows + kUB - 1) / kUB;
-        union_block_kernel<<<dim3(nblk, L.n_plots), 256, 0, st>>>(L.rows, ws.row_off, ws.plot_base, ws.plot_ok, ws);
+        union_block_kernel<<<dim3(nblk, L.n_plots), kUThreads, 0, st>>>(L.rows, ws.row_off, ws.plot_base, ws.plot_ok, ws);
         if (nblk > 1) {
             dim3 bgrid((nblk - 1 + 7) / 8, L.n_plots);
             union_boundary_kernel<<<bgrid, 256, 0, st>>>(L.rows, ws.row_off, ws.plot_base, ws.plot_ok, ws);
