@@ -503,78 +503,9 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
             tma_load_box(bt_vals + b * kBox * kTileCols, &tmap, col0, rbase + b * kBox, p, &box_bar[b]);
         }
     }
-    for (int i = tid; i < kTileCols * kHistStride; i += kBinThreads) hist[i] = 0;
-    __syncthreads();  // mbarrier init visible
-
-    // ---- sweep A: two threads per row, one float4 (4 columns) each; fminf /
-    // fmaxf equal std::min / std::max here (NaN is never taken by either, and
-    // the sign of a zero extreme never reaches an output)
-    {
-        const int hh = tid & 1;
-        float lo4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
-        float hi4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-        // exactly two rows of each box per thread, branch-free: rows past the
-        // CTA's last row re-read that row (a repeated value changes no extreme)
-        static_assert(kBox == 2 * (kBinThreads / 2), "two rows of a box per thread");
-        const int last = rows - 1;
-        for (int b = 0; b < nbox; ++b) {
-            mbar_wait(&box_bar[b], 0);
-            const int r0 = min(b * kBox + (tid >> 1), last);
-            const int r1 = min(b * kBox + kBinThreads / 2 + (tid >> 1), last);
-            const float4 x = *reinterpret_cast<const float4*>(bt_vals + r0 * kTileCols + 4 * hh);
-            const float4 y = *reinterpret_cast<const float4*>(bt_vals + r1 * kTileCols + 4 * hh);
-            lo4[0] = fminf(lo4[0], fminf(x.x, y.x)); hi4[0] = fmaxf(hi4[0], fmaxf(x.x, y.x));
-            lo4[1] = fminf(lo4[1], fminf(x.y, y.y)); hi4[1] = fmaxf(hi4[1], fmaxf(x.y, y.y));
-            lo4[2] = fminf(lo4[2], fminf(x.z, y.z)); hi4[2] = fmaxf(hi4[2], fmaxf(x.z, y.z));
-            lo4[3] = fminf(lo4[3], fminf(x.w, y.w)); hi4[3] = fmaxf(hi4[3], fmaxf(x.w, y.w));
-        }
-#pragma unroll
-        for (int o = 2; o < 32; o <<= 1)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                lo4[q] = fminf(lo4[q], __shfl_xor_sync(0xffffffffu, lo4[q], o));
-                hi4[q] = fmaxf(hi4[q], __shfl_xor_sync(0xffffffffu, hi4[q], o));
-            }
-        if (lane < 2) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                s_lo[warp][4 * lane + q] = lo4[q];
-                s_hi[warp][4 * lane + q] = hi4[q];
-            }
-        }
-    }
-    __syncthreads();
-    if constexpr (NSPLIT > 1) {
-        if (tid < kTileCols) {
-            float l = s_lo[0][tid], h = s_hi[0][tid];
-            for (int q = 1; q < kBinWarps; ++q) {
-                l = fminf(l, s_lo[q][tid]);
-                h = fmaxf(h, s_hi[q][tid]);
-            }
-            part_lo[tid] = l;
-            part_hi[tid] = h;
-            // push into the partner too (peer slot): after the barrier both
-            // read only local shared memory
-            cg::cluster_group cl = cg::this_cluster();
-            *cl.map_shared_rank(&peer_lo[tid], rank ^ 1) = l;
-            *cl.map_shared_rank(&peer_hi[tid], rank ^ 1) = h;
-        }
-        cg::this_cluster().sync();
-    }
-    if (tid < kTileCols) {
-        float l, h;
-        if constexpr (NSPLIT > 1) {
-            // min / max are order-free: every CTA of the cluster derives the same extremes
-            l = fminf(part_lo[tid], peer_lo[tid]);
-            h = fmaxf(part_hi[tid], peer_hi[tid]);
-        } else {
-            l = s_lo[0][tid];
-            h = s_hi[0][tid];
-            for (int q = 1; q < kBinWarps; ++q) {
-                l = fminf(l, s_lo[q][tid]);
-                h = fmaxf(h, s_hi[q][tid]);
-            }
-        }
+    // per-column binning constants from the column extremes (bin_of,
+    // detector.cpp:28-39); thread tid < 8 owns column col0 + tid
+    auto set_col = [&](float l, float h) {
         const float scale = __fdiv_rn(256.0f, __fsub_rn(h, l));
         const bool valid = h > l && isfinite(scale);
         const bool act = (col0 + tid < cols) && ((abyte >> tid) & 1u);
@@ -583,16 +514,132 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
         c_span[tid] = __dsub_rn(static_cast<double>(h), static_cast<double>(l));
         c_use[tid] = (act && valid) ? 1 : 0;
         c_thr[tid] = INFINITY;
+    };
+    // extremes supplied by the fused K1 (exact: order-free min / max of the
+    // same floats): no min / max sweep, and each box is binned as it lands
+    const bool ext = a.col_lo != nullptr;
+    for (int i = tid; i < kTileCols * kHistStride; i += kBinThreads) hist[i] = 0;
+    if (ext && tid < kTileCols) {
+        const long long ci = static_cast<long long>(p) * cols + col0 + tid;
+        set_col(a.col_lo[ci], a.col_hi[ci]);
     }
-    __syncthreads();
+    __syncthreads();  // mbarrier init (+ the constants) visible
 
-    // ---- sweep B: histograms from shared memory.  Two threads per row, one
-    // float4 (4 columns) each, as in sweep A: one LDS.128 per 4 values and
-    // the per-column constants in registers.  Branch-free: a column that is
-    // not binarised (inactive or constant) still counts into its own
-    // histogram (bin_index stays in [0, 255] for any input), which Otsu then
-    // ignores
-    {
+    if (!ext) {
+        // ---- sweep A: two threads per row, one float4 (4 columns) each; fminf /
+        // fmaxf equal std::min / std::max here (NaN is never taken by either, and
+        // the sign of a zero extreme never reaches an output)
+        {
+            const int hh = tid & 1;
+            float lo4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+            float hi4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+            // exactly two rows of each box per thread, branch-free: rows past the
+            // CTA's last row re-read that row (a repeated value changes no extreme)
+            static_assert(kBox == 2 * (kBinThreads / 2), "two rows of a box per thread");
+            const int last = rows - 1;
+            for (int b = 0; b < nbox; ++b) {
+                mbar_wait(&box_bar[b], 0);
+                const int r0 = min(b * kBox + (tid >> 1), last);
+                const int r1 = min(b * kBox + kBinThreads / 2 + (tid >> 1), last);
+                const float4 x = *reinterpret_cast<const float4*>(bt_vals + r0 * kTileCols + 4 * hh);
+                const float4 y = *reinterpret_cast<const float4*>(bt_vals + r1 * kTileCols + 4 * hh);
+                lo4[0] = fminf(lo4[0], fminf(x.x, y.x)); hi4[0] = fmaxf(hi4[0], fmaxf(x.x, y.x));
+                lo4[1] = fminf(lo4[1], fminf(x.y, y.y)); hi4[1] = fmaxf(hi4[1], fmaxf(x.y, y.y));
+                lo4[2] = fminf(lo4[2], fminf(x.z, y.z)); hi4[2] = fmaxf(hi4[2], fmaxf(x.z, y.z));
+                lo4[3] = fminf(lo4[3], fminf(x.w, y.w)); hi4[3] = fmaxf(hi4[3], fmaxf(x.w, y.w));
+            }
+    #pragma unroll
+            for (int o = 2; o < 32; o <<= 1)
+    #pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    lo4[q] = fminf(lo4[q], __shfl_xor_sync(0xffffffffu, lo4[q], o));
+                    hi4[q] = fmaxf(hi4[q], __shfl_xor_sync(0xffffffffu, hi4[q], o));
+                }
+            if (lane < 2) {
+    #pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    s_lo[warp][4 * lane + q] = lo4[q];
+                    s_hi[warp][4 * lane + q] = hi4[q];
+                }
+            }
+        }
+        __syncthreads();
+        if constexpr (NSPLIT > 1) {
+            if (tid < kTileCols) {
+                float l = s_lo[0][tid], h = s_hi[0][tid];
+                for (int q = 1; q < kBinWarps; ++q) {
+                    l = fminf(l, s_lo[q][tid]);
+                    h = fmaxf(h, s_hi[q][tid]);
+                }
+                part_lo[tid] = l;
+                part_hi[tid] = h;
+                // push into the partner too (peer slot): after the barrier both
+                // read only local shared memory
+                cg::cluster_group cl = cg::this_cluster();
+                *cl.map_shared_rank(&peer_lo[tid], rank ^ 1) = l;
+                *cl.map_shared_rank(&peer_hi[tid], rank ^ 1) = h;
+            }
+            cg::this_cluster().sync();
+        }
+        if (tid < kTileCols) {
+            float l, h;
+            if constexpr (NSPLIT > 1) {
+                // min / max are order-free: every CTA of the cluster derives the same extremes
+                l = fminf(part_lo[tid], peer_lo[tid]);
+                h = fmaxf(part_hi[tid], peer_hi[tid]);
+            } else {
+                l = s_lo[0][tid];
+                h = s_hi[0][tid];
+                for (int q = 1; q < kBinWarps; ++q) {
+                    l = fminf(l, s_lo[q][tid]);
+                    h = fmaxf(h, s_hi[q][tid]);
+                }
+            }
+            set_col(l, h);
+        }
+        __syncthreads();
+
+        // ---- sweep B: histograms from shared memory.  Two threads per row, one
+        // float4 (4 columns) each, as in sweep A: one LDS.128 per 4 values and
+        // the per-column constants in registers.  Branch-free: a column that is
+        // not binarised (inactive or constant) still counts into its own
+        // histogram (bin_index stays in [0, 255] for any input), which Otsu then
+        // ignores
+        {
+            const int hh = tid & 1;
+            float clo[4], csc[4];
+            uint32_t* hc[4];
+            bool any = false;
+    #pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int cc = 4 * hh + q;
+                clo[q] = c_lo[cc];
+                csc[q] = c_scale[cc];
+                hc[q] = hist + cc * kHistStride;
+                any |= c_use[cc] != 0;
+            }
+            if (any) {
+                constexpr int RS = kBinThreads / 2;  // row stride
+                int r = tid >> 1;
+                for (; r + RS < rows; r += 2 * RS) {
+                    const float4 x0 = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols + 4 * hh);
+                    const float4 x1 = *reinterpret_cast<const float4*>(bt_vals + (r + RS) * kTileCols + 4 * hh);
+                    const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+    #pragma unroll
+                    for (int q = 0; q < 8; ++q) atomicAdd(hc[q & 3] + bin_index(xv[q], clo[q & 3], csc[q & 3]), 1u);
+                }
+                if (r < rows) {
+                    const float4 x0 = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols + 4 * hh);
+                    const float xv[4] = {x0.x, x0.y, x0.z, x0.w};
+    #pragma unroll
+                    for (int q = 0; q < 4; ++q) atomicAdd(hc[q] + bin_index(xv[q], clo[q], csc[q]), 1u);
+                }
+            }
+        }
+    } else {
+        // ---- sweep B, streaming: two rows of each box per thread (one float4
+        // of 4 columns each) as soon as the box lands; every thread waits for
+        // every box, since sweep C reads them all
         const int hh = tid & 1;
         float clo[4], csc[4];
         uint32_t* hc[4];
@@ -605,19 +652,18 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
             hc[q] = hist + cc * kHistStride;
             any |= c_use[cc] != 0;
         }
-        if (any) {
-            constexpr int RS = kBinThreads / 2;  // row stride
-            int r = tid >> 1;
-            for (; r + RS < rows; r += 2 * RS) {
-                const float4 x0 = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols + 4 * hh);
-                const float4 x1 = *reinterpret_cast<const float4*>(bt_vals + (r + RS) * kTileCols + 4 * hh);
-                const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        for (int b = 0; b < nbox; ++b) {
+            mbar_wait(&box_bar[b], 0);
+            const int ra = b * kBox + (tid >> 1), rb = ra + kBinThreads / 2;
+            if (any && ra < rows) {
+                const float4 x = *reinterpret_cast<const float4*>(bt_vals + ra * kTileCols + 4 * hh);
+                const float xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-                for (int q = 0; q < 8; ++q) atomicAdd(hc[q & 3] + bin_index(xv[q], clo[q & 3], csc[q & 3]), 1u);
+                for (int q = 0; q < 4; ++q) atomicAdd(hc[q] + bin_index(xv[q], clo[q], csc[q]), 1u);
             }
-            if (r < rows) {
-                const float4 x0 = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols + 4 * hh);
-                const float xv[4] = {x0.x, x0.y, x0.z, x0.w};
+            if (any && rb < rows) {
+                const float4 x = *reinterpret_cast<const float4*>(bt_vals + rb * kTileCols + 4 * hh);
+                const float xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) atomicAdd(hc[q] + bin_index(xv[q], clo[q], csc[q]), 1u);
             }
@@ -674,6 +720,13 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
 constexpr int kTileSplitRows = 3264;
 
 bool binarize_tile_ok(int rows, int cols) { return cols % 32 == 0 && rows <= 2 * kTileMaxRows && rows > 0; }
+
+// The 2-CTA cluster form (rows > kTileSplitRows) gains from the fused K1's
+// column extremes (no min / max sweep, no extremes exchange, histograms built
+// as boxes land: Hann K4 7.43 -> 5.97 ms per step against +1.0 ms of K1); the
+// single-CTA form's min / max sweep already hides under its box loads, so
+// there the extremes cost K1 more than they save (C5r: K1 +0.49, K4 -0.43).
+bool binarize_wants_extremes(int rows) { return rows > kTileSplitRows; }
 
 // The [plots][rows][cols] fp32 TF tensor as a TMA tensor map with 8 x kBox x 1
 // boxes (rows past the end of a plot read as zeros and are never used).

@@ -324,7 +324,8 @@ long long worst_pool(int rows, int cols) { return static_cast<long long>(rows) *
 // already in psd (fused into K1); else computed here.
 ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int cols,
                         const unsigned long long* seq_dev, double fs, const ss_detector_cfg& cfg,
-                        float* psd, bool psd_ready, const ss_batch_out& out_dev, int time_bins = 0) {
+                        float* psd, bool psd_ready, const ss_batch_out& out_dev, int time_bins = 0,
+                        const float* col_lo = nullptr, const float* col_hi = nullptr) {
     const int W = (cols + 31) / 32;
     const double* wts = nullptr;
     ss_status s = weights(ctx, cfg.savgol_window, cfg.savgol_order, &wts);
@@ -370,6 +371,8 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
     B.active_bits = abits;
     const bool tile = ssb::binarize_tile_ok(rows, cols);
     if (tile) {
+        B.col_lo = col_lo;  // column extremes from the fused K1, when it made them
+        B.col_hi = col_hi;
         B.mask_bytes = reinterpret_cast<uint8_t*>(m0);  // the bit mask, written bytewise
         B.skip_empty = true;  // empty column groups stay unwritten; K5 reads them as background
     } else {
@@ -904,6 +907,15 @@ static ss_status sense_device(ss_ctx* ctx, const void* diq, ss_fmt fmt, int n_ff
     L.iq = diq;
     L.tf = tf;
     L.psd_out = praw;
+    float* col_lo = nullptr;
+    float* col_hi = nullptr;
+    if (fused && ssb::fft_psd_extremes(ilog2(n_fft)) && ssb::binarize_tile_ok(rows, cols) &&
+        ssb::binarize_wants_extremes(rows)) {
+        SS_WS(clo, float, "det.col_lo", static_cast<size_t>(n_plots) * cols);
+        SS_WS(chi, float, "det.col_hi", static_cast<size_t>(n_plots) * cols);
+        col_lo = L.col_lo = clo;
+        col_hi = L.col_hi = chi;
+    }
     L.tw = tw;
     L.total_rows = static_cast<long long>(rows) * n_plots;
     L.rows_per_plot = rows;
@@ -934,7 +946,7 @@ static ss_status sense_device(ss_ctx* ctx, const void* diq, ss_fmt fmt, int n_ff
         ctx->launches += 1;
         seq = sq;
     }
-    return detect_device(ctx, tf, n_plots, rows, cols, seq, sample_rate_hz, cfg, praw, true, dev, hop);
+    return detect_device(ctx, tf, n_plots, rows, cols, seq, sample_rate_hz, cfg, praw, true, dev, hop, col_lo, col_hi);
 }
 
 // outputs of plots [p0, p0 + n) inside a batch-out block of box capacity K

@@ -397,6 +397,8 @@ struct FftArgs {
     const void* iq;      // n_rows_total * N samples, f32 or i16 interleaved
     float* tf;           // n_rows_total * N floats, may be null in PSD mode
     float* psd;          // n_plots * N (PSD mode)
+    float* col_lo;       // n_plots * N column minima / maxima of the plot (PSD mode, TMEM shapes) or null
+    float* col_hi;
     const double2* tw;   // per-N pass twiddle table (global)
     long long total_rows;
     int rows_per_plot;   // PSD mode: T
@@ -425,6 +427,9 @@ struct K1Shape {
     static constexpr int WARPS = THREADS / 32;
     // TMEM: warp w uses lanes 32*(w%4).., columns 32*(w/4) .. +31 (16 doubles)
     static constexpr int TMEM_COLS = WARPS <= 4 ? 32 : WARPS <= 8 ? 64 : WARPS <= 16 ? 128 : 256;
+    // column extremes (fminf / fmaxf of the plot's magnitudes, for K4) in a
+    // second block of TMEM_COLS columns: 16 minima + 16 maxima per thread
+    __host__ __device__ static constexpr int tmem_alloc_cols(bool ext) { return ext ? 2 * TMEM_COLS : TMEM_COLS; }
     static_assert(!ACC_TMEM || PL::P == 16, "one 32-column TMEM slot holds 16 double accumulators");
     __host__ __device__ static constexpr size_t tw_bytes() { return TW_SMEM ? sizeof(double2) * (PL::tw_size() > 0 ? PL::tw_size() : 1) : 0; }
     __host__ __device__ static constexpr size_t group_bytes(int sample_bytes) {
@@ -434,7 +439,7 @@ struct K1Shape {
     __host__ __device__ static constexpr size_t smem(int sample_bytes) { return tw_bytes() + GROUPS * group_bytes(sample_bytes); }
 };
 
-template <int LOGN, int FMT, bool PSD, bool WIN>
+template <int LOGN, int FMT, bool PSD, bool WIN, bool EXT>
 __global__ void __launch_bounds__(K1Shape<LOGN>::THREADS, 1)
 fft_mag_kernel(FftArgs a) {
     using PL = FftPlan<LOGN>;
@@ -499,7 +504,7 @@ fft_mag_kernel(FftArgs a) {
     __shared__ uint32_t tmem_slot;
     const int wid = static_cast<int>(threadIdx.x) >> 5;
     if constexpr (PSD && KS::ACC_TMEM) {
-        if (wid == 0) tmem_alloc<KS::TMEM_COLS>(&tmem_slot);
+        if (wid == 0) tmem_alloc<KS::tmem_alloc_cols(EXT)>(&tmem_slot);
         tmem_fence_before();
     }
     __syncthreads();  // twiddle copy + mbarrier init (+ TMEM address) visible to all groups
@@ -511,6 +516,15 @@ fft_mag_kernel(FftArgs a) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) z[i] = 0u;  // +0.0 in both halves of every double
         tmem_st32(taddr, z);
+        if constexpr (EXT) {
+            uint32_t ext[32];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                ext[i] = 0x7f800000u;       // +inf: minima
+                ext[16 + i] = 0xff800000u;  // -inf: maxima
+            }
+            tmem_st32(taddr + KS::TMEM_COLS, ext);
+        }
     }
     if (lt == 0 && it_begin < it_end) {
         StageIssue first{stage, nullptr, 0u, bar, true, true};
@@ -607,7 +621,6 @@ fft_mag_kernel(FftArgs a) {
                 }
             }
             if constexpr (PSD) {
-                // G == 1: every row of the iteration space is valid (warp-uniform)
                 tmem_wait_ld();
 #pragma unroll
                 for (int i = 0; i < PL::P; ++i) {
@@ -617,6 +630,17 @@ fft_mag_kernel(FftArgs a) {
                     t[2 * i + 1] = static_cast<uint32_t>(__double2hiint(s));
                 }
                 tmem_st32(taddr, t);
+                if constexpr (EXT) {  // column extremes for K4 (order-free, exact)
+                    uint32_t e[32];
+                    tmem_ld32(taddr + KS::TMEM_COLS, e);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < PL::P; ++i) {
+                        e[i] = __float_as_uint(fminf(__uint_as_float(e[i]), m[i]));
+                        e[16 + i] = __float_as_uint(fmaxf(__uint_as_float(e[16 + i]), m[i]));
+                    }
+                    tmem_st32(taddr + KS::TMEM_COLS, e);
+                }
             }
         } else {
             // stage magnitudes so stores are row-contiguous and PSD runs in row order
@@ -674,6 +698,19 @@ fft_mag_kernel(FftArgs a) {
                         const double sum = __hiloint2double(static_cast<int>(t[2 * i + 1]), static_cast<int>(t[2 * i]));
                         psd[k] = __double2float_rn(__dmul_rn(sum, inv_rows));
                     }
+                if constexpr (EXT) {
+                    tmem_ld32(taddr + KS::TMEM_COLS, t);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int u = 0; u < UL; ++u)
+#pragma unroll
+                        for (int r = 0; r < RL; ++r) {
+                            const int i = u * RL + r;
+                            const int k = (j + PL::TPR * u + r * NSL + N / 2) & (N - 1);
+                            a.col_lo[plot * N + k] = __uint_as_float(t[i]);
+                            a.col_hi[plot * N + k] = __uint_as_float(t[16 + i]);
+                        }
+                }
             } else {
 #pragma unroll
                 for (int i = 0; i < NACC; ++i) {
@@ -687,7 +724,7 @@ fft_mag_kernel(FftArgs a) {
             tmem_fence_before();
             __syncthreads();  // every warp is done with its columns
             tmem_fence_after();
-            if (wid == 0) tmem_dealloc<KS::TMEM_COLS>(tmem_slot);
+            if (wid == 0) tmem_dealloc<KS::tmem_alloc_cols(EXT)>(tmem_slot);
         }
     }
 }
@@ -722,11 +759,11 @@ static void build_tw(std::vector<double2>& out) {
     }
 }
 
-template <int LOGN, int FMT, bool PSD, bool WIN>
+template <int LOGN, int FMT, bool PSD, bool WIN, bool EXT = false>
 static cudaError_t ensure_smem_attr() {
     static std::atomic<unsigned long long> attr_done;  // per instantiation, one bit per device
     return set_attr_once(attr_done, [] {
-        return cudaFuncSetAttribute(fft_mag_kernel<LOGN, FMT, PSD, WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        return cudaFuncSetAttribute(fft_mag_kernel<LOGN, FMT, PSD, WIN, EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(K1Shape<LOGN>::smem(FMT == 0 ? 8 : 4)));
     });
 }
@@ -736,25 +773,27 @@ template <int LOGN, int FMT, bool WIN>
 static int psd_slots_one() {
     if (ensure_smem_attr<LOGN, FMT, true, WIN>() != cudaSuccess) return 0;
     int blocks = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fft_mag_kernel<LOGN, FMT, true, WIN>,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fft_mag_kernel<LOGN, FMT, true, WIN, false>,
                                                       K1Shape<LOGN>::THREADS,
                                                       K1Shape<LOGN>::smem(FMT == 0 ? 8 : 4)) != cudaSuccess)
         return 0;
     return blocks * K1Shape<LOGN>::GROUPS;
 }
 
-template <int LOGN, int FMT, bool PSD, bool WIN>
+template <int LOGN, int FMT, bool PSD, bool WIN, bool EXT = false>
 static cudaError_t launch_one(const FftLaunch& L, cudaStream_t st) {
     using PL = FftPlan<LOGN>;
     using KS = K1Shape<LOGN>;
-    auto kern = fft_mag_kernel<LOGN, FMT, PSD, WIN>;
+    auto kern = fft_mag_kernel<LOGN, FMT, PSD, WIN, EXT>;
     const size_t smem = KS::smem(FMT == 0 ? 8 : 4);
-    cudaError_t e = ensure_smem_attr<LOGN, FMT, PSD, WIN>();
+    cudaError_t e = ensure_smem_attr<LOGN, FMT, PSD, WIN, EXT>();
     if (e != cudaSuccess) return e;
     FftArgs a;
     a.iq = L.iq;
     a.tf = L.tf;
     a.psd = L.psd_out;
+    a.col_lo = EXT ? L.col_lo : nullptr;
+    a.col_hi = EXT ? L.col_hi : nullptr;
     a.tw = L.tw;
     a.total_rows = L.total_rows;
     a.rows_per_plot = L.rows_per_plot;
@@ -776,6 +815,12 @@ static cudaError_t launch_one(const FftLaunch& L, cudaStream_t st) {
 
 template <int LOGN>
 static cudaError_t dispatch_fmt(const FftLaunch& L, cudaStream_t st) {
+    if constexpr (K1Shape<LOGN>::ACC_TMEM) {  // fused PSD + column extremes (K4's cluster form)
+        if (L.psd && L.col_lo) {
+            if (L.win) return L.fmt == 0 ? launch_one<LOGN, 0, true, true, true>(L, st) : launch_one<LOGN, 1, true, true, true>(L, st);
+            return L.fmt == 0 ? launch_one<LOGN, 0, true, false, true>(L, st) : launch_one<LOGN, 1, true, false, true>(L, st);
+        }
+    }
     if (L.win) {
         if (L.fmt == 0) return L.psd ? launch_one<LOGN, 0, true, true>(L, st) : launch_one<LOGN, 0, false, true>(L, st);
         return L.psd ? launch_one<LOGN, 1, true, true>(L, st) : launch_one<LOGN, 1, false, true>(L, st);
@@ -819,6 +864,8 @@ static int psd_slots_fmt(int fmt, bool win) {
     if (win) return fmt == 0 ? psd_slots_one<LOGN, 0, true>() : psd_slots_one<LOGN, 1, true>();
     return fmt == 0 ? psd_slots_one<LOGN, 0, false>() : psd_slots_one<LOGN, 1, false>();
 }
+
+bool fft_psd_extremes(int logn) { return logn == 12 || logn == 13; }  // the TMEM (one row per group) shapes
 
 int fft_psd_slots_per_sm(int logn, int fmt, bool win) {
     switch (logn) {

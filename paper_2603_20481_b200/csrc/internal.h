@@ -16,6 +16,8 @@ struct FftLaunch {
     const void* iq = nullptr;
     float* tf = nullptr;  // may be null when psd
     float* psd_out = nullptr;
+    float* col_lo = nullptr;     // fused PSD, n_fft >= 4096: the plots' column extremes (K4's sweep A) or null
+    float* col_hi = nullptr;
     const double2* tw = nullptr;
     long long total_rows = 0;
     int rows_per_plot = 0;
@@ -27,6 +29,8 @@ struct FftLaunch {
 cudaError_t fft_mag_launch(const FftLaunch& L, cudaStream_t st);
 // plots per SM the fused-PSD K1 grid runs concurrently (one plot per row group)
 int fft_psd_slots_per_sm(int logn, int fmt, bool win);
+// the fused-PSD K1 also writes column extremes (FftLaunch::col_lo / col_hi) for this size
+bool fft_psd_extremes(int logn);
 void fft_window(int n_fft, int kind, std::vector<double>& out);  // kind 0 rect, 1 periodic Hann
 // n_fft = 2^14 .. 2^20: global-memory SSFFT-2 passes + magnitudes (no PSD)
 constexpr int kLargeLogNMax = 20;
@@ -82,6 +86,8 @@ struct BinarizeLaunch {
     int rows = 0;
     int cols = 0;
     const uint32_t* active_bits = nullptr;  // n_plots x W
+    const float* col_lo = nullptr;      // optional n_plots x cols column extremes (from K1): the tile path
+    const float* col_hi = nullptr;      // then skips its min / max sweep and bins boxes as they land
     uint32_t* mask_bits = nullptr;      // n_plots x W x rows word-major bits (bit mode) or null
     uint8_t* mask_bytes = nullptr;     // tile path: the word-major bit mask as bytes (byte k of word w = columns 32w+8k..+7) or null
     bool skip_empty = false;           // tile path: groups with no active column write nothing (K5 masks them)
@@ -93,6 +99,8 @@ struct BinarizeLaunch {
 cudaError_t binarize_launch(const BinarizeLaunch& L, cudaStream_t st);
 // true when the smem-resident tile kernel (bytewise writes into the bit mask) handles this shape
 bool binarize_tile_ok(int rows, int cols);
+// true when the tile path should take column extremes from the fused K1 (BinarizeLaunch::col_lo)
+bool binarize_wants_extremes(int rows);
 
 // ---- K5 morph.cu
 cudaError_t pack_u8_launch(const uint8_t* m, int n_plots, int rows, int cols, uint32_t* bits,

@@ -386,3 +386,45 @@ def test_async_batches_match_sync(ss, ref):
         assert lib.ss_wait(ctx.h) == NAT.SS_OK          # the flags were consumed
     finally:
         lib.ss_set_async(ctx.h, 0)
+
+
+def test_fused_tall_plots_take_k1_extremes(ss, ora):
+    """Config 5 as written at full size (296 plots x 4881 rows, Hann, hop 2048):
+    the fused K1 also writes the column extremes and K4's 2-CTA cluster form
+    bins each box as it lands (no min / max sweep).  Three plots carrying the
+    seeded tone burst (early, middle, late) against the oracle's STFT
+    restatement, bit for bit."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2603_20481_b200 import _native as NAT
+    from paper_2603_20481_b200.specsense import DetectorConfig, _batch_out, _unpack_batch
+
+    n_fft, hop, rows, P, fs = 4096, 2048, 4881, 296, 100e6
+    n = P * rows * hop + n_fft - hop
+    g = torch.Generator(device="cuda").manual_seed(4881)
+    iq = torch.randn(2 * n, generator=g, device="cuda", dtype=torch.float32)
+    t = torch.arange(n, device="cuda", dtype=torch.float64)
+    burst = ((t // (rows * hop)) % 5 == 1) & ((t % (rows * hop)) < rows * hop // 3)
+    ph = 2 * np.pi * 0.17 * t
+    iq[0::2] += (4 * torch.cos(ph) * burst).float()
+    iq[1::2] += (4 * torch.sin(ph) * burst).float()
+    del t, burst, ph
+    tf = torch.empty((P, rows, n_fft), dtype=torch.float32, device="cuda")
+    out_t, out = _batch_out(torch, P, n_fft, 4096)
+    ctx = ss.Context.get(0)
+    cfg = DetectorConfig().c()
+    ctx.check(ctx.lib.ss_stft_sense_batch(ctx.h, C.c_void_p(iq.data_ptr()), NAT.SS_FMT_F32, n_fft, hop, 1, rows, P, 0,
+                                          fs, C.byref(cfg), C.c_void_p(tf.data_ptr()), C.byref(out)))
+    torch.cuda.synchronize()
+    dets = _unpack_batch(out_t, P)
+    for p in (1, 146, 291):  # plots p % 5 == 1 carry the burst
+        seg = iq[2 * p * rows * hop: 2 * (p * rows * hop + (rows - 1) * hop + n_fft)].cpu().numpy().view(np.complex64)
+        exp_tf = ora.stft_plot(seg, n_fft, hop, 1, rows)
+        assert np.array_equal(tf[p].cpu().numpy().view(np.uint32), exp_tf.view(np.uint32)), p
+        exp = ora.detect(exp_tf, start_seq=p * rows, fs=fs)
+        assert np.array_equal(dets[p].psd.raw.view(np.uint32), exp["raw"].view(np.uint32)), p
+        assert np.array_equal(dets[p].active_columns, exp["active"]), p
+        assert np.array_equal(dets[p].bin_boxes, exp["bin_boxes"]), p
+        assert len(dets[p].bin_boxes) > 0, p
