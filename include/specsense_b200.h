@@ -243,6 +243,9 @@ typedef struct {
     int shard_count;       /* multi-GPU: windows are dealt round-robin over shard_count engines */
     int shard_index;       /* ... this engine senses windows w with w % shard_count == shard_index
                               (0 / 0: every window); others are skipped, not counted as lost */
+    int stage_timing;      /* 1: per-stage device times in ss_plot_record.stage_s (event-record nodes
+                              in each window's graph: about 0.12 ms of device time per P window);
+                              0: only gpu_s, the window's whole device time */
 } ss_engine_cfg;
 
 /* runtime::PlotRecord (proj/include/specsense/runtime.hpp:62-69) + extras */
@@ -271,6 +274,14 @@ const char* ss_engine_last_error(const ss_engine* eng);
    buffer, like frontend::PingPongBuffer writers: when push returns, the samples
    have been copied out of `samples` (staged or DMA'd) and it may be reused. */
 ss_status ss_engine_push(ss_engine* eng, const void* samples, int64_t n_chunks, uint64_t first_seq);
+/* As ss_engine_push, but a DMA straight from a pinned / device `samples` is only
+   queued: the caller keeps the buffer unchanged until ss_engine_push_fence
+   returns (or the engine is finished / closed), and back-to-back pushes'
+   copies overlap (an immutable source such as the runtime's MemorySource). */
+ss_status ss_engine_push_async(ss_engine* eng, const void* samples, int64_t n_chunks, uint64_t first_seq);
+/* Every copy out of the caller's buffers queued by ss_engine_push_async has
+   finished. */
+ss_status ss_engine_push_fence(ss_engine* eng);
 /* Chunks [first_seq, last_seq) were lost upstream: their windows drop
    (frontend::PingPongBuffer::mark_lost_range). */
 ss_status ss_engine_mark_lost(ss_engine* eng, uint64_t first_seq, uint64_t last_seq);

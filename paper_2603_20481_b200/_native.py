@@ -47,7 +47,8 @@ class BaselineCfg(C.Structure):
 class EngineCfg(C.Structure):
     _fields_ = [("n_fft", C.c_int), ("plot_rows", C.c_int), ("fmt", C.c_int), ("sample_rate_hz", C.c_double),
                 ("n_banks", C.c_int), ("paced", C.c_int), ("deadline_s", C.c_double), ("box_capacity", C.c_int),
-                ("hop", C.c_int), ("window", C.c_int), ("shard_count", C.c_int), ("shard_index", C.c_int)]
+                ("hop", C.c_int), ("window", C.c_int), ("shard_count", C.c_int), ("shard_index", C.c_int),
+                ("stage_timing", C.c_int)]
 
 
 class PlotRecord(C.Structure):
@@ -100,6 +101,8 @@ SIGNATURES = {
     "ss_engine_close": (None, [_P]),
     "ss_engine_last_error": (C.c_char_p, [_P]),
     "ss_engine_push": (_I, [_P, _P, C.c_int64, C.c_uint64]),
+    "ss_engine_push_async": (_I, [_P, _P, C.c_int64, C.c_uint64]),
+    "ss_engine_push_fence": (_I, [_P]),
     "ss_engine_mark_lost": (_I, [_P, C.c_uint64, C.c_uint64]),
     "ss_engine_finish": (_I, [_P]),
     "ss_engine_poll": (_I, [_P, _I, C.POINTER(PlotRecord), _P, _P, _I, C.POINTER(_I)]),

@@ -367,10 +367,10 @@ ss_status ss_engine_open(int device, const ss_engine_cfg* cfg, const ss_detector
         cudaGraph_t g = nullptr;
         for (cudaEvent_t& ev : b.stage_ev)
             if (cudaEventCreate(&ev) != cudaSuccess) return bad(SS_ECUDA, "event");
-        ssb::engine_stage_events(e->ctx, b.stage_ev, nullptr);
+        if (cfg->stage_timing) ssb::engine_stage_events(e->ctx, b.stage_ev, nullptr);
         const ss_status cs = ssb::engine_sense(e->ctx, b.iq, cfg->fmt, F, e->hop, e->window, T, 0, cfg->sample_rate_hz,
                                                *det, b.tf, dev_out(b, K), b.d_seq);
-        ssb::engine_stage_events(e->ctx, nullptr, b.stage_used);
+        if (cfg->stage_timing) ssb::engine_stage_events(e->ctx, nullptr, b.stage_used);
         bool ok = cs == SS_OK &&
                   cudaMemcpyAsync(&b.host->n_boxes, b.n_boxes, sizeof(int32_t), cudaMemcpyDeviceToHost, e->compute) == cudaSuccess &&
                   cudaMemcpyAsync(&b.host->n_active, b.n_active, sizeof(int32_t), cudaMemcpyDeviceToHost, e->compute) == cudaSuccess &&
@@ -462,7 +462,7 @@ static void windows_of(const ss_engine* e, uint64_t a0, uint64_t a1, uint64_t* w
     *w_hi = (a1 - 1) / e->stride;                               // last w with w*stride < a1
 }
 
-ss_status ss_engine_push(ss_engine* e, const void* samples, int64_t n_chunks, uint64_t first_seq) {
+static ss_status push_impl(ss_engine* e, const void* samples, int64_t n_chunks, uint64_t first_seq, bool sync) {
     if (!e || (!samples && n_chunks > 0) || n_chunks < 0) return SS_EVALIDATION;
     if (n_chunks == 0) return SS_OK;
     const uint64_t F = static_cast<uint64_t>(e->cfg.n_fft);
@@ -518,7 +518,7 @@ ss_status ss_engine_push(ss_engine* e, const void* samples, int64_t n_chunks, ui
             if (s != SS_OK) return s;
         }
     }
-    if (direct) {
+    if (direct && sync) {
         // The reference's push is synchronous: the caller may reuse its buffer
         // as soon as push returns, so wait for the DMA out of it (not for the
         // window's sensing).  Waited on outside the lock.
@@ -532,6 +532,34 @@ ss_status ss_engine_push(ss_engine* e, const void* samples, int64_t n_chunks, ui
             std::lock_guard<std::mutex> g(e->mu);
             return efail(e, SS_ECUDA, std::string("push copy: ") + cudaGetErrorString(w));
         }
+    }
+    return SS_OK;
+}
+
+ss_status ss_engine_push(ss_engine* e, const void* samples, int64_t n_chunks, uint64_t first_seq) {
+    return push_impl(e, samples, n_chunks, first_seq, true);
+}
+
+// The caller keeps `samples` unchanged until ss_engine_push_fence (or the
+// engine's finish / close): consecutive pushes' DMAs queue back to back.
+ss_status ss_engine_push_async(ss_engine* e, const void* samples, int64_t n_chunks, uint64_t first_seq) {
+    return push_impl(e, samples, n_chunks, first_seq, false);
+}
+
+ss_status ss_engine_push_fence(ss_engine* e) {
+    if (!e) return SS_EVALIDATION;
+    cudaEvent_t ev;
+    EN_CK(e, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    cudaError_t r;
+    {
+        std::lock_guard<std::mutex> lk(e->mu);
+        r = cudaEventRecord(ev, e->copy);
+    }
+    const cudaError_t w = r == cudaSuccess ? cudaEventSynchronize(ev) : r;
+    cudaEventDestroy(ev);
+    if (w != cudaSuccess) {
+        std::lock_guard<std::mutex> g(e->mu);
+        return efail(e, SS_ECUDA, std::string("push fence: ") + cudaGetErrorString(w));
     }
     return SS_OK;
 }
@@ -559,6 +587,7 @@ ss_status ss_engine_mark_lost(ss_engine* e, uint64_t first, uint64_t last) {
 
 ss_status ss_engine_finish(ss_engine* e) {
     if (!e) return SS_EVALIDATION;
+    cudaStreamSynchronize(e->copy);  // copies out of ss_engine_push_async buffers are done
     {
         std::lock_guard<std::mutex> lk(e->mu);
         e->finished = true;

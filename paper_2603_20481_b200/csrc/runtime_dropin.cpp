@@ -141,6 +141,7 @@ RunReport run(frontend::ChunkSource& source, const frontend::FrontendConfig& fc,
     ec.paced = source.paced() ? 1 : 0;
     ec.deadline_s = deadline;
     ec.box_capacity = kCap;
+    ec.stage_timing = 1;  // RunReport::stage_totals / fft_time_s, as the reference reports them
     ss_detector_cfg c{};
     c.savgol_window = dc.savgol_window;
     c.savgol_order = dc.savgol_order;

@@ -39,7 +39,11 @@ class FrontendConfig:
 class RuntimeConfig:
     """runtime.hpp:13-24.  The CPU worker counts and halo are validated like
     the reference and otherwise unused (the GPU runs every window whole);
-    ``n_banks`` is the HBM bank count (2 = the reference's ping-pong)."""
+    ``n_banks`` is the HBM bank count (2 = the reference's ping-pong);
+    ``stage_timing`` makes the engine time every stage of every window on the
+    device (ss_plot_record.stage_s: event-record nodes in each window's graph,
+    about 0.12 ms of device time per P window; the C++ drop-in's
+    runtime::run always sets it for RunReport::stage_totals)."""
     n_compute_workers: int = 1
     n_sensing_workers: int = 1
     halo_bins: int = 4
@@ -47,6 +51,7 @@ class RuntimeConfig:
     deadline_s: float = 0.0
     n_banks: int = 2
     box_capacity: int = 16384
+    stage_timing: bool = False
 
     def validate(self):
         if self.n_compute_workers < 1 or self.n_sensing_workers < 1:
@@ -157,6 +162,10 @@ class MemorySource:
     def paced(self) -> bool:
         return self.pace
 
+    # the yielded views point into one private buffer that is never written
+    # again: the engine may DMA out of them asynchronously (Engine.push stable)
+    stable = True
+
     def blocks(self):
         """Yields (first_seq, ndarray view of k chunks); views never wrap the buffer end."""
         seq = 0
@@ -210,7 +219,7 @@ class Engine:
         self.fmt = fmt
         self.cap = rc.box_capacity
         cfg = N.EngineCfg(self.F, self.T, fmt, self.fs, rc.n_banks, int(paced), rc.deadline_s, rc.box_capacity,
-                          hop, window, shard[1], shard[0])
+                          hop, window, shard[1], shard[0], int(rc.stage_timing))
         det = (detector_config or DetectorConfig()).c()
         h = C.c_void_p()
         st = self.lib.ss_engine_open(device, C.byref(cfg), C.byref(det), C.byref(h))
@@ -233,11 +242,19 @@ class Engine:
             raise FormatError(msg)
         raise Error(f"status {st}: {msg}")
 
-    def push(self, samples: np.ndarray, first_seq: int):
+    def push(self, samples: np.ndarray, first_seq: int, stable: bool = False):
+        """stable=True: `samples` stays unchanged until finish() (or
+        push_fence()), so a DMA out of it is only queued (ss_engine_push_async)
+        and consecutive pushes' copies overlap; else push returns once the
+        samples have left the buffer (the reference's synchronous writers)."""
         per = self.F * (2 if self.fmt == N.SS_FMT_I16 else 1)
         if samples.size % per:
             raise ValidationError("push takes whole chunks")
-        self._check(self.lib.ss_engine_push(self.h, C.c_void_p(samples.ctypes.data), samples.size // per, first_seq))
+        fn = self.lib.ss_engine_push_async if stable else self.lib.ss_engine_push
+        self._check(fn(self.h, C.c_void_p(samples.ctypes.data), samples.size // per, first_seq))
+
+    def push_fence(self):
+        self._check(self.lib.ss_engine_push_fence(self.h))
 
     def mark_lost(self, first: int, last: int):
         self._check(self.lib.ss_engine_mark_lost(self.h, first, last))
@@ -300,6 +317,8 @@ def run(source, frontend_config: FrontendConfig, detector_config: DetectorConfig
     errors = []
     wall0 = time.perf_counter()  # after the engine's one-time setup (banks, graphs, warm-up window)
 
+    stable = bool(getattr(source, "stable", False))
+
     def ingest():
         expected = 0
         try:
@@ -307,7 +326,7 @@ def run(source, frontend_config: FrontendConfig, detector_config: DetectorConfig
                 for e_ in engines:  # each engine keeps only its own windows' samples
                     if seq > expected:
                         e_.mark_lost(expected, seq)
-                    e_.push(block, seq)
+                    e_.push(block, seq, stable=stable)
                 expected = seq + block.size // (frontend_config.n_fft * (2 if source.fmt == N.SS_FMT_I16 else 1))
         except Exception as e:  # noqa: BLE001
             errors.append(e)
