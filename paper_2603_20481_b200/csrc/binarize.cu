@@ -495,13 +495,11 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     // ---- load the block: one TMA box per kBox rows (32 B x kBox), each on its
     // own mbarrier, so sweep A starts on the first box while the rest land
     const int nbox = (rows + kBox - 1) / kBox;
-    if (tid == 0) {
-        for (int b = 0; b < nbox; ++b) mbar_init(&box_bar[b], 1);
+    if (tid < nbox) {  // thread b issues box b: the boxes leave in parallel
+        mbar_init(&box_bar[tid], 1);
         fence_mbar_init();
-        for (int b = 0; b < nbox; ++b) {
-            mbar_arrive_expect_tx(&box_bar[b], kBox * kTileCols * sizeof(float));
-            tma_load_box(bt_vals + b * kBox * kTileCols, &tmap, col0, rbase + b * kBox, p, &box_bar[b]);
-        }
+        mbar_arrive_expect_tx(&box_bar[tid], kBox * kTileCols * sizeof(float));
+        tma_load_box(bt_vals + tid * kBox * kTileCols, &tmap, col0, rbase + tid * kBox, p, &box_bar[tid]);
     }
     // per-column binning constants from the column extremes (bin_of,
     // detector.cpp:28-39); thread tid < 8 owns column col0 + tid
