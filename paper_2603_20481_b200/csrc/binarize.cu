@@ -184,28 +184,70 @@ __device__ __forceinline__ int otsu_split_warp_u32(const uint32_t* hq, int lane)
     const double total = static_cast<double>(total_u);
     const double sum_all = static_cast<double>(sum_all_u);
 
-    // estimates: D = sum0*w1 - sum1*w0 exactly in int64 (|D| < 2^37), p = w0*w1 < 2^26
-    double est[8];
-    double m = -1.0;
+    // estimates X_i = D^2 / p, D = sum0*w1 - sum1*w0 exactly in int64
+    // (|D| < 2^37), p = w0*w1 < 2^26.  First in FP32 for every split
+    // (relative error < 2^-21: D and p rounded once, rcp.approx within an ulp,
+    // two rounded products), then in double only for the splits that can
+    // still be candidates.  With f the float and e the double estimates
+    // (|e - X| <= 2^-37 X), every candidate i (e_i >= M_e - tol, below) has
+    // f_i >= (1 - 2^-18) M_f - total^2 2^-34, M_f = max f (the argmax of e is a
+    // candidate itself, so M_e is the maximum over the kept splits).  Bins
+    // with a count but no split (w0 or w1 = 0) have X = 0 exactly; empty bins
+    // none (-1).
+    float fe[8];
+    uint32_t cls0 = 0, cls2 = 0;  // splits with X = 0 exactly / with an estimate
+    long long dds[8];
+    uint32_t ps[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const uint32_t w0 = pcu + cnt[q];
         const uint32_t w1 = total_u - w0;
-        double e = ((nz >> q) & 1u) ? 0.0 : -1.0;
-        if (((nz >> q) & 1u) && w0 > 0u && w1 > 0u) {
-            const uint32_t s0 = psu + wsum[q];
-            const uint32_t s1 = sum_all_u - s0;
-            const long long dd = static_cast<long long>(s0) * w1 - static_cast<long long>(s1) * w0;
-            const double d = static_cast<double>(dd);
-            const double p = static_cast<double>(w0 * w1);
-            e = __dmul_rn(__dmul_rn(d, d), rcp_newton(p));
+        const uint32_t s0 = psu + wsum[q];
+        const uint32_t s1 = sum_all_u - s0;
+        dds[q] = static_cast<long long>(s0) * w1 - static_cast<long long>(s1) * w0;
+        ps[q] = w0 * w1;
+        fe[q] = 0.0f;
+        if ((nz >> q) & 1u) {
+            if (w0 > 0u && w1 > 0u) {
+                const float df = __ll2float_rn(dds[q]);
+                float r;
+                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__uint2float_rn(ps[q])));
+                fe[q] = __fmul_rn(__fmul_rn(df, df), r);
+                cls2 |= 1u << q;
+            } else {
+                cls0 |= 1u << q;
+            }
+        }
+    }
+    float mfl = 0.0f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) mfl = fmaxf(mfl, fe[q]);
+    const float mf = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(mfl)));  // f >= 0: bit order
+    const double thr = static_cast<double>(mf) * (1.0 - 0x1p-17) - total * total * 0x1p-33;  // 2x margins
+    uint32_t kept = cls0 & (thr <= 0.0 ? 0xffu : 0u);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) kept |= ((cls2 >> q) & 1u) && static_cast<double>(fe[q]) >= thr ? (1u << q) : 0u;
+
+    double est[8];
+    double m = -1.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        double e = -1.0;
+        if (__any_sync(0xffffffffu, (kept >> q) & 1u)) {  // nearly always one or two q of the eight
+            if ((kept >> q) & 1u) {
+                e = 0.0;
+                if ((cls2 >> q) & 1u) {
+                    const double d = static_cast<double>(dds[q]);
+                    e = __dmul_rn(__dmul_rn(d, d), rcp_newton(static_cast<double>(ps[q])));
+                }
+            }
         }
         est[q] = e;
         m = fmax(m, e);
     }
     // warp maximum of the estimates, exactly, by two 32-bit REDUX steps on the
     // bit patterns (order-preserving for the non-negative doubles; the -1
-    // placeholders map to +0, and lane 0's bin 0 always holds an estimate >= 0)
+    // placeholders map to +0; the kept set is never empty)
     {
         const unsigned long long key = m > 0.0 ? static_cast<unsigned long long>(__double_as_longlong(m)) : 0ull;
         const uint32_t khi = static_cast<uint32_t>(key >> 32);
@@ -439,6 +481,10 @@ cudaError_t binarize_launch(const BinarizeLaunch& L, cudaStream_t st) {
 // The output byte (8 mask bits) lands in the bit-packed mask word in place
 // (little-endian: byte g of word w = columns 32w + 8g .. +7).
 constexpr int kTileCols = 8;
+// tile histograms: 260 words per column (a multiple of 4, so Otsu reads each
+// lane's 8 bins as two 128-bit loads); an atomic instruction's lanes hit
+// columns q and q + 4 (banks 16 apart for the same bin)
+constexpr int kTileHistStride = 260;
 constexpr int kTileMaxRows = 6144;
 constexpr int kBox = 256;  // rows per TMA box (the box-dimension limit)
 static_assert(kTileMaxRows % kBox == 0, "whole boxes");
@@ -465,8 +511,8 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     static_assert(NSPLIT == 1 || NSPLIT == 2, "pairs: the partner is rank ^ 1");
     extern __shared__ __align__(128) float bt_vals[];     // (rows / NSPLIT, rounded up to kBox) x 8
     __shared__ __align__(8) uint64_t box_bar[kTileMaxRows / kBox];
-    __shared__ uint32_t hist[kTileCols * kHistStride];
-    __shared__ uint32_t hist_peer[NSPLIT > 1 ? kTileCols * kHistStride : 1];  // the partner's partials
+    __shared__ __align__(16) uint32_t hist[kTileCols * kTileHistStride];
+    __shared__ __align__(16) uint32_t hist_peer[NSPLIT > 1 ? kTileCols * kTileHistStride : 4];  // the partner's partials
     __shared__ float s_lo[kBinWarps][kTileCols], s_hi[kBinWarps][kTileCols];
     __shared__ float part_lo[kTileCols], part_hi[kTileCols], peer_lo[kTileCols], peer_hi[kTileCols];
     __shared__ float c_lo[kTileCols], c_scale[kTileCols], c_thr[kTileCols];
@@ -516,7 +562,7 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     // extremes supplied by the fused K1 (exact: order-free min / max of the
     // same floats): no min / max sweep, and each box is binned as it lands
     const bool ext = a.col_lo != nullptr;
-    for (int i = tid; i < kTileCols * kHistStride; i += kBinThreads) hist[i] = 0;
+    for (int i = tid; i < kTileCols * kTileHistStride; i += kBinThreads) hist[i] = 0;
     if (ext && tid < kTileCols) {
         const long long ci = static_cast<long long>(p) * cols + col0 + tid;
         set_col(a.col_lo[ci], a.col_hi[ci]);
@@ -613,7 +659,7 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
                 const int cc = 4 * hh + q;
                 clo[q] = c_lo[cc];
                 csc[q] = c_scale[cc];
-                hc[q] = hist + cc * kHistStride;
+                hc[q] = hist + cc * kTileHistStride;
                 any |= c_use[cc] != 0;
             }
             if (any) {
@@ -647,7 +693,7 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
             const int cc = 4 * hh + q;
             clo[q] = c_lo[cc];
             csc[q] = c_scale[cc];
-            hc[q] = hist + cc * kHistStride;
+            hc[q] = hist + cc * kTileHistStride;
             any |= c_use[cc] != 0;
         }
         for (int b = 0; b < nbox; ++b) {
@@ -676,17 +722,23 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     if constexpr (NSPLIT > 1) {
         cg::cluster_group cl = cg::this_cluster();
         uint32_t* peer = cl.map_shared_rank(hist_peer, rank ^ 1);
-        for (int i = tid; i < kTileCols * kHistStride; i += kBinThreads) peer[i] = hist[i];
+        for (int i = tid; i < kTileCols * kTileHistStride; i += kBinThreads) peer[i] = hist[i];
         cl.sync();
     }
     if (warp < kTileCols && c_use[warp]) {
         const int cc = warp;
         uint32_t hq[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) hq[q] = hist[cc * kHistStride + lane * 8 + q];
+        {
+            const uint4* h4 = reinterpret_cast<const uint4*>(hist + cc * kTileHistStride + lane * 8);
+            const uint4 a0 = h4[0], a1 = h4[1];
+            hq[0] = a0.x; hq[1] = a0.y; hq[2] = a0.z; hq[3] = a0.w;
+            hq[4] = a1.x; hq[5] = a1.y; hq[6] = a1.z; hq[7] = a1.w;
+        }
         if constexpr (NSPLIT > 1) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) hq[q] += hist_peer[cc * kHistStride + lane * 8 + q];
+            const uint4* h4 = reinterpret_cast<const uint4*>(hist_peer + cc * kTileHistStride + lane * 8);
+            const uint4 a0 = h4[0], a1 = h4[1];
+            hq[0] += a0.x; hq[1] += a0.y; hq[2] += a0.z; hq[3] += a0.w;
+            hq[4] += a1.x; hq[5] += a1.y; hq[6] += a1.z; hq[7] += a1.w;
         }
         const int best_i = otsu_split_warp_u32(hq, lane);
         if (lane == 0) {
