@@ -416,7 +416,8 @@ __global__ void __launch_bounds__(kBinThreads) binarize_kernel(BinarizeLaunch a)
         const int best_i = otsu_split_warp(hq, lane);
         if (lane == 0) {
             const double lod = static_cast<double>(c_lo[c]);
-            const double e = __ddiv_rn(__dmul_rn(static_cast<double>(best_i) + 1.0, c_span[c]), 256.0);
+            // /256 as *2^-8: the same correctly rounded value (a power of two), no DDIV
+            const double e = __dmul_rn(__dmul_rn(static_cast<double>(best_i) + 1.0, c_span[c]), 0x1p-8);
             c_thr[c] = __double2float_rn(__dadd_rn(lod, e));
         }
     }
@@ -743,7 +744,8 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
         const int best_i = otsu_split_warp_u32(hq, lane);
         if (lane == 0) {
             const double lod = static_cast<double>(c_lo[cc]);
-            const double e = __ddiv_rn(__dmul_rn(static_cast<double>(best_i) + 1.0, c_span[cc]), 256.0);
+            // /256 as *2^-8: the same correctly rounded value (a power of two), no DDIV
+            const double e = __dmul_rn(__dmul_rn(static_cast<double>(best_i) + 1.0, c_span[cc]), 0x1p-8);
             c_thr[cc] = __double2float_rn(__dadd_rn(lod, e));
         }
     }
