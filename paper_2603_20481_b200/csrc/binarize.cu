@@ -520,137 +520,174 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
     __shared__ double c_span[kTileCols];
     __shared__ int c_use[kTileCols];
 
-    const int grp = blockIdx.x / NSPLIT;  // 8-column group
-    const int rank = NSPLIT == 1 ? 0 : static_cast<int>(cg::this_cluster().block_rank());
-    const int p = blockIdx.y;
-    const int rows_all = a.rows, cols = a.cols;
-    const int half = (rows_all + NSPLIT - 1) / NSPLIT;
-    const int rbase = rank * half;
-    const int rows = max(0, min(rows_all, rbase + half) - rbase);  // this CTA's rows
-    const int W = (cols + 31) / 32;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t abyte = (a.active_bits[static_cast<long long>(p) * W + grp / 4] >> (8 * (grp & 3))) & 0xffu;
-    // byte (grp & 3) of the word-major mask words (grp >> 2, r): the tile path
-    // writes the packed mask K5 reads, 4 bytes apart per row
-    uint8_t* plane = a.mask_bytes + ((static_cast<long long>(p) * W + (grp >> 2)) * mask_rs(rows_all) + rbase) * 4 + (grp & 3);
-    const int col0 = grp * kTileCols;
-    if (abyte == 0) {  // both CTAs of a cluster see the same byte and leave together
-        if (!a.skip_empty)
-            for (int r = tid; r < rows; r += kBinThreads) plane[4 * r] = 0;
-        return;
-    }
-    // ---- load the block: one TMA box per kBox rows (32 B x kBox), each on its
-    // own mbarrier, so sweep A starts on the first box while the rest land
-    const int nbox = (rows + kBox - 1) / kBox;
-    if (tid < nbox) {  // thread b issues box b: the boxes leave in parallel
-        mbar_init(&box_bar[tid], 1);
-        fence_mbar_init();
-        mbar_arrive_expect_tx(&box_bar[tid], kBox * kTileCols * sizeof(float));
-        tma_load_box(bt_vals + tid * kBox * kTileCols, &tmap, col0, rbase + tid * kBox, p, &box_bar[tid]);
-    }
-    // per-column binning constants from the column extremes (bin_of,
-    // detector.cpp:28-39); thread tid < 8 owns column col0 + tid
-    auto set_col = [&](float l, float h) {
-        const float scale = __fdiv_rn(256.0f, __fsub_rn(h, l));
-        const bool valid = h > l && isfinite(scale);
-        const bool act = (col0 + tid < cols) && ((abyte >> tid) & 1u);
-        c_lo[tid] = l;
-        c_scale[tid] = scale;
-        c_span[tid] = __dsub_rn(static_cast<double>(h), static_cast<double>(l));
-        c_use[tid] = (act && valid) ? 1 : 0;
-        c_thr[tid] = INFINITY;
-    };
-    // extremes supplied by the fused K1 (exact: order-free min / max of the
-    // same floats): no min / max sweep, and each box is binned as it lands
-    const bool ext = a.col_lo != nullptr;
-    for (int i = tid; i < kTileCols * kTileHistStride; i += kBinThreads) hist[i] = 0;
-    if (ext && tid < kTileCols) {
-        const long long ci = static_cast<long long>(p) * cols + col0 + tid;
-        set_col(a.col_lo[ci], a.col_hi[ci]);
-    }
-    __syncthreads();  // mbarrier init (+ the constants) visible
+    // one column group of plot p; par = this CTA's use count of the box
+    // barriers (parity), first = initialise them
+    auto run_group = [&](int p, int grp, uint32_t par, bool first) {
+        const int rank = NSPLIT == 1 ? 0 : static_cast<int>(cg::this_cluster().block_rank());
+        const int rows_all = a.rows, cols = a.cols;
+        const int half = (rows_all + NSPLIT - 1) / NSPLIT;
+        const int rbase = rank * half;
+        const int rows = max(0, min(rows_all, rbase + half) - rbase);  // this CTA's rows
+        const int W = (cols + 31) / 32;
+        const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+        const uint32_t abyte = (a.active_bits[static_cast<long long>(p) * W + grp / 4] >> (8 * (grp & 3))) & 0xffu;
+        // byte (grp & 3) of the word-major mask words (grp >> 2, r): the tile path
+        // writes the packed mask K5 reads, 4 bytes apart per row
+        uint8_t* plane = a.mask_bytes + ((static_cast<long long>(p) * W + (grp >> 2)) * mask_rs(rows_all) + rbase) * 4 + (grp & 3);
+        const int col0 = grp * kTileCols;
+        if (abyte == 0) {  // both CTAs of a cluster see the same byte and leave together
+            if (!a.skip_empty)
+                for (int r = tid; r < rows; r += kBinThreads) plane[4 * r] = 0;
+            return;
+        }
+        // ---- load the block: one TMA box per kBox rows (32 B x kBox), each on its
+        // own mbarrier, so sweep A starts on the first box while the rest land
+        const int nbox = (rows + kBox - 1) / kBox;
+        if (tid < nbox) {  // thread b issues box b: the boxes leave in parallel
+            if (first) {  // persistent CTAs reuse the barriers: one phase per group
+                mbar_init(&box_bar[tid], 1);
+                fence_mbar_init();
+            }
+            mbar_arrive_expect_tx(&box_bar[tid], kBox * kTileCols * sizeof(float));
+            tma_load_box(bt_vals + tid * kBox * kTileCols, &tmap, col0, rbase + tid * kBox, p, &box_bar[tid]);
+        }
+        // per-column binning constants from the column extremes (bin_of,
+        // detector.cpp:28-39); thread tid < 8 owns column col0 + tid
+        auto set_col = [&](float l, float h) {
+            const float scale = __fdiv_rn(256.0f, __fsub_rn(h, l));
+            const bool valid = h > l && isfinite(scale);
+            const bool act = (col0 + tid < cols) && ((abyte >> tid) & 1u);
+            c_lo[tid] = l;
+            c_scale[tid] = scale;
+            c_span[tid] = __dsub_rn(static_cast<double>(h), static_cast<double>(l));
+            c_use[tid] = (act && valid) ? 1 : 0;
+            c_thr[tid] = INFINITY;
+        };
+        // extremes supplied by the fused K1 (exact: order-free min / max of the
+        // same floats): no min / max sweep, and each box is binned as it lands
+        const bool ext = a.col_lo != nullptr;
+        for (int i = tid; i < kTileCols * kTileHistStride; i += kBinThreads) hist[i] = 0;
+        if (ext && tid < kTileCols) {
+            const long long ci = static_cast<long long>(p) * cols + col0 + tid;
+            set_col(a.col_lo[ci], a.col_hi[ci]);
+        }
+        __syncthreads();  // mbarrier init (+ the constants) visible
 
-    if (!ext) {
-        // ---- sweep A: two threads per row, one float4 (4 columns) each; fminf /
-        // fmaxf equal std::min / std::max here (NaN is never taken by either, and
-        // the sign of a zero extreme never reaches an output)
-        {
-            const int hh = tid & 1;
-            float lo4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
-            float hi4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-            // exactly two rows of each box per thread, branch-free: rows past the
-            // CTA's last row re-read that row (a repeated value changes no extreme)
-            static_assert(kBox == 2 * (kBinThreads / 2), "two rows of a box per thread");
-            const int last = rows - 1;
-            for (int b = 0; b < nbox; ++b) {
-                mbar_wait(&box_bar[b], 0);
-                const int r0 = min(b * kBox + (tid >> 1), last);
-                const int r1 = min(b * kBox + kBinThreads / 2 + (tid >> 1), last);
-                const float4 x = *reinterpret_cast<const float4*>(bt_vals + r0 * kTileCols + 4 * hh);
-                const float4 y = *reinterpret_cast<const float4*>(bt_vals + r1 * kTileCols + 4 * hh);
-                lo4[0] = fminf(lo4[0], fminf(x.x, y.x)); hi4[0] = fmaxf(hi4[0], fmaxf(x.x, y.x));
-                lo4[1] = fminf(lo4[1], fminf(x.y, y.y)); hi4[1] = fmaxf(hi4[1], fmaxf(x.y, y.y));
-                lo4[2] = fminf(lo4[2], fminf(x.z, y.z)); hi4[2] = fmaxf(hi4[2], fmaxf(x.z, y.z));
-                lo4[3] = fminf(lo4[3], fminf(x.w, y.w)); hi4[3] = fmaxf(hi4[3], fmaxf(x.w, y.w));
-            }
-    #pragma unroll
-            for (int o = 2; o < 32; o <<= 1)
-    #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    lo4[q] = fminf(lo4[q], __shfl_xor_sync(0xffffffffu, lo4[q], o));
-                    hi4[q] = fmaxf(hi4[q], __shfl_xor_sync(0xffffffffu, hi4[q], o));
+        if (!ext) {
+            // ---- sweep A: two threads per row, one float4 (4 columns) each; fminf /
+            // fmaxf equal std::min / std::max here (NaN is never taken by either, and
+            // the sign of a zero extreme never reaches an output)
+            {
+                const int hh = tid & 1;
+                float lo4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+                float hi4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+                // exactly two rows of each box per thread, branch-free: rows past the
+                // CTA's last row re-read that row (a repeated value changes no extreme)
+                static_assert(kBox == 2 * (kBinThreads / 2), "two rows of a box per thread");
+                const int last = rows - 1;
+                for (int b = 0; b < nbox; ++b) {
+                    mbar_wait(&box_bar[b], par);
+                    const int r0 = min(b * kBox + (tid >> 1), last);
+                    const int r1 = min(b * kBox + kBinThreads / 2 + (tid >> 1), last);
+                    const float4 x = *reinterpret_cast<const float4*>(bt_vals + r0 * kTileCols + 4 * hh);
+                    const float4 y = *reinterpret_cast<const float4*>(bt_vals + r1 * kTileCols + 4 * hh);
+                    lo4[0] = fminf(lo4[0], fminf(x.x, y.x)); hi4[0] = fmaxf(hi4[0], fmaxf(x.x, y.x));
+                    lo4[1] = fminf(lo4[1], fminf(x.y, y.y)); hi4[1] = fmaxf(hi4[1], fmaxf(x.y, y.y));
+                    lo4[2] = fminf(lo4[2], fminf(x.z, y.z)); hi4[2] = fmaxf(hi4[2], fmaxf(x.z, y.z));
+                    lo4[3] = fminf(lo4[3], fminf(x.w, y.w)); hi4[3] = fmaxf(hi4[3], fmaxf(x.w, y.w));
                 }
-            if (lane < 2) {
-    #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    s_lo[warp][4 * lane + q] = lo4[q];
-                    s_hi[warp][4 * lane + q] = hi4[q];
+        #pragma unroll
+                for (int o = 2; o < 32; o <<= 1)
+        #pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        lo4[q] = fminf(lo4[q], __shfl_xor_sync(0xffffffffu, lo4[q], o));
+                        hi4[q] = fmaxf(hi4[q], __shfl_xor_sync(0xffffffffu, hi4[q], o));
+                    }
+                if (lane < 2) {
+        #pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        s_lo[warp][4 * lane + q] = lo4[q];
+                        s_hi[warp][4 * lane + q] = hi4[q];
+                    }
                 }
             }
-        }
-        __syncthreads();
-        if constexpr (NSPLIT > 1) {
-            if (tid < kTileCols) {
-                float l = s_lo[0][tid], h = s_hi[0][tid];
-                for (int q = 1; q < kBinWarps; ++q) {
-                    l = fminf(l, s_lo[q][tid]);
-                    h = fmaxf(h, s_hi[q][tid]);
-                }
-                part_lo[tid] = l;
-                part_hi[tid] = h;
-                // push into the partner too (peer slot): after the barrier both
-                // read only local shared memory
-                cg::cluster_group cl = cg::this_cluster();
-                *cl.map_shared_rank(&peer_lo[tid], rank ^ 1) = l;
-                *cl.map_shared_rank(&peer_hi[tid], rank ^ 1) = h;
-            }
-            cg::this_cluster().sync();
-        }
-        if (tid < kTileCols) {
-            float l, h;
+            __syncthreads();
             if constexpr (NSPLIT > 1) {
-                // min / max are order-free: every CTA of the cluster derives the same extremes
-                l = fminf(part_lo[tid], peer_lo[tid]);
-                h = fmaxf(part_hi[tid], peer_hi[tid]);
-            } else {
-                l = s_lo[0][tid];
-                h = s_hi[0][tid];
-                for (int q = 1; q < kBinWarps; ++q) {
-                    l = fminf(l, s_lo[q][tid]);
-                    h = fmaxf(h, s_hi[q][tid]);
+                if (tid < kTileCols) {
+                    float l = s_lo[0][tid], h = s_hi[0][tid];
+                    for (int q = 1; q < kBinWarps; ++q) {
+                        l = fminf(l, s_lo[q][tid]);
+                        h = fmaxf(h, s_hi[q][tid]);
+                    }
+                    part_lo[tid] = l;
+                    part_hi[tid] = h;
+                    // push into the partner too (peer slot): after the barrier both
+                    // read only local shared memory
+                    cg::cluster_group cl = cg::this_cluster();
+                    *cl.map_shared_rank(&peer_lo[tid], rank ^ 1) = l;
+                    *cl.map_shared_rank(&peer_hi[tid], rank ^ 1) = h;
+                }
+                cg::this_cluster().sync();
+            }
+            if (tid < kTileCols) {
+                float l, h;
+                if constexpr (NSPLIT > 1) {
+                    // min / max are order-free: every CTA of the cluster derives the same extremes
+                    l = fminf(part_lo[tid], peer_lo[tid]);
+                    h = fmaxf(part_hi[tid], peer_hi[tid]);
+                } else {
+                    l = s_lo[0][tid];
+                    h = s_hi[0][tid];
+                    for (int q = 1; q < kBinWarps; ++q) {
+                        l = fminf(l, s_lo[q][tid]);
+                        h = fmaxf(h, s_hi[q][tid]);
+                    }
+                }
+                set_col(l, h);
+            }
+            __syncthreads();
+
+            // ---- sweep B: histograms from shared memory.  Two threads per row, one
+            // float4 (4 columns) each, as in sweep A: one LDS.128 per 4 values and
+            // the per-column constants in registers.  Branch-free: a column that is
+            // not binarised (inactive or constant) still counts into its own
+            // histogram (bin_index stays in [0, 255] for any input), which Otsu then
+            // ignores
+            {
+                const int hh = tid & 1;
+                float clo[4], csc[4];
+                uint32_t* hc[4];
+                bool any = false;
+        #pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int cc = 4 * hh + q;
+                    clo[q] = c_lo[cc];
+                    csc[q] = c_scale[cc];
+                    hc[q] = hist + cc * kTileHistStride;
+                    any |= c_use[cc] != 0;
+                }
+                if (any) {
+                    constexpr int RS = kBinThreads / 2;  // row stride
+                    int r = tid >> 1;
+                    for (; r + RS < rows; r += 2 * RS) {
+                        const float4 x0 = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols + 4 * hh);
+                        const float4 x1 = *reinterpret_cast<const float4*>(bt_vals + (r + RS) * kTileCols + 4 * hh);
+                        const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        #pragma unroll
+                        for (int q = 0; q < 8; ++q) atomicAdd(hc[q & 3] + bin_index(xv[q], clo[q & 3], csc[q & 3]), 1u);
+                    }
+                    if (r < rows) {
+                        const float4 x0 = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols + 4 * hh);
+                        const float xv[4] = {x0.x, x0.y, x0.z, x0.w};
+        #pragma unroll
+                        for (int q = 0; q < 4; ++q) atomicAdd(hc[q] + bin_index(xv[q], clo[q], csc[q]), 1u);
+                    }
                 }
             }
-            set_col(l, h);
-        }
-        __syncthreads();
-
-        // ---- sweep B: histograms from shared memory.  Two threads per row, one
-        // float4 (4 columns) each, as in sweep A: one LDS.128 per 4 values and
-        // the per-column constants in registers.  Branch-free: a column that is
-        // not binarised (inactive or constant) still counts into its own
-        // histogram (bin_index stays in [0, 255] for any input), which Otsu then
-        // ignores
-        {
+        } else {
+            // ---- sweep B, streaming: two rows of each box per thread (one float4
+            // of 4 columns each) as soon as the box lands; every thread waits for
+            // every box, since sweep C reads them all
             const int hh = tid & 1;
             float clo[4], csc[4];
             uint32_t* hc[4];
@@ -663,108 +700,92 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
                 hc[q] = hist + cc * kTileHistStride;
                 any |= c_use[cc] != 0;
             }
-            if (any) {
-                constexpr int RS = kBinThreads / 2;  // row stride
-                int r = tid >> 1;
-                for (; r + RS < rows; r += 2 * RS) {
-                    const float4 x0 = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols + 4 * hh);
-                    const float4 x1 = *reinterpret_cast<const float4*>(bt_vals + (r + RS) * kTileCols + 4 * hh);
-                    const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+            for (int b = 0; b < nbox; ++b) {
+                mbar_wait(&box_bar[b], par);
+                const int ra = b * kBox + (tid >> 1), rb = ra + kBinThreads / 2;
+                if (any && ra < rows) {
+                    const float4 x = *reinterpret_cast<const float4*>(bt_vals + ra * kTileCols + 4 * hh);
+                    const float xv[4] = {x.x, x.y, x.z, x.w};
     #pragma unroll
-                    for (int q = 0; q < 8; ++q) atomicAdd(hc[q & 3] + bin_index(xv[q], clo[q & 3], csc[q & 3]), 1u);
+                    for (int q = 0; q < 4; ++q) atomicAdd(hc[q] + bin_index(xv[q], clo[q], csc[q]), 1u);
                 }
-                if (r < rows) {
-                    const float4 x0 = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols + 4 * hh);
-                    const float xv[4] = {x0.x, x0.y, x0.z, x0.w};
+                if (any && rb < rows) {
+                    const float4 x = *reinterpret_cast<const float4*>(bt_vals + rb * kTileCols + 4 * hh);
+                    const float xv[4] = {x.x, x.y, x.z, x.w};
     #pragma unroll
                     for (int q = 0; q < 4; ++q) atomicAdd(hc[q] + bin_index(xv[q], clo[q], csc[q]), 1u);
                 }
             }
         }
-    } else {
-        // ---- sweep B, streaming: two rows of each box per thread (one float4
-        // of 4 columns each) as soon as the box lands; every thread waits for
-        // every box, since sweep C reads them all
-        const int hh = tid & 1;
-        float clo[4], csc[4];
-        uint32_t* hc[4];
-        bool any = false;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int cc = 4 * hh + q;
-            clo[q] = c_lo[cc];
-            csc[q] = c_scale[cc];
-            hc[q] = hist + cc * kTileHistStride;
-            any |= c_use[cc] != 0;
-        }
-        for (int b = 0; b < nbox; ++b) {
-            mbar_wait(&box_bar[b], 0);
-            const int ra = b * kBox + (tid >> 1), rb = ra + kBinThreads / 2;
-            if (any && ra < rows) {
-                const float4 x = *reinterpret_cast<const float4*>(bt_vals + ra * kTileCols + 4 * hh);
-                const float xv[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) atomicAdd(hc[q] + bin_index(xv[q], clo[q], csc[q]), 1u);
-            }
-            if (any && rb < rows) {
-                const float4 x = *reinterpret_cast<const float4*>(bt_vals + rb * kTileCols + 4 * hh);
-                const float xv[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) atomicAdd(hc[q] + bin_index(xv[q], clo[q], csc[q]), 1u);
-            }
-        }
-    }
-    __syncthreads();
+        __syncthreads();
 
-    // cluster: each CTA pushes its partial histograms into its partner's
-    // hist_peer (DSMEM stores) before the one barrier; afterwards both hold
-    // the full histograms locally, run all 8 Otsu splits themselves and touch
-    // no remote memory again, so no second barrier is needed
-    if constexpr (NSPLIT > 1) {
-        cg::cluster_group cl = cg::this_cluster();
-        uint32_t* peer = cl.map_shared_rank(hist_peer, rank ^ 1);
-        for (int i = tid; i < kTileCols * kTileHistStride; i += kBinThreads) peer[i] = hist[i];
-        cl.sync();
-    }
-    if (warp < kTileCols && c_use[warp]) {
-        const int cc = warp;
-        uint32_t hq[8];
-        {
-            const uint4* h4 = reinterpret_cast<const uint4*>(hist + cc * kTileHistStride + lane * 8);
-            const uint4 a0 = h4[0], a1 = h4[1];
-            hq[0] = a0.x; hq[1] = a0.y; hq[2] = a0.z; hq[3] = a0.w;
-            hq[4] = a1.x; hq[5] = a1.y; hq[6] = a1.z; hq[7] = a1.w;
-        }
+        // cluster: each CTA pushes its partial histograms into its partner's
+        // hist_peer (DSMEM stores) before the one barrier; afterwards both hold
+        // the full histograms locally, run all 8 Otsu splits themselves and touch
+        // no remote memory again, so no second barrier is needed
         if constexpr (NSPLIT > 1) {
-            const uint4* h4 = reinterpret_cast<const uint4*>(hist_peer + cc * kTileHistStride + lane * 8);
-            const uint4 a0 = h4[0], a1 = h4[1];
-            hq[0] += a0.x; hq[1] += a0.y; hq[2] += a0.z; hq[3] += a0.w;
-            hq[4] += a1.x; hq[5] += a1.y; hq[6] += a1.z; hq[7] += a1.w;
+            cg::cluster_group cl = cg::this_cluster();
+            uint32_t* peer = cl.map_shared_rank(hist_peer, rank ^ 1);
+            for (int i = tid; i < kTileCols * kTileHistStride; i += kBinThreads) peer[i] = hist[i];
+            cl.sync();
         }
-        const int best_i = otsu_split_warp_u32(hq, lane);
-        if (lane == 0) {
-            const double lod = static_cast<double>(c_lo[cc]);
-            // /256 as *2^-8: the same correctly rounded value (a power of two), no DDIV
-            const double e = __dmul_rn(__dmul_rn(static_cast<double>(best_i) + 1.0, c_span[cc]), 0x1p-8);
-            c_thr[cc] = __double2float_rn(__dadd_rn(lod, e));
+        if (warp < kTileCols && c_use[warp]) {
+            const int cc = warp;
+            uint32_t hq[8];
+            {
+                const uint4* h4 = reinterpret_cast<const uint4*>(hist + cc * kTileHistStride + lane * 8);
+                const uint4 a0 = h4[0], a1 = h4[1];
+                hq[0] = a0.x; hq[1] = a0.y; hq[2] = a0.z; hq[3] = a0.w;
+                hq[4] = a1.x; hq[5] = a1.y; hq[6] = a1.z; hq[7] = a1.w;
+            }
+            if constexpr (NSPLIT > 1) {
+                const uint4* h4 = reinterpret_cast<const uint4*>(hist_peer + cc * kTileHistStride + lane * 8);
+                const uint4 a0 = h4[0], a1 = h4[1];
+                hq[0] += a0.x; hq[1] += a0.y; hq[2] += a0.z; hq[3] += a0.w;
+                hq[4] += a1.x; hq[5] += a1.y; hq[6] += a1.z; hq[7] += a1.w;
+            }
+            const int best_i = otsu_split_warp_u32(hq, lane);
+            if (lane == 0) {
+                const double lod = static_cast<double>(c_lo[cc]);
+                // /256 as *2^-8: the same correctly rounded value (a power of two), no DDIV
+                const double e = __dmul_rn(__dmul_rn(static_cast<double>(best_i) + 1.0, c_span[cc]), 0x1p-8);
+                c_thr[cc] = __double2float_rn(__dadd_rn(lod, e));
+            }
         }
-    }
-    __syncthreads();
-    if (a.col_thr && tid < kTileCols && col0 + tid < cols && rank == 0)
-        a.col_thr[static_cast<long long>(p) * cols + col0 + tid] = c_thr[tid];
+        __syncthreads();
+        if (a.col_thr && tid < kTileCols && col0 + tid < cols && rank == 0)
+            a.col_thr[static_cast<long long>(p) * cols + col0 + tid] = c_thr[tid];
 
-    // ---- sweep C: one row per thread, 8 compares -> one mask byte
-    float thr[kTileCols];
-#pragma unroll
-    for (int q = 0; q < kTileCols; ++q) thr[q] = c_thr[q];
-    for (int r = tid; r < rows; r += kBinThreads) {
-        const float4 x0 = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols);
-        const float4 x1 = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols + 4);
-        const uint32_t b = (x0.x > thr[0] ? 1u : 0u) | (x0.y > thr[1] ? 2u : 0u) | (x0.z > thr[2] ? 4u : 0u) |
-                           (x0.w > thr[3] ? 8u : 0u) | (x1.x > thr[4] ? 16u : 0u) | (x1.y > thr[5] ? 32u : 0u) |
-                           (x1.z > thr[6] ? 64u : 0u) | (x1.w > thr[7] ? 128u : 0u);
-        plane[4 * r] = static_cast<uint8_t>(b);
+        // ---- sweep C: one row per thread, 8 compares -> one mask byte
+        float thr[kTileCols];
+    #pragma unroll
+        for (int q = 0; q < kTileCols; ++q) thr[q] = c_thr[q];
+        for (int r = tid; r < rows; r += kBinThreads) {
+            const float4 x0 = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols);
+            const float4 x1 = *reinterpret_cast<const float4*>(bt_vals + r * kTileCols + 4);
+            const uint32_t b = (x0.x > thr[0] ? 1u : 0u) | (x0.y > thr[1] ? 2u : 0u) | (x0.z > thr[2] ? 4u : 0u) |
+                               (x0.w > thr[3] ? 8u : 0u) | (x1.x > thr[4] ? 16u : 0u) | (x1.y > thr[5] ? 32u : 0u) |
+                               (x1.z > thr[6] ? 64u : 0u) | (x1.w > thr[7] ? 128u : 0u);
+            plane[4 * r] = static_cast<uint8_t>(b);
+        }
+    };
+    if constexpr (NSPLIT == 1) {
+        if (a.group_list) {
+            // persistent: the CTA walks the active column groups (K3's list, in
+            // plot and group order), so empty groups cost no CTA at all
+            const int G = a.cols / kTileCols;
+            const int count = *a.group_count;
+            uint32_t par = 0;
+            for (int it = blockIdx.x; it < count; it += gridDim.x) {
+                const int e = a.group_list[it];
+                run_group(e / G, e % G, par, it == static_cast<int>(blockIdx.x));
+                par ^= 1u;
+                __syncthreads();  // the block buffer and histograms are reused
+            }
+            return;
+        }
     }
+    run_group(blockIdx.y, blockIdx.x / NSPLIT, 0u, true);
 }
 
 // one CTA per column group while its block leaves room for 2 CTAs per SM,
@@ -779,6 +800,8 @@ bool binarize_tile_ok(int rows, int cols) { return cols % 32 == 0 && rows <= 2 *
 // single-CTA form's min / max sweep already hides under its box loads, so
 // there the extremes cost K1 more than they save (C5r: K1 +0.49, K4 -0.43).
 bool binarize_wants_extremes(int rows) { return rows > kTileSplitRows; }
+
+bool binarize_tile_persistent(int rows, int cols) { return binarize_tile_ok(rows, cols) && rows <= kTileSplitRows; }
 
 // The [plots][rows][cols] fp32 TF tensor as a TMA tensor map with 8 x kBox x 1
 // boxes (rows past the end of a plot read as zeros and are never used).
@@ -818,6 +841,14 @@ cudaError_t binarize_tile_launch(const BinarizeLaunch& L, cudaStream_t st) {
     const cudaError_t me = make_tf_map(L, &map);
     if (me != cudaSuccess) return me;
     if (split == 1) {
+        if (L.group_list) {  // persistent: 2 CTAs per SM walk the active groups
+            static int sms[64] = {};
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (!sms[dev & 63]) cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+            binarize_tile_kernel<1><<<2 * sms[dev & 63], kBinThreads, smem, st>>>(L, map);
+            return cudaGetLastError();
+        }
         dim3 grid(L.cols / kTileCols, L.n_plots);
         binarize_tile_kernel<1><<<grid, kBinThreads, smem, st>>>(L, map);
         return cudaGetLastError();

@@ -356,6 +356,16 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
     F.active = out_dev.active ? out_dev.active : act;
     F.n_active = out_dev.n_active ? out_dev.n_active : nact;
     F.active_bits = abits;
+    const bool persistent = ssb::binarize_tile_persistent(rows, cols);
+    int* glist = nullptr;
+    int* gcount = nullptr;
+    if (persistent) {  // K4's work list of active column groups, built by K3
+        SS_WS(gl, int, "det.group_list", static_cast<size_t>(n_plots) * ((cols + 7) / 8));
+        SS_WS(gc, int, "det.group_count", 1);
+        SS_CK(ctx, cudaMemsetAsync(gc, 0, sizeof(int), ctx->stream));
+        glist = F.group_list = gl;
+        gcount = F.group_count = gc;
+    }
     if (ssb::floor_needs_scratch(F.n, F.window)) {
         SS_WS(fscr, float, "floor.scratch", 2 * static_cast<size_t>(F.n_plots) * F.n);
         F.scratch = fscr;
@@ -373,6 +383,8 @@ ss_status detect_device(ss_ctx* ctx, const float* tf, int n_plots, int rows, int
     if (tile) {
         B.col_lo = col_lo;  // column extremes from the fused K1, when it made them
         B.col_hi = col_hi;
+        B.group_list = glist;
+        B.group_count = gcount;
         B.mask_bytes = reinterpret_cast<uint8_t*>(m0);  // the bit mask, written bytewise
         B.skip_empty = true;  // empty column groups stay unwritten; K5 reads them as background
     } else {

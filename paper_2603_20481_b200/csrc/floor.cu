@@ -168,6 +168,32 @@ __global__ void __launch_bounds__(kFloorThreads) floor_kernel(FloorLaunch a) {
             bits[wd] = b;
         }
     }
+    if (a.group_list) {
+        // K4's work list: the plot's 8-column groups with an active column, in
+        // group order, in one block of the batch list reserved by one atomic
+        const int G = (n + 7) / 8;
+        auto active_group = [&](int g) {
+            bool any = false;
+            for (int k = 8 * g; k < min(n, 8 * g + 8); ++k) any |= raw[k] >= thr;
+            return any ? 1 : 0;
+        };
+        int mine = 0;
+        for (int g = tid; g < G; g += nt) mine += active_group(g);
+        int total_g = 0;
+        (void)block_excl_scan(mine, red_i, &total_g);
+        __shared__ int base_s;
+        if (tid == 0) base_s = atomicAdd(a.group_count, total_g);
+        __syncthreads();
+        int base = base_s;
+        for (int g0 = 0; g0 < G; g0 += nt) {
+            const int g = g0 + tid;
+            const int f = g < G ? active_group(g) : 0;
+            int round_total = 0;
+            const int o = block_excl_scan(f, red_i, &round_total);
+            if (f) a.group_list[base + o] = p * G + g;
+            base += round_total;
+        }
+    }
 }
 
 cudaError_t floor_launch(const FloorLaunch& L, cudaStream_t st) {

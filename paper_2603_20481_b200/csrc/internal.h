@@ -59,6 +59,8 @@ struct FloorLaunch {
     int* active = nullptr;        // n_plots x n (compacted, ascending)
     int* n_active = nullptr;      // n_plots
     uint32_t* active_bits = nullptr;  // n_plots x W (W = ceil(n/32)), may be null
+    int* group_list = nullptr;    // optional: p * ceil(n/8) + g for every 8-column group g with an active column
+    int* group_count = nullptr;   // ... appended per plot at *group_count (zeroed by the caller)
     float* scratch = nullptr;     // n_plots x 2n floats: the dB / smoothed rows when they exceed shared memory
 };
 // true when the floor stage needs FloorLaunch::scratch (rows of n floats do not fit shared memory)
@@ -86,6 +88,8 @@ struct BinarizeLaunch {
     int rows = 0;
     int cols = 0;
     const uint32_t* active_bits = nullptr;  // n_plots x W
+    const int* group_list = nullptr;    // optional (single-CTA tile path): the active 8-column groups, p * (cols/8) + g,
+    const int* group_count = nullptr;   // and their count (device): persistent CTAs walk them
     const float* col_lo = nullptr;      // optional n_plots x cols column extremes (from K1): the tile path
     const float* col_hi = nullptr;      // then skips its min / max sweep and bins boxes as they land
     uint32_t* mask_bits = nullptr;      // n_plots x W x rows word-major bits (bit mode) or null
@@ -101,6 +105,8 @@ cudaError_t binarize_launch(const BinarizeLaunch& L, cudaStream_t st);
 bool binarize_tile_ok(int rows, int cols);
 // true when the tile path should take column extremes from the fused K1 (BinarizeLaunch::col_lo)
 bool binarize_wants_extremes(int rows);
+// true when the tile path runs as persistent CTAs over a list of active groups (FloorLaunch::group_list)
+bool binarize_tile_persistent(int rows, int cols);
 
 // ---- K5 morph.cu
 cudaError_t pack_u8_launch(const uint8_t* m, int n_plots, int rows, int cols, uint32_t* bits,
