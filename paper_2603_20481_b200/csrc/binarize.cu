@@ -490,27 +490,7 @@ constexpr int kTileMaxRows = 6144;
 constexpr int kBox = 256;  // rows per TMA box (the box-dimension limit)
 static_assert(kTileMaxRows % kBox == 0, "whole boxes");
 
-// Persistent form: the two CTAs of an SM take turns loading.  A CTA holds its
-// SM's load lock from the issue of a group's TMA boxes until all but
-// K4_LOCK_EARLY of them have landed, so one CTA's loads run under the other's
-// histogram / Otsu / threshold phases instead of both loading, then both
-// computing (measured: the kernel's time was the plain sum of its phases).
-#ifndef K4_LOCK
-#define K4_LOCK 0
-#endif
-#ifndef K4_LOCK_EARLY
-#define K4_LOCK_EARLY 0
-#endif
-
 namespace ssb {
-
-__device__ unsigned int k4_load_lock[256 * 32];  // one 128-byte line per SM; always released
-
-__device__ __forceinline__ unsigned int sm_id() {
-    unsigned int s;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
-    return s;
-}
 
 // TMA tile load of box (8 columns x kBox rows x 1 plot) at (c0, r0, p) of the
 // [plots][rows][cols] fp32 TF tensor, completion counted on `bar`
@@ -528,7 +508,7 @@ __device__ __forceinline__ void tma_load_box(void* dst, const CUtensorMap* map, 
 // pushes its partial histograms into the partner's shared memory before the
 // second (last) cluster barrier, and both run the same Otsu locally.
 template <int NSPLIT>
-__global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaunch a, const __grid_constant__ CUtensorMap tmap) {
+__global__ void __launch_bounds__(kBinThreads, 2) binarize_tile_kernel(BinarizeLaunch a, const __grid_constant__ CUtensorMap tmap) {
     static_assert(NSPLIT == 1 || NSPLIT == 2, "pairs: the partner is rank ^ 1");
     extern __shared__ __align__(128) float bt_vals[];     // (rows / NSPLIT, rounded up to kBox) x 8
     __shared__ __align__(8) uint64_t box_bar[kTileMaxRows / kBox];
@@ -563,18 +543,6 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
         // ---- load the block: one TMA box per kBox rows (32 B x kBox), each on its
         // own mbarrier, so sweep A starts on the first box while the rest land
         const int nbox = (rows + kBox - 1) / kBox;
-        unsigned int* lock = nullptr;
-        if constexpr (K4_LOCK && NSPLIT == 1) {
-            if (a.group_list) {
-                lock = &k4_load_lock[(sm_id() & 255u) * 32u];
-                if (warp == 0) {
-                    if (lane == 0)
-                        while (atomicCAS(lock, 0u, 1u) != 0u) __nanosleep(64);
-                    __syncwarp();
-                }
-            }
-        }
-        const int rel_box = max(0, nbox - 1 - K4_LOCK_EARLY);  // the lock goes when this box has landed
         if (tid < nbox) {  // thread b issues box b: the boxes leave in parallel
             if (first) {  // persistent CTAs reuse the barriers: one phase per group
                 mbar_init(&box_bar[tid], 1);
@@ -619,7 +587,6 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
                 const int last = rows - 1;
                 for (int b = 0; b < nbox; ++b) {
                     mbar_wait(&box_bar[b], par);
-                    if (K4_LOCK && lock && tid == 0 && b == rel_box) atomicExch(lock, 0u);
                     const int r0 = min(b * kBox + (tid >> 1), last);
                     const int r1 = min(b * kBox + kBinThreads / 2 + (tid >> 1), last);
                     const float4 x = *reinterpret_cast<const float4*>(bt_vals + r0 * kTileCols + 4 * hh);
@@ -735,7 +702,6 @@ __global__ void __launch_bounds__(kBinThreads) binarize_tile_kernel(BinarizeLaun
             }
             for (int b = 0; b < nbox; ++b) {
                 mbar_wait(&box_bar[b], par);
-                if (K4_LOCK && lock && tid == 0 && b == rel_box) atomicExch(lock, 0u);
                 const int ra = b * kBox + (tid >> 1), rb = ra + kBinThreads / 2;
                 if (any && ra < rows) {
                     const float4 x = *reinterpret_cast<const float4*>(bt_vals + ra * kTileCols + 4 * hh);

@@ -343,20 +343,36 @@ __device__ __forceinline__ double rsqrt_seed(double x) {
 }
 
 // |X| rounded to float, bit-identical to float(sqrt(fma(re, re, im*im))).
-// Fast path: MUFU.RSQ64H seed (rel. err <= 2^-20, measured) + one Newton
-// step in double gives sqrt(q) within 2^12.6 double ulps; when that estimate
-// is more than 2^16 ulps from a float rounding midpoint (low 29 mantissa bits
-// vs 2^28), rounding it to float equals rounding the correctly rounded double
-// sqrt (no midpoint lies between them); the rounding itself is one
-// F2F.F32.F64 (conversion unit, off the FP64 pipe).  A normal float result
-// also proves q far from the seed's flush range and from overflow.  Otherwise
-// (p ~ 2^-12, or zero / subnormal / huge magnitudes) the IEEE __dsqrt_rn + F2F.
-// Magnitudes of the thread's P outputs, branch-free on the fast path; lanes
-// flagged in the warp-uniform slow pass redo theirs with __dsqrt_rn.
+// Fast path (every point, branch-free): MUFU.RSQ64H seed + one Newton step in
+// double gives sqrt(q) within 11,681 double ulps (bound below); when that
+// estimate is further than kMidMargin ulps from a float rounding midpoint
+// (low 29 mantissa bits vs 2^28), rounding it to float equals rounding the
+// correctly rounded double sqrt -- no midpoint lies between them; the
+// rounding itself is one F2F.F32.F64 (conversion unit, off the FP64 pipe).  A
+// normal float result also proves q far from the seed's flush range and from
+// overflow.  Otherwise (2^-14.4 of the points, or zero / subnormal / huge
+// magnitudes) the warp takes a uniform branch in which the flagged lanes redo
+// theirs with the IEEE __dsqrt_rn + F2F.  That branch delays the whole row
+// group at its next barrier, so its rate matters: with the former 2^16-ulp
+// margin 64 % of the rows had a flagged point and K1 lost 0.9 of 12.9 ms
+// (measured with the branch disabled); a second Newton level ahead of
+// __dsqrt_rn spilled registers in the row loop (14.5 ms).
 // SH: the transform ran on inputs scaled by 2^SH (int16 IQ without its exact
 // 2^-15 decode factor); power-of-two scaling commutes with every rounding of
 // the FFT, so the true magnitude is the computed one times 2^-SH, applied as
 // an exponent offset (fast path) or an exact multiply (slow path).
+//
+// kMidMargin: tools/rsq_probe.cu evaluates the seed on every high word of
+// [1,4) (it depends on the high word only) at both ends of the low word:
+// relative error e <= 2^-20.037, so the Newton estimate is within 1.5 e^2 =
+// 11,680.2 ulps of sqrt(q), + 0.5 for its own rounding (11,589.7 observed);
+// the reference's RN_d(sqrt(q)) is within 0.5 ulp of sqrt(q).  12,288 >
+// 11,681.2, so no float midpoint separates the two.
+#ifndef K1_MID_MARGIN
+#define K1_MID_MARGIN 12288
+#endif
+constexpr uint32_t kMidMargin = K1_MID_MARGIN;
+
 template <int P, int SH>
 __device__ __forceinline__ void mags(const cd* v, float* m) {
     uint32_t slow = 0;
@@ -373,12 +389,10 @@ __device__ __forceinline__ void mags(const cd* v, float* m) {
         const uint32_t hi = static_cast<uint32_t>(__double2hiint(s1));
         const uint32_t lo = static_cast<uint32_t>(__double2loint(s1));
         // float rounding by F2F.F32.F64 (the conversion unit); 2^-SH as an
-        // exponent decrement first.  Fast path valid when the result is a
-        // normal float (q far from the rsqrt seed's flush range, no overflow)
-        // and s1 is > 2^16 ulps from a float rounding midpoint
-        const uint32_t mid = (lo & 0x1FFFFFFFu) + (65536u - (1u << 28));  // > 131072: |dist| > 65536
+        // exponent decrement first
+        const uint32_t mid = (lo & 0x1FFFFFFFu) + (kMidMargin - (1u << 28));  // > 2 * margin: |dist| > margin
         const float mf = __double2float_rn(SH ? __hiloint2double(static_cast<int>(hi - (SH << 20)), static_cast<int>(lo)) : s1);
-        const bool ok = (__float_as_uint(mf) - 0x00800000u) < (0x7f800000u - 0x00800000u) && mid > 131072u;
+        const bool ok = (__float_as_uint(mf) - 0x00800000u) < (0x7f800000u - 0x00800000u) && mid > 2u * kMidMargin;
         m[i] = mf;
         slow |= ok ? 0u : (1u << i);
     }
