@@ -350,7 +350,7 @@ __device__ __forceinline__ double rsqrt_seed(double x) {
 // correctly rounded double sqrt -- no midpoint lies between them; the
 // rounding itself is one F2F.F32.F64 (conversion unit, off the FP64 pipe).  A
 // normal float result also proves q far from the seed's flush range and from
-// overflow.  Otherwise (2^-14.4 of the points, or zero / subnormal / huge
+// overflow.  Otherwise (2^-15.4 of the points, or zero / subnormal / huge
 // magnitudes) the warp takes a uniform branch in which the flagged lanes redo
 // theirs with the IEEE __dsqrt_rn + F2F.  That branch delays the whole row
 // group at its next barrier, so its rate matters: with the former 2^16-ulp
@@ -366,12 +366,17 @@ __device__ __forceinline__ double rsqrt_seed(double x) {
 // [1,4) (it depends on the high word only) at both ends of the low word:
 // relative error e <= 2^-20.037, so the Newton estimate is within 1.5 e^2 =
 // 11,680.2 ulps of sqrt(q), + 0.5 for its own rounding (11,589.7 observed);
-// the reference's RN_d(sqrt(q)) is within 0.5 ulp of sqrt(q).  12,288 >
-// 11,681.2, so no float midpoint separates the two.
+// the reference's s = RN_d(sqrt(q)) is within 0.5 ulp of sqrt(q).  The Newton
+// error is one-sided: s1 - sqrt(q) = -sqrt(q) (1.5 e^2 + 2 e d1 + ..), d1 the
+// 2^-53 rounding of s0, so s1 exceeds sqrt(q) by at most its own rounding
+// (probe: +0.5 ulp) and s - s1 lies in [-1.01, 11,681.7].  A float midpoint m
+// can separate s1 from s, or equal s, only if m - s1 is in that interval: a
+// point is flagged iff m - s1 is in [-kMidAbove, kMidMargin] = [-4, 12288].
 #ifndef K1_MID_MARGIN
 #define K1_MID_MARGIN 12288
 #endif
 constexpr uint32_t kMidMargin = K1_MID_MARGIN;
+constexpr uint32_t kMidAbove = 4;
 
 template <int P, int SH>
 __device__ __forceinline__ void mags(const cd* v, float* m) {
@@ -390,9 +395,10 @@ __device__ __forceinline__ void mags(const cd* v, float* m) {
         const uint32_t lo = static_cast<uint32_t>(__double2loint(s1));
         // float rounding by F2F.F32.F64 (the conversion unit); 2^-SH as an
         // exponent decrement first
-        const uint32_t mid = (lo & 0x1FFFFFFFu) + (kMidMargin - (1u << 28));  // > 2 * margin: |dist| > margin
+        // dist = low 29 bits - 2^28 (ulps from the midpoint); flagged iff -margin <= dist <= above
+        const uint32_t mid = (lo & 0x1FFFFFFFu) + (kMidMargin - (1u << 28));
         const float mf = __double2float_rn(SH ? __hiloint2double(static_cast<int>(hi - (SH << 20)), static_cast<int>(lo)) : s1);
-        const bool ok = (__float_as_uint(mf) - 0x00800000u) < (0x7f800000u - 0x00800000u) && mid > 2u * kMidMargin;
+        const bool ok = (__float_as_uint(mf) - 0x00800000u) < (0x7f800000u - 0x00800000u) && mid > kMidMargin + kMidAbove;
         m[i] = mf;
         slow |= ok ? 0u : (1u << i);
     }

@@ -4,7 +4,8 @@
 // 1/sqrt(x) is largest at one end of the low word's range, so both ends are
 // evaluated (in double-double via fma residuals).  Also: the worst distance,
 // in double ulps, between K1's one-step Newton sqrt (fft_mag.cu: mags) and
-// sqrt(q), over the same grid plus random low words.
+// sqrt(q), over the same grid plus random low words -- separately above and
+// below sqrt(q): the Newton step's error is -1.5 e^2 sqrt(q), one-sided.
 #include <cmath>
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -24,7 +25,7 @@ __device__ double rel_err(double x, double y) {
     return fma(y, s, -1.0) + y * r;
 }
 
-__device__ double newton_ulps(double q) {
+__device__ double newton_ulps(double q, double* above) {
     const double y = rsq64(q);
     const double s0 = __dmul_rn(q, y);
     const double d = __fma_rn(-s0, s0, q);
@@ -34,11 +35,12 @@ __device__ double newton_ulps(double q) {
     const double r = fma(-s, s, q) / (2.0 * s);    // sqrt(q) = s + r
     const double diff = (s1 - s) - r;              // s1 - sqrt(q); s1 - s is exact (close doubles)
     const double ulp = __longlong_as_double((__double_as_longlong(s) & 0x7ff0000000000000ll)) * 0x1p-52;
+    *above = fmax(*above, diff / ulp);
     return fabs(diff) / ulp;
 }
 
 __global__ void probe(double* out) {
-    double me = 0, mu = 0;
+    double me = 0, mu = 0, ma = -1e300;
     unsigned long long rng = 0x9E3779B97F4A7C15ull * (blockIdx.x * blockDim.x + threadIdx.x + 1);
     for (unsigned int hw = blockIdx.x * blockDim.x + threadIdx.x; hw < (2u << 20); hw += gridDim.x * blockDim.x) {
         const unsigned int hi = 0x3ff00000u + hw;  // [1,4): exponents 0x3ff, 0x400
@@ -46,31 +48,35 @@ __global__ void probe(double* out) {
         const double x1 = __hiloint2double(static_cast<int>(hi), static_cast<int>(0xffffffffu));
         const double y = rsq64(x0);
         me = fmax(me, fmax(fabs(rel_err(x0, y)), fabs(rel_err(x1, y))));
-        mu = fmax(mu, fmax(newton_ulps(x0), newton_ulps(x1)));
+        mu = fmax(mu, fmax(newton_ulps(x0, &ma), newton_ulps(x1, &ma)));
         for (int k = 0; k < 8; ++k) {
             rng = rng * 6364136223846793005ull + 1442695040888963407ull;
-            mu = fmax(mu, newton_ulps(__hiloint2double(static_cast<int>(hi), static_cast<int>(rng >> 32))));
+            mu = fmax(mu, newton_ulps(__hiloint2double(static_cast<int>(hi), static_cast<int>(rng >> 32)), &ma));
         }
     }
     for (int o = 16; o; o >>= 1) {
         me = fmax(me, __shfl_xor_sync(0xffffffffu, me, o));
         mu = fmax(mu, __shfl_xor_sync(0xffffffffu, mu, o));
+        ma = fmax(ma, __shfl_xor_sync(0xffffffffu, ma, o));
     }
     if ((threadIdx.x & 31) == 0) {
         atomicMax(reinterpret_cast<unsigned long long*>(out), static_cast<unsigned long long>(__double_as_longlong(me)));
         atomicMax(reinterpret_cast<unsigned long long*>(out + 1), static_cast<unsigned long long>(__double_as_longlong(mu)));
+        // ma may be negative: order by value through an offset
+        atomicMax(reinterpret_cast<unsigned long long*>(out + 2), static_cast<unsigned long long>(__double_as_longlong(ma + 1e6)));
     }
 }
 
 int main() {
     double* d;
-    cudaMalloc(&d, 16);
-    cudaMemset(d, 0, 16);
+    cudaMalloc(&d, 24);
+    cudaMemset(d, 0, 24);
     probe<<<1024, 256>>>(d);
-    double h[2];
-    if (cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost) != cudaSuccess) { printf("cuda error\n"); return 1; }
+    double h[3];
+    if (cudaMemcpy(h, d, 24, cudaMemcpyDeviceToHost) != cudaSuccess) { printf("cuda error\n"); return 1; }
     printf("rsqrt.approx.ftz.f64 on [1,4), every high word, both ends of the low word: max rel err %.6e (2^%.3f)\n", h[0], log2(h[0]));
     printf("one-step Newton sqrt (K1 mags) vs sqrt(q): max distance %.1f double ulps (2^%.3f); analytic 1.5 e^2 2^53 = %.1f\n",
            h[1], log2(h[1]), 1.5 * h[0] * h[0] * 0x1p53);
+    printf("largest s1 - sqrt(q): %+.3f double ulps (the estimate never exceeds sqrt(q) by more than its own rounding)\n", h[2] - 1e6);
     return 0;
 }
