@@ -384,23 +384,31 @@ __device__ __forceinline__ void mags(const cd* v, float* m) {
 #pragma unroll
     for (int i = 0; i < P; ++i) {
         const double q = __fma_rn(v[i].re, v[i].re, __dmul_rn(v[i].im, v[i].im));
+        // Newton step s1 = s0 + (q - s0^2) y/2, s0 = q y.  Only h = y/2 is kept
+        // (an exponent decrement of the seed, integer pipe) and s0 = 2 (q h) by
+        // an exponent increment: power-of-two scalings commute with the
+        // roundings, so s0 and s1 are the same doubles, with one register pair
+        // and two integer instructions less per point than holding y and h.
+        // (q = 0 or non-finite: the increments yield finite garbage or NaN,
+        // the float is not normal, and the point is flagged.)
         const double y = rsqrt_seed(q);
-        const double s0 = __dmul_rn(q, y);
-        const double d = __fma_rn(-s0, s0, q);
-        // y/2 by an exponent decrement (integer pipe): the FP64 pipe keeps only
-        // the 5 arithmetic ops
         const double h = __hiloint2double(__double2hiint(y) - (1 << 20), __double2loint(y));
+        const double w = __dmul_rn(q, h);
+        const double s0 = __hiloint2double(__double2hiint(w) + (1 << 20), __double2loint(w));
+        const double d = __fma_rn(-s0, s0, q);
         const double s1 = __fma_rn(d, h, s0);
         const uint32_t hi = static_cast<uint32_t>(__double2hiint(s1));
         const uint32_t lo = static_cast<uint32_t>(__double2loint(s1));
         // float rounding by F2F.F32.F64 (the conversion unit); 2^-SH as an
         // exponent decrement first
-        // dist = low 29 bits - 2^28 (ulps from the midpoint); flagged iff -margin <= dist <= above
-        const uint32_t mid = (lo & 0x1FFFFFFFu) + (kMidMargin - (1u << 28));
         const float mf = __double2float_rn(SH ? __hiloint2double(static_cast<int>(hi - (SH << 20)), static_cast<int>(lo)) : s1);
-        const bool ok = (__float_as_uint(mf) - 0x00800000u) < (0x7f800000u - 0x00800000u) && mid > kMidMargin + kMidAbove;
+        // dist = low 29 bits - 2^28 (ulps from the midpoint); flagged iff
+        // -margin <= dist <= above, tested on 8 * (low 29 bits) (one IMAD
+        // drops the three high bits and subtracts the window's start)
+        const uint32_t mid8 = lo * 8u - 8u * ((1u << 28) - kMidMargin);
+        const bool normal = __float_as_uint(mf) >= 0x00800000u && __float_as_uint(mf) < 0x7f800000u;
         m[i] = mf;
-        slow |= ok ? 0u : (1u << i);
+        if (!(normal && mid8 > 8u * (kMidMargin + kMidAbove) + 7u)) slow |= 1u << i;
     }
     if (__any_sync(0xffffffffu, slow != 0)) {
 #pragma unroll
@@ -636,7 +644,8 @@ fft_mag_kernel(FftArgs a) {
 #pragma unroll
                 for (int r = 0; r < RL; ++r) {
                     const int q = j + PL::TPR * u + r * NSL;
-                    const int k = (q + N / 2) & (N - 1);
+                    // j < TPR and every other term is a multiple of TPR: the DC shift is a constant offset
+                    const int k = j + ((q - j + N / 2) & (N - 1));
                     if (valid && out) out[k] = m[u * RL + r];
                 }
             }
@@ -670,7 +679,8 @@ fft_mag_kernel(FftArgs a) {
 #pragma unroll
                 for (int r = 0; r < RL; ++r) {
                     const int q = j + PL::TPR * u + r * NSL;
-                    const int k = (q + N / 2) & (N - 1);
+                    // j < TPR and every other term is a multiple of TPR: the DC shift is a constant offset
+                    const int k = j + ((q - j + N / 2) & (N - 1));
                     mrow[k] = m[u * RL + r];
                 }
             }
@@ -714,7 +724,8 @@ fft_mag_kernel(FftArgs a) {
                     for (int r = 0; r < RL; ++r) {
                         const int i = u * RL + r;
                         const int q = j + PL::TPR * u + r * NSL;
-                        const int k = (q + N / 2) & (N - 1);
+                        // j < TPR and every other term is a multiple of TPR: the DC shift is a constant offset
+                    const int k = j + ((q - j + N / 2) & (N - 1));
                         const double sum = __hiloint2double(static_cast<int>(t[2 * i + 1]), static_cast<int>(t[2 * i]));
                         psd[k] = __double2float_rn(__dmul_rn(sum, inv_rows));
                     }
@@ -726,7 +737,7 @@ fft_mag_kernel(FftArgs a) {
 #pragma unroll
                         for (int r = 0; r < RL; ++r) {
                             const int i = u * RL + r;
-                            const int k = (j + PL::TPR * u + r * NSL + N / 2) & (N - 1);
+                            const int k = j + ((PL::TPR * u + r * NSL + N / 2) & (N - 1));
                             a.col_lo[plot * N + k] = __uint_as_float(t[i]);
                             a.col_hi[plot * N + k] = __uint_as_float(t[16 + i]);
                         }
