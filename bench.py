@@ -55,9 +55,10 @@ class Workload:
         self.alg_bytes = self.stride * self.sb + self.rows * N_FFT * 4
         self.alg_flop64 = self.rows * 5 * N_FFT * 12                   # conventional 5 N log2 N per row
         # FP64 warp-instructions K1 executes per row and warp (ncu source view of
-        # fft_mag_kernel<12,0,1,0>): the SSFFT-2 work itself,
-        # counted for the default (rect, fp32) kernel only
-        self.k1_fp64_instr = 824 if (name == "c5r" and window == 0) else None
+        # fft_mag_kernel<12,0,1,0,0>: 809.5 = DADD 408 + DFMA
+        # 204.8 + DMUL 196.7): the SSFFT-2 work itself, counted for the default
+        # (rect, fp32) kernel only
+        self.k1_fp64_instr = 810 if (name == "c5r" and window == 0) else None
 
     def samples(self, plots):
         return plots * self.stride + self.tail
