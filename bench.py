@@ -468,7 +468,14 @@ def measure(args, wl, B, D, steps, warmup, e2e_batch, with_gather=True):
     e2e = None
     if Be:
         per = 2 if wl.i16 else 1
-        host_iq = torch.empty(per * wl.samples(Be), dtype=iq.dtype, pin_memory=True)
+        while True:  # N ranks pin N buffers on one host: shrink the e2e batch rather than fail
+            try:
+                host_iq = torch.empty(per * wl.samples(Be), dtype=iq.dtype, pin_memory=True)
+                break
+            except RuntimeError:
+                if Be == 1:
+                    raise
+                Be = max(1, Be // 2)
         host_iq.copy_(iq[: per * wl.samples(Be)])
         host_out = {k: torch.empty((Be,) + tuple(v.shape[1:]), dtype=v.dtype, pin_memory=True)
                     for k, v in outs.items()}
