@@ -143,3 +143,49 @@ def test_large_fft_int16_and_stft(ss, ref, ora):
     got = ss.stft_plots(x, 1e6, n_fft, 8192, 1, 5)
     exp = ora.stft_plot(x, n_fft, 8192, 1, 10).reshape(2, 5, n_fft)
     assert np.array_equal(got.view(np.uint32), exp.view(np.uint32))
+
+
+def _midpoint_cases(seed=11, n_mid=3000, span=13200):
+    """Float pairs (a, b) whose magnitude sqrt(a^2 + b^2) lies within `span`
+    double ulps of a float rounding midpoint, on both sides: a = the float half
+    an ulp below the midpoint m, b scanned ulp by ulp around sqrt(m^2 - a^2)
+    (one float ulp of b moves the magnitude by ~45 double ulps)."""
+    rng = np.random.default_rng(seed)
+    mant = rng.integers(1 << 23, 1 << 24, n_mid).astype(np.float64)
+    expo = rng.choice(np.array([-60, -20, -3, 0, 1, 7, 30, 60]), n_mid).astype(np.float64)
+    hu = np.ldexp(0.5, (expo - 23).astype(np.int64))           # half a float ulp
+    m = np.ldexp(mant, (expo - 23).astype(np.int64)) + hu       # midpoint (25 significant bits)
+    a = (m - hu).astype(np.float32)
+    b0 = np.sqrt(hu * (2.0 * m - hu)).astype(np.float32)
+    k = np.arange(-320, 321, dtype=np.int32)
+    bb = (b0.view(np.int32)[:, None] + k[None, :]).view(np.float32)   # b0 +- k float ulps
+    aa = np.broadcast_to(a[:, None], bb.shape)
+    a64, b64 = aa.astype(np.float64), bb.astype(np.float64)
+    q = a64 * a64 + b64 * b64                 # both squares exact: one rounding, = fma(re, re, im*im)
+    s = np.sqrt(q)
+    dist = (s.view(np.uint64) & np.uint64(0x1FFFFFFF)).astype(np.int64) - (1 << 28)
+    keep = np.abs(dist) <= span
+    return aa[keep], bb[keep], s[keep].astype(np.float32), dist[keep]
+
+
+def test_magnitudes_around_float_midpoints(ss, ref):
+    """K1's magnitude rounds a one-step Newton square root to float and redoes,
+    with the IEEE square root, the points whose estimate lies in [-12288, +4]
+    double ulps of a float rounding midpoint (fft_mag.cu: mags).  An impulse
+    x[0] = a + ib transforms to X[k] = a + ib in every bin (n_fft = 8), so
+    |X| = sqrt(a^2 + b^2) for chosen floats: ~1.7M magnitudes within 13,200 ulps
+    of a midpoint, both sides, window edges included, against numpy's correctly
+    rounded sqrt and against the reference.  (A build with a 1,024-ulp window
+    fails this test; the proven 12,288-ulp window passes.)"""
+    a, b, want, dist = _midpoint_cases()
+    assert a.size > 500_000
+    # the sample brackets the window: inside, at its edges, and just outside
+    for lo, hi in [(-12288, 4), (-12400, -12200), (-13200, -12300), (-8, 16), (100, 13200)]:
+        assert np.count_nonzero((dist >= lo) & (dist <= hi)) > 500, (lo, hi)
+    n = a.size
+    x = np.zeros((n, 8), np.complex64)
+    x[:, 0] = a + 1j * b
+    got = ss.make_plots(x.reshape(-1), 1e6, 8, n)[0]
+    assert np.array_equal(got.view(np.uint32), np.broadcast_to(want.view(np.uint32)[:, None], got.shape))
+    exp = ref.make_plots(x.reshape(-1), 1e6, 8, n)[0]
+    assert np.array_equal(got.view(np.uint32), exp.view(np.uint32))
