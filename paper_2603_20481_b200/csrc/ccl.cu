@@ -325,8 +325,14 @@ __device__ __forceinline__ void sm_unite(int* par, int a, int b) {
 // first row) are joined to the row above by union_boundary_kernel afterwards.
 // Launched for every plot, one row included (rows == 1: each run alone).
 constexpr int kUB = 16;  // 16 beat 32 (0.78 ms per C5r step) and 64 (1.02)
-constexpr int kUCap = 1024;
-constexpr int kUThreads = 256;  // 256 beat 128 (0.72 ms per C5r step), 64 (0.96), 32 (1.27)
+#ifndef K6_UCAP
+#define K6_UCAP 1024
+#endif
+constexpr int kUCap = K6_UCAP;
+#ifndef K6_UTHREADS
+#define K6_UTHREADS 256
+#endif
+constexpr int kUThreads = K6_UTHREADS;  // warp-per-row-pair form: 256 beat 128 (0.72 ms per C5r step), 64 (0.96), 32 (1.27)
 
 __global__ void __launch_bounds__(kUThreads) union_block_kernel(int rows, const int* row_off, const long long* plot_base,
                                                           const int* plot_ok, CclWorkspace ws) {
@@ -365,32 +371,40 @@ __global__ void __launch_bounds__(kUThreads) union_block_kernel(int rows, const 
     }
     for (int j = threadIdx.x; j <= r1 - r0; j += blockDim.x) roff[j] = off[r0 + j] - g0;
     __syncthreads();
-    // one warp per row pair (j-1, j), lanes over row j's runs
-    for (int j = 1 + (threadIdx.x >> 5); j < r1 - r0; j += blockDim.x >> 5) {
-        const int pb = roff[j - 1], cb = roff[j], ce = roff[j + 1];
-        for (int i = cb + lane; i < ce; i += 32) {
-            const int b = sb[i], e = se[i];
-            int lo = pb, hi = cb;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (se[mid] > b) hi = mid;
-                else lo = mid + 1;
-            }
-            for (int q = lo; q < cb && sb[q] < e; ++q) sm_unite(sp, i, q);
+    // one thread per run (a block holds ~70 runs on a C5r plot: a warp per row
+    // pair left most lanes idle and walked the pairs in turn); the run's row
+    // is the last j with roff[j] <= i
+    auto row_of = [&](int i) {
+        int lo = 0, hi = r1 - r0 - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (roff[mid] <= i) lo = mid;
+            else hi = mid - 1;
         }
+        return lo;
+    };
+    for (int i = roff[1] + threadIdx.x; i < n; i += blockDim.x) {
+        const int j = row_of(i);
+        const int pb = roff[j - 1], cb = roff[j];
+        const int b = sb[i], e = se[i];
+        int lo = pb, hi = cb;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (se[mid] > b) hi = mid;
+            else lo = mid + 1;
+        }
+        for (int q = lo; q < cb && sb[q] < e; ++q) sm_unite(sp, i, q);
     }
     __syncthreads();
-    // parents and block-local statistics; one warp per row (the row is the run's)
-    for (int j = threadIdx.x >> 5; j < r1 - r0; j += blockDim.x >> 5) {
-        for (int i = roff[j] + lane; i < roff[j + 1]; i += 32) {
-            int x = i;
-            while (sp[x] != x) x = sp[x];
-            ws.parent[gb + i] = static_cast<int>(gb + x);
-            atomicAdd(&s_area[x], se[i] - sb[i]);
-            atomicMax(&s_maxt[x], r0 + j);
-            atomicMin(&s_minf[x], sb[i]);
-            atomicMax(&s_maxf[x], se[i] - 1);
-        }
+    // parents and block-local statistics
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        int x = i;
+        while (sp[x] != x) x = sp[x];
+        ws.parent[gb + i] = static_cast<int>(gb + x);
+        atomicAdd(&s_area[x], se[i] - sb[i]);
+        atomicMax(&s_maxt[x], r0 + row_of(i));
+        atomicMin(&s_minf[x], sb[i]);
+        atomicMax(&s_maxf[x], se[i] - 1);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
