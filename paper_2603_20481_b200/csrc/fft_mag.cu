@@ -457,7 +457,11 @@ struct K1Shape {
     static constexpr int TMEM_COLS = WARPS <= 4 ? 32 : WARPS <= 8 ? 64 : WARPS <= 16 ? 128 : 256;
     // column extremes (fminf / fmaxf of the plot's magnitudes, for K4) in a
     // second block of TMEM_COLS columns: 16 minima + 16 maxima per thread
-    __host__ __device__ static constexpr int tmem_alloc_cols(bool ext) { return ext ? 2 * TMEM_COLS : TMEM_COLS; }
+    // blocks of TMEM_COLS columns: PSD sums, [column extremes], [window weights]; the allocation is a power of two
+    __host__ __device__ static constexpr int tmem_alloc_cols(bool ext, bool wint = false) {
+        const int nb = 1 + (ext ? 1 : 0) + (wint ? 1 : 0);
+        return (nb == 1 ? 1 : nb == 2 ? 2 : 4) * TMEM_COLS;
+    }
     static_assert(!ACC_TMEM || PL::P == 16, "one 32-column TMEM slot holds 16 double accumulators");
     __host__ __device__ static constexpr size_t tw_bytes() { return TW_SMEM ? sizeof(double2) * (PL::tw_size() > 0 ? PL::tw_size() : 1) : 0; }
     __host__ __device__ static constexpr size_t group_bytes(int sample_bytes) {
@@ -475,6 +479,11 @@ fft_mag_kernel(FftArgs a) {
     constexpr int N = PL::N;
     constexpr int G = PL::G;
     constexpr int SAMPLE_BYTES = FMT == 0 ? 8 : 4;
+    // STFT window weights of this thread's 16 samples (the same every row) in a
+    // third block of TMEM columns: one tcgen05.ld per row, issued ahead of the
+    // stage wait, instead of 16 L1 loads at the start of the row
+    constexpr bool WINT = WIN && PSD && KS::ACC_TMEM && PL::radix(0) == 16 && PL::P == 16;
+    constexpr int WOFF = KS::TMEM_COLS * (EXT ? 2 : 1);
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bars[KS::GROUPS];
 
@@ -532,7 +541,7 @@ fft_mag_kernel(FftArgs a) {
     __shared__ uint32_t tmem_slot;
     const int wid = static_cast<int>(threadIdx.x) >> 5;
     if constexpr (PSD && KS::ACC_TMEM) {
-        if (wid == 0) tmem_alloc<KS::tmem_alloc_cols(EXT)>(&tmem_slot);
+        if (wid == 0) tmem_alloc<KS::tmem_alloc_cols(EXT, WINT)>(&tmem_slot);
         tmem_fence_before();
     }
     __syncthreads();  // twiddle copy + mbarrier init (+ TMEM address) visible to all groups
@@ -552,6 +561,17 @@ fft_mag_kernel(FftArgs a) {
                 ext[16 + i] = 0xff800000u;  // -inf: maxima
             }
             tmem_st32(taddr + KS::TMEM_COLS, ext);
+        }
+        if constexpr (WINT) {
+            uint32_t wb[32];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const double w = __ldg(a.win + j + r * (N / 16));
+                wb[2 * r] = static_cast<uint32_t>(__double2loint(w));
+                wb[2 * r + 1] = static_cast<uint32_t>(__double2hiint(w));
+            }
+            tmem_st32(taddr + WOFF, wb);
+            tmem_wait_st();
         }
     }
     if (lt == 0 && it_begin < it_end) {
@@ -574,8 +594,11 @@ fft_mag_kernel(FftArgs a) {
         const long long row = r0 + g;
         const bool valid = G == 1 || row < row_limit;  // G == 1: the iteration space is exactly the rows
 
+        uint32_t wb[WINT ? 32 : 1];
+        if constexpr (WINT) tmem_ld32(taddr + WOFF, wb);
         mbar_wait(bar, phase);
         phase ^= 1;
+        if constexpr (WINT) tmem_wait_ld();
 
         // pass-0 inputs from the stage
         cd v[16];
@@ -611,7 +634,8 @@ fft_mag_kernel(FftArgs a) {
                         v[u * R0 + r] = {static_cast<double>(x.x), static_cast<double>(x.y)};
                     }
                     if constexpr (WIN) {  // STFT extension: one rounded product per component
-                        const double w = __ldg(a.win + n);
+                        const double w = WINT ? __hiloint2double(static_cast<int>(wb[WINT ? 2 * r + 1 : 0]), static_cast<int>(wb[WINT ? 2 * r : 0]))
+                                              : __ldg(a.win + n);
                         v[u * R0 + r] = {__dmul_rn(v[u * R0 + r].re, w), __dmul_rn(v[u * R0 + r].im, w)};
                     }
                 }
@@ -755,7 +779,7 @@ fft_mag_kernel(FftArgs a) {
             tmem_fence_before();
             __syncthreads();  // every warp is done with its columns
             tmem_fence_after();
-            if (wid == 0) tmem_dealloc<KS::tmem_alloc_cols(EXT)>(tmem_slot);
+            if (wid == 0) tmem_dealloc<KS::tmem_alloc_cols(EXT, WINT)>(tmem_slot);
         }
     }
 }
